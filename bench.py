@@ -1,0 +1,405 @@
+"""Benchmark of the Winograd layer hot path (BASELINE.json metric:
+"Winograd conv direct-equiv TFLOP/s").
+
+Default workload = BASELINE.json configs[1]: F(2x2, 3x3), points {0,1,-1,inf},
+fp32 throughout (huffman transforms, linear channel sum, exact contraction),
+N=32 per GPU, C=K=128, H=W=28, pad 1, x ~ U[-1,1], w ~ He-normal, seeded.
+A step = filter transform + input transform + channel contraction + output
+transform of one batch (the four libwino kernels, inputs resident in HBM).
+Multi-GPU: one process per GPU, each rank runs its own batch (global image
+indices rank*N .. rank*N+N-1) -> weak scaling; NCCL only reduces timings and
+error statistics.  `--impl reference` times the CPU port of the reference's
+arithmetic (oracle/) on the host cores for the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Winograd conv direct-equiv TFLOP/s"
+
+CONFIGS = {
+    # name: (r, m, points, N, C, K, H, pad, x_dist, w_init, precision, dot_order, channel_sum)
+    "cfg2": (3, 2, "0,1,-1,inf", 32, 128, 128, 28, 1, "uniform", "he", "fp32", "huffman", "linear"),
+    "cfg1": (3, 4, "0,1,-1,1/2,-1/2,inf", 8, 64, 64, 56, 1, "uniform", "uniform", "fp32", "huffman", "linear"),
+    "cfg3_m6": (3, 6, "0,-1,1,1/2,-1/2,2,-2,inf", 64, 256, 256, 28, 1, "uniform", "he", "fp32", "huffman",
+                "linear"),
+    "cfg3_m6_mixed_pw": (3, 6, "0,-1,1,1/2,-1/2,2,-2,inf", 64, 256, 256, 28, 1, "uniform", "he", "mixed",
+                         "huffman", "pairwise"),
+    "cfg4_m4": (5, 4, "0,-1,1,1/2,-1/2,2,-2,inf", 32, 512, 512, 14, 2, "uniform01", "he", "fp32", "huffman",
+                "pairwise"),
+    "vgg_l5": (3, 6, "0,-1,1,1/2,-1/2,2,-2,inf", 256, 128, 256, 56, 1, "uniform", "he", "fp32", "huffman",
+               "pairwise"),
+}
+
+
+def synth(shape, seed, idx, dist):
+    g = np.random.Generator(np.random.Philox(key=np.array([seed, idx], dtype=np.uint64)))
+    if dist == "uniform":
+        return g.random(shape, dtype=np.float32) * np.float32(2) - np.float32(1)
+    if dist == "uniform01":
+        return g.random(shape, dtype=np.float32)
+    return g.standard_normal(shape, dtype=np.float32)
+
+
+def make_inputs(cfg, rank, seed=2024):
+    r, m, pts, N, C, K, H, pad, xd, wi = cfg[:10]
+    x = np.stack([synth((C, H, H), seed, rank * N + i, xd) for i in range(N)])
+    if wi == "he":
+        w = synth((K, C, r, r), seed, 10_000_000, "normal") * np.float32(np.sqrt(2.0 / (r * r * C)))
+    else:
+        w = synth((K, C, r, r), seed, 10_000_000, "uniform")
+    return np.ascontiguousarray(x), np.ascontiguousarray(w.astype(np.float32))
+
+
+def direct_flops(cfg):
+    r, m, pts, N, C, K, H, pad = cfg[:8]
+    Ho = H + 2 * pad - r + 1
+    return 2 * N * K * C * Ho * Ho * r * r
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.samples, self._stop = index, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.samples.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------- CPU side
+_CPU = {}
+
+
+def _cpu_worker(span):
+    from oracle import wino_oracle as O
+    i0, i1 = span
+    c = _CPU
+    return O.layer_conv2d(c["trip"], c["x"][i0:i1], c["w"], c["pad"], c["prec"], c["order"], c["cs"])
+
+
+def cpu_layer_time(cfg, x, w, procs):
+    """Time the oracle port (the reference's arithmetic on numpy) over images
+    x with `procs` worker processes; returns seconds."""
+    from concurrent.futures import ProcessPoolExecutor
+    import multiprocessing as mp
+    from oracle import wino_oracle as O
+    r, m, pts, N, C, K, H, pad = cfg[:8]
+    _CPU.update(trip=O.Triple.from_points(r, m, pts), x=x, w=w, pad=pad, prec=cfg[10], order=cfg[11], cs=cfg[12])
+    n = x.shape[0]
+    spans = [(i * n // procs, (i + 1) * n // procs) for i in range(procs)]
+    spans = [s for s in spans if s[1] > s[0]]
+    ctx = mp.get_context("fork")
+    with ProcessPoolExecutor(max_workers=len(spans), mp_context=ctx) as ex:
+        list(ex.map(_cpu_worker, [(0, 1)] * len(spans)))  # warm the workers
+        t0 = time.perf_counter()
+        list(ex.map(_cpu_worker, spans))
+        return time.perf_counter() - t0
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    x, w = make_inputs(cfg, 0)
+    procs = min(host_cores(), x.shape[0])
+    times = []
+    for i in range(args.warmup + args.steps):
+        t = cpu_layer_time(cfg, x, w, procs)
+        if i >= args.warmup:
+            times.append(t)
+    ms = 1e3 * float(np.mean(times))
+    val = direct_flops(cfg) / (ms * 1e-3) / 1e12
+    line = {"metric": METRIC, "value": val, "unit": "TFLOP/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if cfg[10] == "fp32" else "f32/f64",
+            "data": "synthetic (seeded Philox U[-1,1] inputs, He-normal filters)",
+            "config": config_dict(args, cfg),
+            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": procs, "kind": "port",
+                             "sample": f"full batch of {x.shape[0]} images per step, oracle/wino_oracle.py "
+                                       f"layer_conv2d (numpy restatement of the reference) over {procs} processes"},
+            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args, cfg, world=1):
+    r, m, pts, N, C, K, H, pad, xd, wi, prec, order, cs = cfg
+    return {"workload": args.config, "winograd": f"F({m}x{m},{r}x{r})", "points": pts, "N_per_gpu": N,
+            "global_batch": N * world, "C": C, "K": K, "H": H, "W": H, "pad": pad, "precision": prec,
+            "dot_order": order, "channel_sum": cs, "contraction": args.contraction,
+            "x_dist": xd, "w_init": wi, "l2": "flushed between timed steps (256 MiB write)",
+            "parallelism": f"dp{world} (independent batches per GPU)"}
+
+
+# --------------------------------------------------------------------- GPU side
+def run_gpu(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1803_10986_b200 as W
+    from paper_1803_10986_b200 import _native
+
+    r, m, pts, N, C, K, H, pad, xd, wi, prec, order, cs = cfg
+    ts = W.build_transforms(r, m, W.parse_points(pts))
+    wcfg = W.ConvConfig(prec, order, cs)
+    op = W.layer_op(ts, wcfg, N, C, H, H, K, pad, args.contraction)
+    L = op.layout
+    x_np, w_np = make_inputs(cfg, rank)
+    x = torch.from_numpy(x_np).cuda()
+    w = torch.from_numpy(w_np).cuda()
+    y = torch.empty(op.out_shape, dtype=torch.float32 if prec == "fp32" else torch.float64, device="cuda")
+    uvdt = torch.float64 if prec == "fp64" else torch.float32
+    U = torch.empty((L.P, L.Cp, L.Kp), dtype=uvdt, device="cuda")
+    V = torch.empty((L.P, L.Cp, L.Tp), dtype=uvdt, device="cuda")
+    M = torch.empty((L.P, L.Kp, L.Tp), dtype=uvdt, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    lib = _native.lib()
+    shp = op.shape
+    import ctypes
+    sref = ctypes.byref(shp)
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        _native.check(lib.wino_filter_transform(op.plan.handle, sref, _native.as_ptr(w), _native.as_ptr(U), sh))
+        if ev is not None:
+            ev[1].record(stream)
+        _native.check(lib.wino_input_transform(op.plan.handle, sref, _native.as_ptr(x), _native.as_ptr(V), sh))
+        if ev is not None:
+            ev[2].record(stream)
+        _native.check(lib.wino_contract(op.plan.handle, sref, _native.as_ptr(U), _native.as_ptr(V),
+                                        _native.as_ptr(M), sh))
+        if ev is not None:
+            ev[3].record(stream)
+        _native.check(lib.wino_output_transform(op.plan.handle, sref, _native.as_ptr(M), _native.as_ptr(y), sh))
+        if ev is not None:
+            ev[4].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    n0 = _native.launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # evict L2 (outside the timed interval of the step)
+            step(evs[i])
+        torch.cuda.synchronize()
+    n_launch = _native.launch_count() - n0
+    if world > 1:
+        dist.barrier()
+    stage = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(4)] for i in range(args.steps)])
+    ms_step = float(stage.sum(axis=1).mean())
+    ms_stage = stage.mean(axis=0)
+    if world > 1:
+        t = torch.tensor([ms_step], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    value = direct_flops(cfg) * world / (ms_step * 1e-3) / 1e12
+
+    # ---- end to end through the public API: pinned host in, pinned host out
+    xh = torch.from_numpy(x_np).pin_memory()
+    wh = torch.from_numpy(w_np).pin_memory()
+    yh = torch.empty(op.out_shape, dtype=y.dtype).pin_memory()
+    xd_, wd_ = torch.empty_like(x), torch.empty_like(w)
+
+    def e2e_step():
+        xd_.copy_(xh, non_blocking=True)
+        wd_.copy_(wh, non_blocking=True)
+        out = op(xd_, wd_, out=y)
+        yh.copy_(out, non_blocking=True)
+
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0.record(stream)
+        e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    e2e_t = float(np.mean(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    e2e_val = direct_flops(cfg) * world / (e2e_t * 1e-3) / 1e12
+
+    # ---- error vs fp64 direct (device oracle kernel), per-image partials gathered in image order
+    y_ref = op(x, w)
+    y64 = W.direct_layer_f64(x, w, pad)
+    st = W.layer_error_stats(y_ref, y64)
+    if world > 1:
+        allst = [torch.empty_like(st) for _ in range(world)]
+        dist.all_gather(allst, st)
+        st = torch.cat(allst)
+    st = st.cpu().numpy()
+    err = {"rel_l1": float(st[:, 0].sum() / st[:, 1].sum()), "per_point_l1": float(st[:, 0].sum() / st[:, 2].sum()),
+           "max_abs": float(st[:, 3].max()), "images": int(st.shape[0]), "reference": "fp64 direct (device kernel)"}
+
+    # ---- roofline of the dominant kernel (the contraction: FP32 CUDA-core bound)
+    peak = measure_peaks(lib, _native, torch)
+    flops_c = 2 * L.P * L.T * C * K
+    ach = flops_c / (ms_stage[2] * 1e-3) / 1e12
+    exact = args.contraction == "exact"
+    pk = peak["ffma_tflops"]
+    roof = {"kernel": "wino_contract", "bound": "fp32", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+            "frac": ach / pk, "traffic": None,
+            "peak_source": "measured in this run: libwino wino_peak_probe FFMA (8 chains x 148*8 CTAs)",
+            "exact_ceiling_tflops": peak["fmul_fadd_tflops"] if exact else None,
+            "frac_of_exact_ceiling": ach / peak["fmul_fadd_tflops"] if exact else None,
+            "flops_per_launch": flops_c, "share_of_step": float(ms_stage[2] / ms_stage.sum())}
+    hbm = 6553.9
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            hbm = json.load(fh)["hbm_gbs"]
+    except Exception:
+        pass
+    eb = L.elem_bytes_uv
+    stage_bytes = [4 * K * C * r * r + eb * L.P * C * K,
+                   4 * N * C * H * H + eb * L.P * L.T * C,
+                   None,
+                   eb * L.P * L.T * K + (4 if prec == "fp32" else 8) * N * K * L.Ho * L.Wo]
+    stages = {}
+    for j, name in enumerate(["filter_transform", "input_transform", "contract", "output_transform"]):
+        d = {"ms": float(ms_stage[j])}
+        if stage_bytes[j] is not None:
+            d["gbs"] = stage_bytes[j] / (ms_stage[j] * 1e-3) / 1e9
+            d["frac_hbm"] = d["gbs"] / hbm
+        else:
+            d["tflops"] = ach
+        stages[name] = d
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32" if prec == "fp32" else "f32/f64",
+                "data": "synthetic (seeded Philox U[-1,1] inputs, He-normal filters)",
+                "config": config_dict(args, cfg, world), "roofline": roof, "stages": stages,
+                "error_vs_fp64": err,
+                "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": x_np.nbytes + w_np.nbytes,
+                        "d2h_bytes_per_step": yh.numel() * yh.element_size(), "ms_per_step": e2e_t},
+                "gpu_launches": int(n_launch), "clocks": clk.summary(), "peaks": peak}
+        if world == 1 and not args.no_cpu:
+            xs = x_np[: args.cpu_images]
+            procs = min(host_cores(), xs.shape[0])
+            t = cpu_layer_time(cfg, xs, w_np, procs)
+            fl = direct_flops(cfg) * xs.shape[0] / N
+            line["cpu_baseline"] = {"value": fl / t / 1e12, "unit": "TFLOP/s", "cores": procs, "kind": "port",
+                                    "sample": f"{xs.shape[0]} of {N} images of the same layer, oracle/wino_oracle.py "
+                                              f"layer_conv2d over {procs} processes, {t:.2f} s"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def measure_peaks(lib, _native, torch):
+    import ctypes
+    out = torch.zeros(4, dtype=torch.float32, device="cuda")
+    sm = torch.cuda.get_device_properties(0).multi_processor_count
+    blocks, iters = sm * 8, 4096
+    res = {}
+    for mode, name in ((0, "ffma_tflops"), (1, "fmul_fadd_tflops"), (2, "dfma_tflops"), (3, "dmul_dadd_tflops")):
+        it = iters if mode < 2 else iters // 8
+        for _ in range(2):
+            _native.check(lib.wino_peak_probe(mode, blocks, it, ctypes.c_void_p(out.data_ptr()),
+                                              torch.cuda.current_stream().cuda_stream))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _native.check(lib.wino_peak_probe(mode, blocks, it, ctypes.c_void_p(out.data_ptr()),
+                                          torch.cuda.current_stream().cuda_stream))
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        # FFMA / DFMA step = 2 flops; FMUL+FADD step = 2 flops (one mul, one add)
+        res[name] = blocks * 256 * 8 * it * 2 / (ms * 1e-3) / 1e12
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--contraction", default="exact", choices=["exact", "ffma"])
+    ap.add_argument("--cpu-images", type=int, default=32)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_gpu(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

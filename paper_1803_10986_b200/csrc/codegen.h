@@ -1,0 +1,44 @@
+// CUDA source generation for the transform kernels of one transform triple.
+//
+// Each matrix row is a postfix program (wino_op).  The emitter turns it into
+// straight-line SSA code with explicit round-to-nearest intrinsics
+// (__fmul_rn/__fadd_rn/__fsub_rn or their f64 forms) so that every product and
+// every sum rounds exactly once, exactly as the reference's numpy evaluation
+// (engine.py:191-232).  Exact rewrites only:
+//   * coefficient +1: the operand itself (1*x == x);
+//   * coefficient -1: a pending negation, folded into the consuming add as a
+//     subtraction (a + (-1*x) == a - x bit for bit; (-x) + (-y) == (-x) - y);
+//   * a row with no nonzero coefficient yields +0 (np.zeros_like).
+#pragma once
+#include <string>
+#include <vector>
+
+#include "../../include/wino.h"
+
+namespace wino {
+
+struct RowProg {
+    std::vector<wino_op> ops;
+};
+
+struct MatProg {
+    int rows = 0, cols = 0;
+    std::vector<RowProg> row;
+};
+
+struct GenTypes {
+    bool compute_double;  // transform arithmetic type
+    bool in_double;       // layer / tile inputs (x, w, h)
+    bool uv_double;       // U, V, M, z (working precision of the Hadamard stage)
+    bool y_double;        // outputs
+};
+
+// validate the stack discipline of a program; returns "" or an error message
+std::string validate(const MatProg& m, int expect_rows, int expect_cols, const char* name);
+
+std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
+                             const GenTypes& ty);
+std::string gen_tile_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
+                            const GenTypes& ty);
+
+}  // namespace wino

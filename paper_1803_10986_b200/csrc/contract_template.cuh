@@ -1,0 +1,257 @@
+// Channel-contraction kernel template (K3), JIT-compiled by NVRTC for sm_100a.
+//
+//   M_p[k][t] = sum_c U_p[c][k] * V_p[c][t]   for every Winograd point p < P
+//
+// which is the Hadamard product + channel reduction of the reference
+// (engine.py:415 `u * v`, engine.py:252-278 `_reduce_linear/_reduce_pairwise`,
+// engine.py:336-338 `channel_reduce`) batched over all (k, tile) pairs.
+//
+// The host prepends #defines:
+//   WINO_DT       float | double
+//   WINO_TM/TN    per-thread microtile (rows k / columns t), multiples of the
+//                 16-byte vector width
+//   WINO_THM/THN  thread grid of the CTA; BM = THM*TM, BN = THN*TN
+//   WINO_BK       channels per pipeline stage (multiple of 8)
+//   WINO_STAGES   smem ring depth
+//   WINO_SUM      0 exact-linear, 1 exact-pairwise, 2 ffma-linear, 3 ffma-pairwise
+//   WINO_LEVELS   pairwise: slots of the chunk-level binary counter
+//
+// Summation order (exact modes, bitwise equal to the reference):
+//   linear   : acc = -0; acc = acc + fl(u*v) for c = 0, 1, ...  (-0 + z = z exactly)
+//   pairwise : the reference's halving tree == a binary counter over the
+//              products in c order: aligned blocks of 8 are summed as a perfect
+//              tree in registers, block sums are pushed into a counter whose
+//              slot j holds a block of 2^j chunks; the final fold adds the
+//              occupied slots from the smallest block upwards.
+// Padded channels (c >= C) carry -0 products and leave every sum unchanged.
+//
+// Data movement: one thread issues cp.async.bulk (TMA bulk copies, SASS UBLKCP)
+// of every BM- and BN-wide channel row of a stage into shared memory, tracked by
+// an mbarrier per stage (complete_tx); the CTA consumes stage s while the next
+// WINO_STAGES-1 stages are in flight.
+
+#define DT WINO_DT
+#define BM (WINO_THM * WINO_TM)
+#define BN (WINO_THN * WINO_TN)
+#define NTHR (WINO_THM * WINO_THN)
+#define VW (16 / (int)sizeof(DT))
+#define GM (WINO_TM / VW)
+#define GN (WINO_TN / VW)
+
+typedef unsigned long long u64;
+
+#if WINO_DT_IS_DOUBLE
+#define XMUL(a, b) __dmul_rn((a), (b))
+#define XADD(a, b) __dadd_rn((a), (b))
+#define XFMA(a, b, c) __fma_rn((a), (b), (c))
+typedef double2 vec_t;
+#else
+#define XMUL(a, b) __fmul_rn((a), (b))
+#define XADD(a, b) __fadd_rn((a), (b))
+#define XFMA(a, b, c) __fmaf_rn((a), (b), (c))
+typedef float4 vec_t;
+#endif
+
+static __device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+static __device__ __forceinline__ void mbar_init(u64* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+static __device__ __forceinline__ void mbar_expect_tx(u64* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+static __device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WINO_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WINO_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+static __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, u64* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+extern "C" __global__ void __launch_bounds__(NTHR) wino_contract(const DT* __restrict__ U,
+                                                               const DT* __restrict__ V,
+                                                               DT* __restrict__ M, long long Kp,
+                                                               long long Tp, long long Cp) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    DT* sU = reinterpret_cast<DT*>(smem_raw);      // [STAGES][BK][BM]
+    DT* sV = sU + WINO_STAGES * WINO_BK * BM;      // [STAGES][BK][BN]
+    u64* bar = reinterpret_cast<u64*>(sV + WINO_STAGES * WINO_BK * BN);
+
+    const int tid = threadIdx.x;
+    const int tn = tid % WINO_THN;
+    const int tm = tid / WINO_THN;
+    const long long p = blockIdx.z;
+    const long long k0 = (long long)blockIdx.y * BM;
+    const long long t0 = (long long)blockIdx.x * BN;
+    const DT* gU = U + p * Cp * Kp + k0;
+    const DT* gV = V + p * Cp * Tp + t0;
+    const int nk = (int)(Cp / WINO_BK);
+
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < WINO_STAGES; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto issue = [&](int kt) {
+        const int s = kt % WINO_STAGES;
+        mbar_expect_tx(&bar[s], (unsigned)(WINO_BK * (BM + BN) * sizeof(DT)));
+#pragma unroll 1
+        for (int r = 0; r < WINO_BK; ++r) {
+            const long long c = (long long)kt * WINO_BK + r;
+            bulk_g2s(sU + (s * WINO_BK + r) * BM, gU + c * Kp, BM * sizeof(DT), &bar[s]);
+            bulk_g2s(sV + (s * WINO_BK + r) * BN, gV + c * Tp, BN * sizeof(DT), &bar[s]);
+        }
+    };
+    if (tid == 0) {
+        for (int kt = 0; kt < WINO_STAGES - 1 && kt < nk; ++kt) issue(kt);
+    }
+
+#if WINO_SUM == 0
+    DT acc[WINO_TM][WINO_TN];
+#pragma unroll
+    for (int i = 0; i < WINO_TM; ++i)
+#pragma unroll
+        for (int j = 0; j < WINO_TN; ++j) acc[i][j] = (DT)(-0.0);
+#elif WINO_SUM == 2
+    DT acc[WINO_TM][WINO_TN];
+#pragma unroll
+    for (int i = 0; i < WINO_TM; ++i)
+#pragma unroll
+        for (int j = 0; j < WINO_TN; ++j) acc[i][j] = (DT)0;
+#else
+    DT pa[WINO_TM][WINO_TN];
+#if WINO_SUM == 1
+    DT pb[WINO_TM][WINO_TN], pd[WINO_TM][WINO_TN];
+#endif
+    DT slot[WINO_LEVELS][WINO_TM][WINO_TN];
+#endif
+
+#pragma unroll 1
+    for (int kt = 0; kt < nk; ++kt) {
+        __syncthreads();  // every thread is done with the stage refilled below
+        if (tid == 0 && kt + WINO_STAGES - 1 < nk) issue(kt + WINO_STAGES - 1);
+        const int s = kt % WINO_STAGES;
+        mbar_wait(&bar[s], (unsigned)((kt / WINO_STAGES) & 1));
+        const DT* cu = sU + s * WINO_BK * BM;
+        const DT* cv = sV + s * WINO_BK * BN;
+#pragma unroll
+        for (int kk = 0; kk < WINO_BK; ++kk) {
+            DT a[WINO_TM], b[WINO_TN];
+#pragma unroll
+            for (int g = 0; g < GM; ++g) {
+                vec_t q = *reinterpret_cast<const vec_t*>(cu + kk * BM + g * (WINO_THM * VW) + tm * VW);
+                const DT* qq = reinterpret_cast<const DT*>(&q);
+#pragma unroll
+                for (int v = 0; v < VW; ++v) a[g * VW + v] = qq[v];
+            }
+#pragma unroll
+            for (int g = 0; g < GN; ++g) {
+                vec_t q = *reinterpret_cast<const vec_t*>(cv + kk * BN + g * (WINO_THN * VW) + tn * VW);
+                const DT* qq = reinterpret_cast<const DT*>(&q);
+#pragma unroll
+                for (int v = 0; v < VW; ++v) b[g * VW + v] = qq[v];
+            }
+#if WINO_SUM == 0
+#pragma unroll
+            for (int i = 0; i < WINO_TM; ++i)
+#pragma unroll
+                for (int j = 0; j < WINO_TN; ++j) acc[i][j] = XADD(acc[i][j], XMUL(a[i], b[j]));
+#elif WINO_SUM == 2
+#pragma unroll
+            for (int i = 0; i < WINO_TM; ++i)
+#pragma unroll
+                for (int j = 0; j < WINO_TN; ++j) acc[i][j] = XFMA(a[i], b[j], acc[i][j]);
+#else
+            const int pos = kk & 7;  // compile-time after unrolling
+#pragma unroll
+            for (int i = 0; i < WINO_TM; ++i)
+#pragma unroll
+                for (int j = 0; j < WINO_TN; ++j) {
+#if WINO_SUM == 1
+                    const DT z = XMUL(a[i], b[j]);
+                    if (pos == 0) pa[i][j] = z;
+                    else if (pos == 1) pa[i][j] = XADD(pa[i][j], z);
+                    else if (pos == 2) pb[i][j] = z;
+                    else if (pos == 3) { pb[i][j] = XADD(pb[i][j], z); pa[i][j] = XADD(pa[i][j], pb[i][j]); }
+                    else if (pos == 4) pb[i][j] = z;
+                    else if (pos == 5) pb[i][j] = XADD(pb[i][j], z);
+                    else if (pos == 6) pd[i][j] = z;
+                    else { pd[i][j] = XADD(pd[i][j], z); pb[i][j] = XADD(pb[i][j], pd[i][j]); pa[i][j] = XADD(pa[i][j], pb[i][j]); }
+#else
+                    if (pos == 0) pa[i][j] = XMUL(a[i], b[j]);
+                    else pa[i][j] = XFMA(a[i], b[j], pa[i][j]);
+#endif
+                }
+            if (pos == 7) {
+                // push the 8-channel block sum into the chunk-level counter
+                const int q = kt * (WINO_BK / 8) + (kk >> 3);
+                const int d = __ffs(~q) - 1;  // trailing ones of q = merges
+#pragma unroll
+                for (int L = 0; L < WINO_LEVELS; ++L) {
+                    if (d == L) {
+#pragma unroll
+                        for (int i = 0; i < WINO_TM; ++i)
+#pragma unroll
+                            for (int j = 0; j < WINO_TN; ++j) {
+                                DT cy = pa[i][j];
+#pragma unroll
+                                for (int e = 0; e < L; ++e) cy = XADD(slot[e][i][j], cy);
+                                slot[L][i][j] = cy;
+                            }
+                    }
+                }
+            }
+#endif
+        }
+    }
+
+#if WINO_SUM == 1 || WINO_SUM == 3
+    // fold the occupied slots (set bits of the chunk count), smallest block first
+    DT acc[WINO_TM][WINO_TN];
+    {
+        const long long Q = Cp / 8;
+        bool have = false;
+#pragma unroll
+        for (int L = 0; L < WINO_LEVELS; ++L) {
+            if ((Q >> L) & 1) {
+#pragma unroll
+                for (int i = 0; i < WINO_TM; ++i)
+#pragma unroll
+                    for (int j = 0; j < WINO_TN; ++j)
+                        acc[i][j] = have ? XADD(slot[L][i][j], acc[i][j]) : slot[L][i][j];
+                have = true;
+            }
+        }
+    }
+#endif
+
+    DT* gM = M + p * Kp * Tp + k0 * Tp + t0;
+#pragma unroll
+    for (int g = 0; g < GM; ++g)
+#pragma unroll
+        for (int v = 0; v < VW; ++v) {
+            const int i = g * VW + v;
+            const long long row = g * (WINO_THM * VW) + tm * VW + v;
+#pragma unroll
+            for (int h = 0; h < GN; ++h) {
+                vec_t q;
+                DT* qq = reinterpret_cast<DT*>(&q);
+#pragma unroll
+                for (int u = 0; u < VW; ++u) qq[u] = acc[i][h * VW + u];
+                *reinterpret_cast<vec_t*>(gM + row * Tp + h * (WINO_THN * VW) + tn * VW) = q;
+            }
+        }
+}

@@ -1,0 +1,463 @@
+// libwino host side: plans, NVRTC JIT of generated sm_100a kernels, driver-API
+// module loading and launches, and the C-ABI entry points of include/wino.h.
+//
+// A plan mirrors (TransformSet, ConvConfig) of the reference (transforms.py:41-145,
+// engine.py:27-55): it owns the row programs of G, B^T and A^T, the generated
+// transform source, and lazily compiled contraction variants.  Nothing here
+// falls back to the CPU: every compute entry point launches device kernels.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <atomic>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "codegen.h"
+#include "wino_internal.h"
+
+namespace wino {
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int after_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(WINO_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    count_launch();
+    return WINO_OK;
+}
+
+// ------------------------------------------------------------------ driver API
+struct Driver {
+    CUresult (*ModuleLoadData)(CUmodule*, const void*) = nullptr;
+    CUresult (*ModuleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
+    CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                             CUstream, void**, void**) = nullptr;
+    CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
+    CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
+    bool ok = false;
+    std::string err;
+};
+
+static Driver& driver() {
+    static Driver d;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        auto get = [](const char* name, void** fn) -> bool {
+            cudaDriverEntryPointQueryResult q;
+            cudaError_t e = cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q);
+            return e == cudaSuccess && q == cudaDriverEntryPointSuccess && *fn;
+        };
+        bool ok = get("cuModuleLoadData", (void**)&d.ModuleLoadData) &&
+                  get("cuModuleGetFunction", (void**)&d.ModuleGetFunction) &&
+                  get("cuLaunchKernel", (void**)&d.LaunchKernel) &&
+                  get("cuFuncSetAttribute", (void**)&d.FuncSetAttribute) &&
+                  get("cuGetErrorString", (void**)&d.GetErrorString);
+        d.ok = ok;
+        if (!ok) d.err = "CUDA driver entry points unavailable (no GPU driver?)";
+    });
+    return d;
+}
+
+static std::string cu_err(CUresult r) {
+    const char* s = nullptr;
+    if (driver().GetErrorString) driver().GetErrorString(r, &s);
+    return s ? s : ("CUresult " + std::to_string((int)r));
+}
+
+// ------------------------------------------------------------------ NVRTC
+struct Compiled {
+    std::vector<char> cubin;
+    std::string log;
+};
+
+static int nvrtc_compile(const std::string& src, const std::string& name, Compiled* out) {
+    nvrtcProgram prog;
+    nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), name.c_str(), 0, nullptr, nullptr);
+    if (r != NVRTC_SUCCESS) return fail(WINO_ECOMPILE, std::string("nvrtcCreateProgram: ") + nvrtcGetErrorString(r));
+    const char* opts[] = {"-arch=sm_100a", "-fmad=false", "-lineinfo", "-std=c++17", "-default-device",
+                          "--ptxas-options=-v"};
+    r = nvrtcCompileProgram(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
+    size_t ls = 0;
+    nvrtcGetProgramLogSize(prog, &ls);
+    out->log.assign(ls, '\0');
+    if (ls) nvrtcGetProgramLog(prog, &out->log[0]);
+    if (r != NVRTC_SUCCESS) {
+        nvrtcDestroyProgram(&prog);
+        return fail(WINO_ECOMPILE, "NVRTC failed on " + name + ": " + out->log.substr(0, 4000));
+    }
+    size_t cs = 0;
+    nvrtcGetCUBINSize(prog, &cs);
+    out->cubin.resize(cs);
+    nvrtcGetCUBIN(prog, out->cubin.data());
+    nvrtcDestroyProgram(&prog);
+    return WINO_OK;
+}
+
+// A generated module: source, cubin, and per-device loaded CUmodule/functions.
+struct Module {
+    std::string name, source;
+    Compiled bin;
+    bool compiled = false;
+    std::mutex mu;
+    std::map<int, CUmodule> mods;
+    std::map<std::pair<int, std::string>, CUfunction> fns;
+
+    int ensure_compiled() {
+        std::lock_guard<std::mutex> g(mu);
+        if (compiled) return WINO_OK;
+        int rc = nvrtc_compile(source, name, &bin);
+        if (rc == WINO_OK) compiled = true;
+        return rc;
+    }
+
+    int function(const char* fname, CUfunction* f) {
+        int rc = ensure_compiled();
+        if (rc) return rc;
+        Driver& d = driver();
+        if (!d.ok) return fail(WINO_ECUDA, d.err);
+        int dev = 0;
+        cudaError_t ce = cudaGetDevice(&dev);
+        if (ce != cudaSuccess) return fail(WINO_ECUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(ce));
+        std::lock_guard<std::mutex> g(mu);
+        auto key = std::make_pair(dev, std::string(fname));
+        auto it = fns.find(key);
+        if (it != fns.end()) {
+            *f = it->second;
+            return WINO_OK;
+        }
+        if (!mods.count(dev)) {
+            cudaFree(nullptr);  // make the runtime's primary context current
+            CUmodule mod;
+            CUresult cr = d.ModuleLoadData(&mod, bin.cubin.data());
+            if (cr != CUDA_SUCCESS) return fail(WINO_ECUDA, "cuModuleLoadData(" + name + "): " + cu_err(cr));
+            mods[dev] = mod;
+        }
+        CUfunction fn;
+        CUresult cr = d.ModuleGetFunction(&fn, mods[dev], fname);
+        if (cr != CUDA_SUCCESS) return fail(WINO_ECUDA, std::string("cuModuleGetFunction(") + fname + "): " + cu_err(cr));
+        fns[key] = fn;
+        *f = fn;
+        return WINO_OK;
+    }
+};
+
+static int launch(CUfunction f, dim3 grid, dim3 block, unsigned smem, void* stream, void** args, const char* what) {
+    if (grid.x == 0 || grid.y == 0 || grid.z == 0) return WINO_OK;
+    if (smem > 48 * 1024) {
+        CUresult cr = driver().FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
+        if (cr != CUDA_SUCCESS) return fail(WINO_ECUDA, std::string(what) + ": set smem: " + cu_err(cr));
+    }
+    CUresult cr = driver().LaunchKernel(f, grid.x, grid.y, grid.z, block.x, block.y, block.z, smem,
+                                        (CUstream)stream, args, nullptr);
+    if (cr != CUDA_SUCCESS) return fail(WINO_ECUDA, std::string(what) + ": " + cu_err(cr));
+    count_launch();
+    return WINO_OK;
+}
+
+// ------------------------------------------------------------------ contraction template
+static const char* kContractTemplate =
+#include "contract_src.inc"
+    ;
+
+struct GemmCfg {
+    int tm, tn, thm, thn, bk, stages;
+    int bm() const { return thm * tm; }
+    int bn() const { return thn * tn; }
+    int threads() const { return thm * thn; }
+};
+
+}  // namespace wino
+
+// ------------------------------------------------------------------ plan
+struct wino_plan {
+    int r, m, n, precision, chsum, mode;
+    wino::MatProg G, BT, AT;
+    wino::GenTypes ty;
+    wino::GemmCfg gemm;
+    wino::Module layer, tile;
+    std::mutex mu;
+    std::map<int, std::unique_ptr<wino::Module>> contract;  // key: counter levels
+
+    int sum_mode() const { return (mode == WINO_CONTRACT_FFMA ? 2 : 0) + (chsum == WINO_SUM_PAIRWISE ? 1 : 0); }
+
+    wino::Module* contract_module(long long Cp) {
+        int levels = 1;
+        const long long Q = Cp / 8;
+        while ((1LL << levels) <= Q) ++levels;  // bit_length(Q)
+        if (chsum != WINO_SUM_PAIRWISE) levels = 0;
+        std::lock_guard<std::mutex> g(mu);
+        auto it = contract.find(levels);
+        if (it != contract.end()) return it->second.get();
+        auto mod = std::make_unique<wino::Module>();
+        std::ostringstream os;
+        const bool dbl = ty.uv_double;
+        os << "#define WINO_DT " << (dbl ? "double" : "float") << "\n#define WINO_DT_IS_DOUBLE " << (dbl ? 1 : 0)
+           << "\n#define WINO_TM " << gemm.tm << "\n#define WINO_TN " << gemm.tn << "\n#define WINO_THM " << gemm.thm
+           << "\n#define WINO_THN " << gemm.thn << "\n#define WINO_BK " << gemm.bk << "\n#define WINO_STAGES "
+           << gemm.stages << "\n#define WINO_SUM " << sum_mode() << "\n#define WINO_LEVELS "
+           << (levels > 0 ? levels : 1) << "\n"
+           << wino::kContractTemplate;
+        mod->source = os.str();
+        mod->name = "wino_contract_s" + std::to_string(sum_mode()) + "_L" + std::to_string(levels) + ".cu";
+        wino::Module* raw = mod.get();
+        contract[levels] = std::move(mod);
+        return raw;
+    }
+};
+
+namespace {
+
+int convert_prog(const wino_prog* p, wino::MatProg* out) {
+    if (!p || p->rows < 1 || p->cols < 1 || !p->row_start) return -1;
+    out->rows = p->rows;
+    out->cols = p->cols;
+    out->row.resize(p->rows);
+    for (int i = 0; i < p->rows; ++i) {
+        const int a = p->row_start[i], b = p->row_start[i + 1];
+        if (a < 0 || b < a || (b > a && !p->ops)) return -1;
+        out->row[i].ops.assign(p->ops + a, p->ops + b);
+    }
+    return 0;
+}
+
+long long round_up(long long v, long long q) { return (v + q - 1) / q * q; }
+
+int layout_of(const wino_plan* p, const wino_layer_shape* s, wino_layer_layout* L) {
+    if (!p || !s || !L) return wino::fail(WINO_EINVAL, "null argument");
+    if (s->N < 0 || s->C < 1 || s->K < 1 || s->H < 1 || s->W < 1 || s->pad < 0)
+        return wino::fail(WINO_EINVAL, "layer shape: N >= 0, C, K, H, W >= 1, pad >= 0 required");
+    const int Ho = s->H + 2 * s->pad - p->r + 1, Wo = s->W + 2 * s->pad - p->r + 1;
+    if (Ho < 1 || Wo < 1) return wino::fail(WINO_EINVAL, "input smaller than kernel");
+    std::memset(L, 0, sizeof *L);
+    L->P = p->n * p->n;
+    L->Ho = Ho;
+    L->Wo = Wo;
+    L->th = (Ho + p->m - 1) / p->m;
+    L->tw = (Wo + p->m - 1) / p->m;
+    L->T = (long long)s->N * L->th * L->tw;
+    L->Tp = round_up(L->T > 0 ? L->T : 1, p->gemm.bn());
+    L->Cp = round_up(s->C, p->gemm.bk);
+    L->Kp = round_up(s->K, p->gemm.bm());
+    L->elem_bytes_uv = p->ty.uv_double ? 8 : 4;
+    L->elem_bytes_y = p->ty.y_double ? 8 : 4;
+    L->u_bytes = (size_t)L->P * L->Cp * L->Kp * L->elem_bytes_uv;
+    L->v_bytes = (size_t)L->P * L->Cp * L->Tp * L->elem_bytes_uv;
+    L->m_bytes = (size_t)L->P * L->Kp * L->Tp * L->elem_bytes_uv;
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    L->workspace_bytes = al(L->u_bytes) + al(L->v_bytes) + al(L->m_bytes);
+    return WINO_OK;
+}
+
+inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
+
+}  // namespace
+
+// ================================================================== C-ABI
+extern "C" {
+
+const char* wino_last_error(void) { return wino::g_last_error.c_str(); }
+const char* wino_version(void) { return "libwino 0.1 (sm_100a)"; }
+int64_t wino_launch_count(void) { return wino::g_launches.load(); }
+
+int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_mode, const wino_prog* G,
+                     const wino_prog* BT, const wino_prog* AT, wino_plan** out) {
+    if (!out) return wino::fail(WINO_EINVAL, "plan_create: null out");
+    *out = nullptr;
+    if (r < 1 || m < 1) return wino::fail(WINO_EINVAL, "kernel and output sizes must be >= 1");
+    if (precision < 0 || precision > 2) return wino::fail(WINO_EINVAL, "precision must be fp32, fp64 or mixed");
+    if (channel_sum < 0 || channel_sum > 1) return wino::fail(WINO_EINVAL, "channel_sum must be linear or pairwise");
+    if (contract_mode < 0 || contract_mode > 1) return wino::fail(WINO_EINVAL, "contract mode must be exact or ffma");
+    const int n = r + m - 1;
+    if (n > 16) return wino::fail(WINO_EUNSUPPORTED, "alpha = r + m - 1 > 16 is not generated");
+    auto p = std::make_unique<wino_plan>();
+    p->r = r;
+    p->m = m;
+    p->n = n;
+    p->precision = precision;
+    p->chsum = channel_sum;
+    p->mode = contract_mode;
+    if (convert_prog(G, &p->G) || convert_prog(BT, &p->BT) || convert_prog(AT, &p->AT))
+        return wino::fail(WINO_EINVAL, "malformed program table");
+    std::string e = wino::validate(p->G, n, r, "G");
+    if (e.empty()) e = wino::validate(p->BT, n, n, "B_T");
+    if (e.empty()) e = wino::validate(p->AT, m, n, "A_T");
+    if (!e.empty()) return wino::fail(WINO_EINVAL, e);
+    const bool dbl64 = precision == WINO_FP64;
+    p->ty.compute_double = precision != WINO_FP32;
+    p->ty.in_double = dbl64;
+    p->ty.uv_double = dbl64;
+    p->ty.y_double = precision != WINO_FP32;
+    if (dbl64)
+        p->gemm = {4, 4, 16, 16, 8, 4};
+    else if (channel_sum == WINO_SUM_PAIRWISE)
+        p->gemm = {4, 4, 16, 16, 8, 4};
+    else
+        p->gemm = {8, 8, 16, 16, 8, 4};
+    const std::string tag = "r" + std::to_string(r) + "m" + std::to_string(m) + "p" + std::to_string(precision);
+    p->layer.name = "wino_layer_" + tag + ".cu";
+    p->layer.source = wino::gen_layer_source(r, m, p->G, p->BT, p->AT, p->ty);
+    p->tile.name = "wino_tile_" + tag + ".cu";
+    p->tile.source = wino::gen_tile_source(r, m, p->G, p->BT, p->AT, p->ty);
+    int rc = p->layer.ensure_compiled();
+    if (rc) return rc;
+    *out = p.release();
+    return WINO_OK;
+}
+
+void wino_plan_destroy(wino_plan* plan) { delete plan; }  // modules unload with their context
+
+int wino_plan_source(const wino_plan* plan, int which, char* buf, size_t cap, size_t* len) {
+    if (!plan || (which != 0 && which != 1)) return wino::fail(WINO_EINVAL, "plan_source: bad arguments");
+    const std::string& s = which == 0 ? plan->layer.source : plan->tile.source;
+    if (len) *len = s.size();
+    if (buf && cap) {
+        const size_t k = s.size() < cap - 1 ? s.size() : cap - 1;
+        std::memcpy(buf, s.data(), k);
+        buf[k] = '\0';
+    }
+    return WINO_OK;
+}
+
+int wino_plan_cubin(wino_plan* plan, int which, int channels, void* buf, size_t cap, size_t* len) {
+    if (!plan || which < 0 || which > 2) return wino::fail(WINO_EINVAL, "plan_cubin: bad arguments");
+    wino::Module* mod = which == 0 ? &plan->layer
+                        : which == 1 ? &plan->tile
+                                     : plan->contract_module(round_up(channels > 0 ? channels : 1, plan->gemm.bk));
+    int rc = mod->ensure_compiled();
+    if (rc) return rc;
+    if (len) *len = mod->bin.cubin.size();
+    if (buf && cap >= mod->bin.cubin.size()) std::memcpy(buf, mod->bin.cubin.data(), mod->bin.cubin.size());
+    return WINO_OK;
+}
+
+int wino_layer_layout_query(const wino_plan* plan, const wino_layer_shape* s, wino_layer_layout* out) {
+    return layout_of(plan, s, out);
+}
+
+int wino_filter_transform(wino_plan* plan, const wino_layer_shape* s, const void* w, void* U, void* stream) {
+    wino_layer_layout L;
+    int rc = layout_of(plan, s, &L);
+    if (rc) return rc;
+    CUfunction f;
+    if ((rc = plan->layer.function("wino_filter_xform", &f))) return rc;
+    int K = s->K, C = s->C;
+    long long Kp = L.Kp, Cp = L.Cp;
+    void* args[] = {(void*)&w, &U, &K, &C, &Kp, &Cp};
+    return wino::launch(f, dim3(cdiv(Kp, 128), (unsigned)Cp, 1), dim3(128), 0, stream, args, "filter_transform");
+}
+
+int wino_input_transform(wino_plan* plan, const wino_layer_shape* s, const void* x, void* V, void* stream) {
+    wino_layer_layout L;
+    int rc = layout_of(plan, s, &L);
+    if (rc) return rc;
+    CUfunction f;
+    if ((rc = plan->layer.function("wino_input_xform", &f))) return rc;
+    int C = s->C, H = s->H, W = s->W, pad = s->pad, th = L.th, tw = L.tw;
+    long long T = L.T, Tp = L.Tp, Cp = L.Cp;
+    void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp};
+    return wino::launch(f, dim3(cdiv(Tp, 128), (unsigned)Cp, 1), dim3(128), 0, stream, args, "input_transform");
+}
+
+int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, const void* V, void* M, void* stream) {
+    wino_layer_layout L;
+    int rc = layout_of(plan, s, &L);
+    if (rc) return rc;
+    if (((uintptr_t)U | (uintptr_t)V | (uintptr_t)M) & 15)
+        return wino::fail(WINO_EINVAL, "contract: U, V, M must be 16-byte aligned");
+    wino::Module* mod = plan->contract_module(L.Cp);
+    CUfunction f;
+    if ((rc = mod->function("wino_contract", &f))) return rc;
+    const wino::GemmCfg& g = plan->gemm;
+    long long Kp = L.Kp, Tp = L.Tp, Cp = L.Cp;
+    void* args[] = {(void*)&U, (void*)&V, &M, &Kp, &Tp, &Cp};
+    const unsigned smem = (unsigned)(g.stages * g.bk * (g.bm() + g.bn()) * L.elem_bytes_uv + g.stages * 8);
+    return wino::launch(f, dim3((unsigned)(Tp / g.bn()), (unsigned)(Kp / g.bm()), (unsigned)L.P),
+                        dim3(g.threads()), smem, stream, args, "contract");
+}
+
+int wino_output_transform(wino_plan* plan, const wino_layer_shape* s, const void* M, void* y, void* stream) {
+    wino_layer_layout L;
+    int rc = layout_of(plan, s, &L);
+    if (rc) return rc;
+    CUfunction f;
+    if ((rc = plan->layer.function("wino_output_xform", &f))) return rc;
+    int K = s->K, Ho = L.Ho, Wo = L.Wo, th = L.th, tw = L.tw;
+    long long T = L.T, Tp = L.Tp, Kp = L.Kp;
+    void* args[] = {(void*)&M, &y, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp};
+    return wino::launch(f, dim3(cdiv(T, 128), (unsigned)K, 1), dim3(128), 0, stream, args, "output_transform");
+}
+
+int wino_conv2d(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w, void* y, void* workspace,
+                size_t workspace_bytes, void* stream) {
+    wino_layer_layout L;
+    int rc = layout_of(plan, s, &L);
+    if (rc) return rc;
+    if (s->N == 0) return WINO_OK;
+    if (!workspace || workspace_bytes < L.workspace_bytes || ((uintptr_t)workspace & 255))
+        return wino::fail(WINO_EINVAL, "conv2d: workspace missing, too small or not 256-byte aligned");
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    char* U = (char*)workspace;
+    char* V = U + al(L.u_bytes);
+    char* M = V + al(L.v_bytes);
+    if ((rc = wino_filter_transform(plan, s, w, U, stream))) return rc;
+    if ((rc = wino_input_transform(plan, s, x, V, stream))) return rc;
+    if ((rc = wino_contract(plan, s, U, V, M, stream))) return rc;
+    return wino_output_transform(plan, s, M, y, stream);
+}
+
+int wino_tile_hadamard2d(wino_plan* plan, int64_t B, int C, const void* h, const void* x, void* z, void* stream) {
+    if (!plan || B < 0 || C < 1) return wino::fail(WINO_EINVAL, "tile_hadamard2d: bad arguments");
+    CUfunction f;
+    int rc = plan->tile.function("wino_tile_h2d", &f);
+    if (rc) return rc;
+    long long BC = B * (long long)C;
+    void* args[] = {(void*)&h, (void*)&x, &z, &BC};
+    return wino::launch(f, dim3(cdiv(BC, 128)), dim3(128), 0, stream, args, "tile_hadamard2d");
+}
+
+int wino_tile_output2d(wino_plan* plan, int64_t B, const void* y, void* out, void* stream) {
+    if (!plan || B < 0) return wino::fail(WINO_EINVAL, "tile_output2d: bad arguments");
+    CUfunction f;
+    int rc = plan->tile.function("wino_tile_o2d", &f);
+    if (rc) return rc;
+    long long b = B;
+    void* args[] = {(void*)&y, &out, &b};
+    return wino::launch(f, dim3(cdiv(b, 128)), dim3(128), 0, stream, args, "tile_output2d");
+}
+
+int wino_tile_hadamard1d(wino_plan* plan, int64_t B, int C, const void* h, const void* x, void* z, void* stream) {
+    if (!plan || B < 0 || C < 1) return wino::fail(WINO_EINVAL, "tile_hadamard1d: bad arguments");
+    CUfunction f;
+    int rc = plan->tile.function("wino_tile_h1d", &f);
+    if (rc) return rc;
+    long long BC = B * (long long)C;
+    void* args[] = {(void*)&h, (void*)&x, &z, &BC};
+    return wino::launch(f, dim3(cdiv(BC, 128)), dim3(128), 0, stream, args, "tile_hadamard1d");
+}
+
+int wino_tile_output1d(wino_plan* plan, int64_t B, const void* y, void* out, void* stream) {
+    if (!plan || B < 0) return wino::fail(WINO_EINVAL, "tile_output1d: bad arguments");
+    CUfunction f;
+    int rc = plan->tile.function("wino_tile_o1d", &f);
+    if (rc) return rc;
+    long long b = B;
+    void* args[] = {(void*)&y, &out, &b};
+    return wino::launch(f, dim3(cdiv(b, 128)), dim3(128), 0, stream, args, "tile_output1d");
+}
+
+}  // extern "C"

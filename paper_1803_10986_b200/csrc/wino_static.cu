@@ -1,0 +1,435 @@
+// Statically compiled (nvcc, sm_100a) kernels of libwino: everything whose
+// code does not depend on the transform triple.
+//   - channel_reduce (linear / halving tree)          reference engine.py:252-287
+//   - direct_products and the layer fp64 direct conv   reference engine.py:309-346
+//   - per-image error partials of a layer
+//   - trial_inputs (numpy Philox4x64-10 on device)     reference harness.py:97-107
+//   - per-trial L1 and the mean in numpy's summation order (harness.py:143-166)
+// All arithmetic uses explicit round-to-nearest intrinsics (no contraction).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "philox.cuh"
+#include "wino_internal.h"
+
+namespace {
+
+template <typename T> __device__ __forceinline__ T radd(T a, T b);
+template <> __device__ __forceinline__ float radd<float>(float a, float b) { return __fadd_rn(a, b); }
+template <> __device__ __forceinline__ double radd<double>(double a, double b) { return __dadd_rn(a, b); }
+template <typename T> __device__ __forceinline__ T rmul(T a, T b);
+template <> __device__ __forceinline__ float rmul<float>(float a, float b) { return __fmul_rn(a, b); }
+template <> __device__ __forceinline__ double rmul<double>(double a, double b) { return __dmul_rn(a, b); }
+
+// ---------------------------------------------------------------- channel sums
+// in[outer][C][inner] -> out[outer][inner]
+template <typename T>
+__global__ void channel_reduce_kernel(int strategy, long long outer, long long C, long long inner,
+                                      const T* __restrict__ in, T* __restrict__ out) {
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= outer * inner) return;
+    const long long o = idx / inner, e = idx - o * inner;
+    const T* src = in + o * C * inner + e;
+    if (strategy == 0 || C == 1) {
+        T acc = src[0];
+        for (long long c = 1; c < C; ++c) acc = radd(acc, src[c * inner]);
+        out[idx] = acc;
+        return;
+    }
+    // halving tree == binary counter: slot j holds a block of 2^j values
+    T slot[64];
+    for (long long c = 0; c < C; ++c) {
+        T cy = src[c * inner];
+        int j = 0;
+        for (long long q = c; q & 1; q >>= 1, ++j) cy = radd(slot[j], cy);
+        slot[j] = cy;
+    }
+    T acc = 0;
+    bool have = false;
+    for (int j = 0; j < 63; ++j)
+        if ((C >> j) & 1) {
+            acc = have ? radd(slot[j], acc) : slot[j];
+            have = true;
+        }
+    out[idx] = acc;
+}
+
+// ---------------------------------------------------------------- direct products
+// h[B][C][r(^2)], x[B][C][n(^2)] -> out[B][C][o(^2)], o = n - r + 1
+template <typename T, typename TI>
+__global__ void direct_products_kernel(int dims, long long BC, int r, int n, const TI* __restrict__ h,
+                                       const TI* __restrict__ x, T* __restrict__ out) {
+    const int o = n - r + 1;
+    const int per = dims == 1 ? o : o * o;
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= BC * per) return;
+    const long long bc = idx / per;
+    const int q = (int)(idx - bc * per);
+    if (dims == 1) {
+        const TI* hh = h + bc * r;
+        const TI* xx = x + bc * n;
+        T acc = rmul((T)hh[0], (T)xx[q]);
+        for (int a = 1; a < r; ++a) acc = radd(acc, rmul((T)hh[a], (T)xx[q + a]));
+        out[idx] = acc;
+        return;
+    }
+    const int qi = q / o, qj = q - qi * o;
+    const TI* hh = h + bc * r * r;
+    const TI* xx = x + bc * n * n;
+    T acc = 0;
+    for (int a = 0; a < r; ++a)
+        for (int b = 0; b < r; ++b) {
+            const T t = rmul((T)hh[a * r + b], (T)xx[(qi + a) * n + qj + b]);
+            acc = (a == 0 && b == 0) ? t : radd(acc, t);
+        }
+    out[idx] = acc;
+}
+
+// ---------------------------------------------------------------- fp64 direct layer
+// One thread per output (n, k, ho, wo); per channel the r*r taps in row-major
+// order, channels left to right (reference direct_products + channel_reduce
+// "linear" on the zero-padded image).  w[k] staged in shared memory.
+__global__ void direct_layer_f64_kernel(int N, int C, int H, int W, int K, int r, int pad, int Ho,
+                                        int Wo, const float* __restrict__ x,
+                                        const float* __restrict__ w, double* __restrict__ y) {
+    extern __shared__ double sw[];  // [C][r][r] of filter k
+    const int k = blockIdx.y;
+    const int n = blockIdx.z;
+    for (int i = threadIdx.x; i < C * r * r; i += blockDim.x) sw[i] = (double)w[(long long)k * C * r * r + i];
+    __syncthreads();
+    const long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pix >= (long long)Ho * Wo) return;
+    const int ho = (int)(pix / Wo), wo = (int)(pix - (long long)ho * Wo);
+    double total = 0.0;
+    for (int c = 0; c < C; ++c) {
+        const float* xc = x + ((long long)n * C + c) * H * W;
+        const double* wc = sw + c * r * r;
+        double acc = 0.0;
+        for (int a = 0; a < r; ++a) {
+            const int hi = ho + a - pad;
+            const bool rin = (unsigned)hi < (unsigned)H;
+            for (int b = 0; b < r; ++b) {
+                const int wi = wo + b - pad;
+                const double xv = (rin && (unsigned)wi < (unsigned)W) ? (double)xc[(long long)hi * W + wi] : 0.0;
+                const double t = __dmul_rn(wc[a * r + b], xv);
+                acc = (a == 0 && b == 0) ? t : __dadd_rn(acc, t);
+            }
+        }
+        total = (c == 0) ? acc : __dadd_rn(total, acc);
+    }
+    y[(((long long)n * K + k) * Ho + ho) * Wo + wo] = total;
+}
+
+// ---------------------------------------------------------------- layer error partials
+template <typename T>
+__global__ void layer_err_kernel(long long N, long long per, const T* __restrict__ y,
+                                 const double* __restrict__ y64, double* __restrict__ stats) {
+    // one block per image; threads stride the image, then a fixed-order tree in smem
+    __shared__ double s_err[256], s_ref[256], s_max[256];
+    const long long n = blockIdx.x;
+    double e = 0.0, rf = 0.0, mx = 0.0;
+    for (long long i = threadIdx.x; i < per; i += blockDim.x) {
+        const double ref = y64[n * per + i];
+        const double d = fabs(__dadd_rn((double)y[n * per + i], -ref));
+        e = __dadd_rn(e, d);
+        rf = __dadd_rn(rf, fabs(ref));
+        mx = fmax(mx, d);
+    }
+    s_err[threadIdx.x] = e;
+    s_ref[threadIdx.x] = rf;
+    s_max[threadIdx.x] = mx;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            s_err[threadIdx.x] = __dadd_rn(s_err[threadIdx.x], s_err[threadIdx.x + s]);
+            s_ref[threadIdx.x] = __dadd_rn(s_ref[threadIdx.x], s_ref[threadIdx.x + s]);
+            s_max[threadIdx.x] = fmax(s_max[threadIdx.x], s_max[threadIdx.x + s]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        stats[n * 4 + 0] = s_err[0];
+        stats[n * 4 + 1] = s_ref[0];
+        stats[n * 4 + 2] = (double)per;
+        stats[n * 4 + 3] = s_max[0];
+    }
+}
+
+
+// ---------------------------------------------------------------- one program, many vectors
+// dot_with_order (engine.py:235-246): evaluate one postfix row program against
+// every vector in[count][cols]; LEAF = one rounded product, ADD = one rounded sum.
+template <typename T>
+__global__ void program_eval_kernel(const wino_op* __restrict__ ops, int nops, int cols, long long count,
+                                    const T* __restrict__ in, T* __restrict__ out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const T* v = in + i * cols;
+    T st[64];
+    int sp = 0;
+    for (int k = 0; k < nops; ++k) {
+        const wino_op op = ops[k];
+        if (op.kind == WINO_OP_LEAF) {
+            st[sp++] = rmul((T)op.coeff, v[op.col]);
+        } else {
+            const T b = st[--sp];
+            const T a = st[--sp];
+            st[sp++] = radd(a, b);
+        }
+    }
+    out[i] = nops ? st[0] : (T)0;
+}
+
+// ---------------------------------------------------------------- Philox trial inputs
+// one thread per (trial, 8-float block of the trial's stream)
+__global__ void trial_inputs_kernel(uint64_t seed, long long t0, long long B, long long fh, long long fx,
+                                    float* __restrict__ h, float* __restrict__ x) {
+    const long long per = fh + fx;
+    const long long nblk = (per + 7) / 8;
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= B * nblk) return;
+    const long long b = idx / nblk, blk = idx - b * nblk;
+    float u[8];
+    wino::philox_block_floats(seed, (uint64_t)(t0 + b), (uint64_t)blk, u);
+    for (int i = 0; i < 8; ++i) {
+        const long long f = blk * 8 + i;
+        if (f >= per) break;
+        const float v = __fadd_rn(__fmul_rn(u[i], 2.0f), -1.0f);
+        if (f < fh) h[b * fh + f] = v;
+        else x[b * fx + (f - fh)] = v;
+    }
+}
+
+// ---------------------------------------------------------------- numpy pairwise sum
+// DOUBLE_pairwise_sum: n < 8 sequential from +0; n <= 128 eight strided partial
+// sums combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a sequential tail;
+// larger n split at n2 = n/2 rounded down to a multiple of 8 (recursively).
+template <typename F>
+__device__ double np_pairwise(long long n, F at) {
+    // explicit stack instead of recursion: (offset, length) segments, left first
+    long long st_off[64], st_len[64];
+    int sp = 0;
+    double vals[64];
+    int vsp = 0;
+    // post-order evaluation: push root; combine results as segments complete
+    // encode "combine" markers with len = -1
+    st_off[sp] = 0;
+    st_len[sp] = n;
+    ++sp;
+    while (sp > 0) {
+        --sp;
+        const long long off = st_off[sp], len = st_len[sp];
+        if (len < 0) {
+            const double rgt = vals[--vsp];
+            const double lft = vals[--vsp];
+            vals[vsp++] = __dadd_rn(lft, rgt);
+            continue;
+        }
+        if (len < 8) {
+            double res = 0.0;
+            for (long long i = 0; i < len; ++i) res = __dadd_rn(res, at(off + i));
+            vals[vsp++] = res;
+        } else if (len <= 128) {
+            double r[8];
+            for (int j = 0; j < 8; ++j) r[j] = at(off + j);
+            long long i = 8;
+            for (; i < len - (len % 8); i += 8)
+                for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], at(off + i + j));
+            double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                                   __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+            for (; i < len; ++i) res = __dadd_rn(res, at(off + i));
+            vals[vsp++] = res;
+        } else {
+            long long n2 = len / 2;
+            n2 -= n2 % 8;
+            // evaluate left, then right, then combine
+            st_off[sp] = 0; st_len[sp] = -1; ++sp;
+            st_off[sp] = off + n2; st_len[sp] = len - n2; ++sp;
+            st_off[sp] = off; st_len[sp] = n2; ++sp;
+        }
+    }
+    return vals[0];
+}
+
+template <typename T>
+__global__ void trial_l1_kernel(long long B, long long per, const T* __restrict__ out,
+                                const double* __restrict__ ref, double* __restrict__ per_trial) {
+    const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const T* o = out + b * per;
+    const double* rf = ref + b * per;
+    per_trial[b] = np_pairwise(per, [&](long long i) { return fabs(__dadd_rn((double)o[i], -rf[i])); });
+}
+
+__global__ void mean_kernel(long long n, const double* __restrict__ v, double* __restrict__ out) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const double s = np_pairwise(n, [&](long long i) { return v[i]; });
+        out[0] = __ddiv_rn(s, (double)n);
+    }
+}
+
+
+// ---------------------------------------------------------------- peak probes
+// Arithmetic-throughput probes for the roofline denominators (mode 0: FFMA,
+// 1: FMUL+FADD pairs, 2: DFMA, 3: DMUL+DADD).  8 independent chains per thread.
+__global__ void peak_probe_kernel(int mode, int iters, float seedf, float* __restrict__ out) {
+    float a[8];
+    double d[8];
+    for (int i = 0; i < 8; ++i) {
+        a[i] = seedf + 0.001f * (threadIdx.x + i);
+        d[i] = (double)a[i];
+    }
+    const float m = 0.9999f, c = 1e-7f;
+    if (mode == 0) {
+        for (int it = 0; it < iters; ++it)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = __fmaf_rn(a[i], m, c);
+    } else if (mode == 1) {
+        for (int it = 0; it < iters; ++it)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = __fadd_rn(__fmul_rn(a[i], m), c);
+    } else if (mode == 2) {
+        for (int it = 0; it < iters; ++it)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) d[i] = __fma_rn(d[i], (double)m, (double)c);
+    } else {
+        for (int it = 0; it < iters; ++it)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) d[i] = __dadd_rn(__dmul_rn(d[i], (double)m), (double)c);
+    }
+    float s = 0.f;
+    for (int i = 0; i < 8; ++i) s += a[i] + (float)d[i];
+    if (s == 12345.678f) out[0] = s;  // keep the chains alive
+}
+
+inline unsigned blocks_for(long long n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+// ============================================================== C-ABI launchers
+extern "C" {
+
+int wino_channel_reduce(int dtype, int strategy, int64_t outer, int64_t C, int64_t inner, const void* in,
+                        void* out, void* stream) {
+    if ((dtype != 0 && dtype != 1) || (strategy != 0 && strategy != 1) || outer < 0 || C < 1 || inner < 0 ||
+        C >= (1LL << 62))
+        return wino::fail(WINO_EINVAL, "channel_reduce: bad arguments");
+    const long long n = outer * inner;
+    if (n == 0) return WINO_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == 0)
+        channel_reduce_kernel<float><<<blocks_for(n, 128), 128, 0, s>>>(strategy, outer, C, inner,
+                                                                       (const float*)in, (float*)out);
+    else
+        channel_reduce_kernel<double><<<blocks_for(n, 128), 128, 0, s>>>(strategy, outer, C, inner,
+                                                                        (const double*)in, (double*)out);
+    return wino::after_launch("channel_reduce");
+}
+
+int wino_direct_products(int dims, int dtype, int in_dtype, int64_t B, int C, int r, int n, const void* h,
+                         const void* x, void* out, void* stream) {
+    if ((dims != 1 && dims != 2) || B < 0 || C < 1 || r < 1 || n < r || (dtype | in_dtype) & ~1)
+        return wino::fail(WINO_EINVAL, "direct_products: bad arguments");
+    const int o = n - r + 1;
+    const long long total = B * (long long)C * (dims == 1 ? o : o * o);
+    if (total == 0) return WINO_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const unsigned g = blocks_for(total, 128);
+    const long long BC = B * (long long)C;
+    if (dtype == 1 && in_dtype == 1)
+        direct_products_kernel<double, double><<<g, 128, 0, s>>>(dims, BC, r, n, (const double*)h, (const double*)x, (double*)out);
+    else if (dtype == 1)
+        direct_products_kernel<double, float><<<g, 128, 0, s>>>(dims, BC, r, n, (const float*)h, (const float*)x, (double*)out);
+    else if (in_dtype == 1)
+        direct_products_kernel<float, double><<<g, 128, 0, s>>>(dims, BC, r, n, (const double*)h, (const double*)x, (float*)out);
+    else
+        direct_products_kernel<float, float><<<g, 128, 0, s>>>(dims, BC, r, n, (const float*)h, (const float*)x, (float*)out);
+    return wino::after_launch("direct_products");
+}
+
+
+int wino_program_eval(int dtype, const void* ops, int nops, int cols, int64_t count, const void* in, void* out,
+                      void* stream) {
+    if ((dtype != 0 && dtype != 1) || nops < 0 || nops > 127 || cols < 1 || count < 0)
+        return wino::fail(WINO_EINVAL, "program_eval: bad arguments");
+    if (count == 0) return WINO_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == 0)
+        program_eval_kernel<float><<<blocks_for(count, 128), 128, 0, s>>>((const wino_op*)ops, nops, cols, count,
+                                                                         (const float*)in, (float*)out);
+    else
+        program_eval_kernel<double><<<blocks_for(count, 128), 128, 0, s>>>((const wino_op*)ops, nops, cols, count,
+                                                                          (const double*)in, (double*)out);
+    return wino::after_launch("program_eval");
+}
+
+
+int wino_peak_probe(int mode, int blocks, int iters, float* out, void* stream) {
+    if (mode < 0 || mode > 3 || blocks < 1 || iters < 1) return wino::fail(WINO_EINVAL, "peak_probe: bad arguments");
+    peak_probe_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(mode, iters, 1.0f, out);
+    return wino::after_launch("peak_probe");
+}
+
+int wino_direct_layer_f64(const wino_layer_shape* sh, int r, const float* x, const float* w, double* y64,
+                          void* stream) {
+    if (!sh || r < 1 || sh->N < 0 || sh->C < 1 || sh->K < 1 || sh->pad < 0)
+        return wino::fail(WINO_EINVAL, "direct_layer_f64: bad arguments");
+    const int Ho = sh->H + 2 * sh->pad - r + 1, Wo = sh->W + 2 * sh->pad - r + 1;
+    if (Ho < 1 || Wo < 1) return wino::fail(WINO_EINVAL, "direct_layer_f64: input smaller than kernel");
+    if (sh->N == 0) return WINO_OK;
+    const size_t smem = (size_t)sh->C * r * r * sizeof(double);
+    if (smem > 200 * 1024) return wino::fail(WINO_EUNSUPPORTED, "direct_layer_f64: C*r*r too large");
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(direct_layer_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dim3 grid(blocks_for((long long)Ho * Wo, 128), sh->K, sh->N);
+    direct_layer_f64_kernel<<<grid, 128, smem, (cudaStream_t)stream>>>(sh->N, sh->C, sh->H, sh->W, sh->K, r,
+                                                                       sh->pad, Ho, Wo, x, w, y64);
+    return wino::after_launch("direct_layer_f64");
+}
+
+int wino_layer_error_stats(int64_t N, int64_t per_image, int y_dtype, const void* y, const double* y64,
+                           double* stats, void* stream) {
+    if (N < 0 || per_image < 1 || (y_dtype != 0 && y_dtype != 1))
+        return wino::fail(WINO_EINVAL, "layer_error_stats: bad arguments");
+    if (N == 0) return WINO_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (y_dtype == 0)
+        layer_err_kernel<float><<<(unsigned)N, 256, 0, s>>>(N, per_image, (const float*)y, y64, stats);
+    else
+        layer_err_kernel<double><<<(unsigned)N, 256, 0, s>>>(N, per_image, (const double*)y, y64, stats);
+    return wino::after_launch("layer_error_stats");
+}
+
+int wino_trial_inputs(uint64_t seed, int64_t t0, int64_t B, int dims, int r, int n, int C, float* h, float* x,
+                      void* stream) {
+    if ((dims != 1 && dims != 2) || B < 0 || t0 < 0 || C < 1 || r < 1 || n < 1)
+        return wino::fail(WINO_EINVAL, "trial_inputs: bad arguments");
+    if (B == 0) return WINO_OK;
+    const long long fh = (long long)C * (dims == 1 ? r : r * r);
+    const long long fx = (long long)C * (dims == 1 ? n : n * n);
+    const long long nblk = (fh + fx + 7) / 8;
+    trial_inputs_kernel<<<blocks_for(B * nblk, 128), 128, 0, (cudaStream_t)stream>>>(seed, t0, B, fh, fx, h, x);
+    return wino::after_launch("trial_inputs");
+}
+
+int wino_trial_l1(int64_t B, int64_t per, int out_dtype, const void* out, const double* ref, double* per_trial,
+                  void* stream) {
+    if (B < 0 || per < 1 || (out_dtype != 0 && out_dtype != 1))
+        return wino::fail(WINO_EINVAL, "trial_l1: bad arguments");
+    if (B == 0) return WINO_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (out_dtype == 0)
+        trial_l1_kernel<float><<<blocks_for(B, 128), 128, 0, s>>>(B, per, (const float*)out, ref, per_trial);
+    else
+        trial_l1_kernel<double><<<blocks_for(B, 128), 128, 0, s>>>(B, per, (const double*)out, ref, per_trial);
+    return wino::after_launch("trial_l1");
+}
+
+int wino_mean_f64(int64_t n, const double* v, double* out, void* stream) {
+    if (n < 1) return wino::fail(WINO_EINVAL, "mean_f64: n must be >= 1");
+    mean_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(n, v, out);
+    return wino::after_launch("mean_f64");
+}
+
+}  // extern "C"
+

@@ -1,0 +1,172 @@
+"""Layer-level Winograd convolution on the B200 -- the north-star hot path.
+
+The reference has no layer API; its arithmetic is reached by
+calling ``conv_2d(ts, w[k], X[tile], cfg)`` for every (output channel, tile)
+of the zero-padded image.  ``conv2d_layer`` computes exactly
+those numbers in four device stages:
+
+  K2 filter transform    U[p][c][k] = (G w[k,c] G^T)[p]
+  K1 input transform     V[p][c][t] = (B^T d[t,c] B)[p]   (gather + zero pad fused)
+  K3 contraction         M[p][k][t] = sum_c U[p][c][k] V[p][c][t]   (linear | pairwise order)
+  K4 output transform    y[n,k,tile] = A^T M[.][k][t] A   (crop + NCHW write-back)
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+
+from . import _native
+from . import device as D
+from .engine import ConvConfig, _input_dtype, _output_dtype, get_plan
+from .transforms import TransformSet
+
+_ws_lock = threading.Lock()
+_workspaces: dict = {}
+
+
+def _workspace(nbytes: int):
+    """Per-device grow-only scratch for U, V and M."""
+    dev = D.torch.cuda.current_device()
+    with _ws_lock:
+        buf = _workspaces.get(dev)
+        if buf is None or buf.numel() < nbytes:
+            buf = D.torch.empty(max(nbytes, 1 << 20), dtype=D.torch.uint8, device=f"cuda:{dev}")
+            _workspaces[dev] = buf
+        return buf
+
+
+class LayerOp:
+    """One layer geometry bound to a compiled plan (reusable across calls)."""
+
+    def __init__(self, ts: TransformSet, cfg: ConvConfig, N, C, H, W, K, pad, contraction="exact"):
+        if pad < 0:
+            raise ValueError("pad must be >= 0")
+        self.ts, self.cfg, self.contraction = ts, cfg, contraction
+        self.plan = get_plan(ts, cfg, contraction)
+        self.shape = _native.LayerShape(N, C, H, W, K, pad)
+        self.layout = self.plan.layout(N, C, H, W, K, pad)
+        self.N, self.C, self.H, self.W, self.K, self.pad = N, C, H, W, K, pad
+        self.out_shape = (N, K, self.layout.Ho, self.layout.Wo)
+        self.in_dtype = _input_dtype(cfg)
+        self.out_dtype = _output_dtype(cfg)
+
+    @property
+    def direct_flops(self) -> int:
+        """Direct-convolution-equivalent FLOPs, 2 N K C Ho Wo r^2."""
+        r = self.ts.n_h
+        return 2 * self.N * self.K * self.C * self.layout.Ho * self.layout.Wo * r * r
+
+    @property
+    def contraction_flops(self) -> int:
+        L = self.layout
+        return 2 * L.P * L.T * self.C * self.K
+
+    def __call__(self, x, w, out=None, workspace=None, stream=None):
+        """x, w: contiguous CUDA tensors of the plan's input dtype."""
+        L = self.layout
+        if out is None:
+            out = D.empty(self.out_shape, self.out_dtype)
+        ws = workspace if workspace is not None else _workspace(L.workspace_bytes)
+        s = D.stream_handle() if stream is None else stream
+        _native.check(_native.lib().wino_conv2d(self.plan.handle, ctypes.byref(self.shape), D.ptr(x), D.ptr(w),
+                                                D.ptr(out), D.ptr(ws), ws.numel(), s), "conv2d")
+        return out
+
+    # -- individual stages (tests, profiling) --------------------------------
+    def _uv_dtype(self):
+        return D.torch.float64 if self.cfg.precision == "fp64" else D.torch.float32
+
+    def filter_transform(self, w):
+        L = self.layout
+        U = D.torch.empty((L.P, L.Cp, L.Kp), dtype=self._uv_dtype(), device="cuda")
+        _native.check(_native.lib().wino_filter_transform(self.plan.handle, ctypes.byref(self.shape), D.ptr(w),
+                                                          D.ptr(U), D.stream_handle()), "filter_transform")
+        return U
+
+    def input_transform(self, x):
+        L = self.layout
+        V = D.torch.empty((L.P, L.Cp, L.Tp), dtype=self._uv_dtype(), device="cuda")
+        _native.check(_native.lib().wino_input_transform(self.plan.handle, ctypes.byref(self.shape), D.ptr(x),
+                                                         D.ptr(V), D.stream_handle()), "input_transform")
+        return V
+
+    def contract(self, U, V):
+        L = self.layout
+        M = D.torch.empty((L.P, L.Kp, L.Tp), dtype=self._uv_dtype(), device="cuda")
+        _native.check(_native.lib().wino_contract(self.plan.handle, ctypes.byref(self.shape), D.ptr(U), D.ptr(V),
+                                                  D.ptr(M), D.stream_handle()), "contract")
+        return M
+
+    def output_transform(self, M, out=None):
+        if out is None:
+            out = D.empty(self.out_shape, self.out_dtype)
+        _native.check(_native.lib().wino_output_transform(self.plan.handle, ctypes.byref(self.shape), D.ptr(M),
+                                                          D.ptr(out), D.stream_handle()), "output_transform")
+        return out
+
+
+_ops_lock = threading.Lock()
+
+
+def layer_op(ts, cfg, N, C, H, W, K, pad, contraction="exact") -> LayerOp:
+    key = ("layer_op", cfg, contraction, N, C, H, W, K, pad)
+    with _ops_lock:
+        op = ts._programs.get(key)
+        if op is None:
+            op = LayerOp(ts, cfg, N, C, H, W, K, pad, contraction)
+            ts._programs[key] = op
+    return op
+
+
+def conv2d_layer(ts: TransformSet, x, w, cfg: ConvConfig = ConvConfig(), pad: int = 0,
+                 contraction: str = "exact"):
+    """Winograd F(m x m, r x r) convolution layer (stride 1, zero padding `pad`).
+
+    x (N, C, H, W), w (K, C, r, r) -> y (N, K, Ho, Wo): numpy in -> numpy out
+    (host<->device copies included), CUDA tensors in -> CUDA tensor out.
+    Output dtype f32 in fp32 mode, f64 in mixed / fp64 mode (reference engine.py:378-387)."""
+    xs, wsh = tuple(D.shape_of(x)), tuple(D.shape_of(w))
+    if len(xs) != 4 or len(wsh) != 4:
+        raise ValueError("x must be (N, C, H, W) and w (K, C, r, r)")
+    N, C, H, W = xs
+    K, C2, r1, r2 = wsh
+    if C2 != C:
+        raise ValueError("x and w disagree on the channel count")
+    if r1 != ts.n_h or r2 != ts.n_h:
+        raise ValueError(f"filter must be {ts.n_h}x{ts.n_h} for this transform set")
+    op = layer_op(ts, cfg, N, C, H, W, K, pad, contraction)
+    xt, hx = D.to_device(x, op.in_dtype)
+    wt, hw = D.to_device(w, op.in_dtype)
+    return D.finish(op(xt, wt), hx or hw)
+
+
+def direct_layer_f64(x, w, pad: int):
+    """fp64 direct correlation of a layer on the device (the error oracle):
+    per output, per channel the r*r taps in row-major order, channels left to
+    right -- reference direct_products + channel_reduce("linear")."""
+    xt, hx = D.to_device(x, np.float32)
+    wt, hw = D.to_device(w, np.float32)
+    N, C, H, W = xt.shape
+    K, _, r, _ = wt.shape
+    Ho, Wo = H + 2 * pad - r + 1, W + 2 * pad - r + 1
+    y = D.empty((N, K, Ho, Wo), np.float64)
+    s = _native.LayerShape(N, C, H, W, K, pad)
+    _native.check(_native.lib().wino_direct_layer_f64(ctypes.byref(s), r, D.ptr(xt), D.ptr(wt), D.ptr(y),
+                                                      D.stream_handle()), "direct_layer_f64")
+    return D.finish(y, hx or hw)
+
+
+def layer_error_stats(y, y64):
+    """Per-image (sum|y - y64|, sum|y64|, count, max|y - y64|) on the device -> (N, 4) f64."""
+    yt = y if isinstance(y, D.torch.Tensor) else D.to_device(y, np.asarray(y).dtype.type)[0]
+    rt = y64 if isinstance(y64, D.torch.Tensor) else D.to_device(y64, np.float64)[0]
+    N = yt.shape[0]
+    per = int(yt.numel() // max(N, 1))
+    stats = D.empty((N, 4), np.float64)
+    _native.check(_native.lib().wino_layer_error_stats(N, per, 0 if yt.dtype == D.torch.float32 else 1,
+                                                       D.ptr(yt), D.ptr(rt), D.ptr(stats), D.stream_handle()),
+                  "layer_error_stats")
+    return stats

@@ -1,0 +1,126 @@
+"""GPU parity of the layer-level hot path (K1-K4 through the C-ABI) against the
+reference's own numbers (golden fixtures) and the CPU oracle, bit for bit."""
+
+import numpy as np
+import pytest
+
+import _golden as G
+from oracle import wino_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+W = pytest.importorskip("paper_1803_10986_b200")
+torch = pytest.importorskip("torch")
+
+
+def _ts(name):
+    d = G.transforms()[name]
+    return W.build_transforms(d["r"], d["m"], W.parse_points(d["points"])), O.Triple.from_points(d["r"], d["m"], d["points"])
+
+
+LAYER = G.cases("layer_cases.json")
+
+
+@pytest.mark.parametrize("case", LAYER["cases"], ids=lambda c: c["name"])
+def test_layer_golden_bitwise(case):
+    arr = G.npz("layer.npz")
+    ts, _ = _ts(case["ts"])
+    x, w = arr[case["name"] + "/x"], arr[case["name"] + "/w"]
+    for prec, order, cs in LAYER["modes"]:
+        y = W.conv2d_layer(ts, x, w, W.ConvConfig(prec, order, cs), pad=case["pad"])
+        want = arr[f"{case['name']}/{prec}-{order}-{cs}/y"]
+        assert G.same_bits(y, want), (prec, order, cs, np.abs(y.astype(np.float64) - want).max())
+    y64 = W.direct_layer_f64(x, w, case["pad"])
+    assert G.same_bits(y64, arr[case["name"] + "/y64"])
+
+
+RANDOM_CASES = [
+    # r, m, points, N, C, K, H, W, pad
+    (3, 2, "0,1,-1,inf", 3, 33, 70, 15, 17, 1),
+    (3, 4, "0,1,-1,1/2,-1/2,inf", 2, 64, 64, 20, 20, 1),
+    (3, 6, "0,-1,1,1/2,-1/2,2,-2,inf", 1, 40, 130, 29, 23, 1),
+    (3, 7, "0,-1,1,1/2,-1/2,2,-2,-1/4,inf", 2, 9, 5, 16, 16, 0),
+    (5, 2, "0,-1,1,1/2,-2,inf", 2, 20, 12, 14, 14, 2),
+    (3, 3, "0,1,-1,2,-2", 1, 3, 64, 30, 30, 1),
+    (2, 3, "0,1,-1,inf", 2, 7, 9, 11, 11, 0),
+]
+
+
+@pytest.mark.parametrize("case", RANDOM_CASES, ids=lambda c: f"r{c[0]}m{c[1]}C{c[4]}K{c[5]}")
+@pytest.mark.parametrize("mode", [("fp32", "huffman", "linear"), ("fp32", "linear", "pairwise"),
+                                  ("mixed", "huffman", "pairwise"), ("fp64", "linear", "linear")],
+                         ids=lambda m: "-".join(m))
+def test_layer_vs_oracle(case, mode):
+    r, m, pts, N, C, K, H, Wd, pad = case
+    ts = W.build_transforms(r, m, W.parse_points(pts))
+    trip = O.Triple.from_points(r, m, pts)
+    x = O.synthetic((N, C, H, Wd), 7, 0)
+    w = O.synthetic((K, C, r, r), 7, 99)
+    y = W.conv2d_layer(ts, x, w, W.ConvConfig(*mode), pad=pad)
+    want = O.layer_conv2d(trip, x, w, pad, *mode)
+    assert G.same_bits(y, want)
+
+
+def test_stages_match_oracle_pieces():
+    """U and V of the generated transforms equal the oracle's (G w G^T) and
+    (B^T d B); padded channels hold +0 (U) and -0 (V)."""
+    pts = "0,1,-1,1/2,-1/2,inf"
+    ts = W.build_transforms(3, 4, W.parse_points(pts))
+    trip = O.Triple.from_points(3, 4, pts)
+    x = O.synthetic((2, 5, 9, 9), 3, 0)
+    w = O.synthetic((3, 5, 3, 3), 3, 1)
+    cfg = W.ConvConfig()
+    op = W.layer_op(ts, cfg, 2, 5, 9, 9, 3, 1)
+    L = op.layout
+    U = op.filter_transform(torch.from_numpy(w).cuda()).cpu().numpy()
+    V = op.input_transform(torch.from_numpy(x).cuda()).cpu().numpy()
+    u_or = O.apply_2d(trip, "G", "huffman", "fp32", w)                     # [K, C, n, n]
+    assert G.same_bits(U[:, :5, :3].reshape(6, 6, 5, 3).transpose(3, 2, 0, 1).copy(), u_or)
+    assert np.all(U[:, 5:, :] == 0) and not np.any(np.signbit(U[:, 5:, :]))
+    tiles = O.gather_tiles(x, 3, 4, 1)                                    # [T, C, n, n]
+    v_or = O.apply_2d(trip, "B_T", "huffman", "fp32", tiles)
+    T = tiles.shape[0]
+    assert G.same_bits(V[:, :5, :T].reshape(6, 6, 5, T).transpose(3, 2, 0, 1).copy(), v_or)
+    assert np.all(np.signbit(V[:, 5:, :T]))
+    assert L.Cp % 8 == 0 and L.Tp >= T
+
+
+@pytest.mark.parametrize("cfgname", ["cfg1", "cfg2"])
+def test_full_size_configs_bitwise(cfgname):
+    """BASELINE configs 1 and 2 at full size, compared with the oracle bit for bit."""
+    if cfgname == "cfg1":
+        r, m, pts, N, C, K, H = 3, 4, "0,1,-1,1/2,-1/2,inf", 8, 64, 64, 56
+        w = O.synthetic((K, C, r, r), 2024, 10_000_000)
+    else:
+        r, m, pts, N, C, K, H = 3, 2, "0,1,-1,inf", 32, 128, 128, 28
+        w = (O.synthetic((K, C, r, r), 2024, 10_000_000, "normal") * np.float32(np.sqrt(2.0 / (9 * C))))
+    x = np.stack([O.synthetic((C, H, H), 2024, i) for i in range(N)])
+    ts = W.build_transforms(r, m, W.parse_points(pts))
+    trip = O.Triple.from_points(r, m, pts)
+    y = W.conv2d_layer(ts, x, w, W.ConvConfig(), pad=1)
+    want = O.layer_conv2d(trip, x, w, 1)
+    assert G.same_bits(y, want)
+    # error statistics vs fp64 direct agree to far better than 2 significant digits
+    y64 = W.direct_layer_f64(x, w, 1)
+    y64o = O.layer_direct_fp64(x[:1], w, 1)
+    assert G.same_bits(y64[:1], y64o)
+
+
+def test_device_tensors_in_device_tensor_out():
+    ts = W.build_transforms(3, 2, W.parse_points("0,1,-1,inf"))
+    x = torch.randn(2, 4, 10, 10, device="cuda")
+    w = torch.randn(3, 4, 3, 3, device="cuda")
+    y = W.conv2d_layer(ts, x, w, pad=1)
+    assert isinstance(y, torch.Tensor) and y.is_cuda and y.shape == (2, 3, 10, 10)
+    ref = torch.nn.functional.conv2d(x.double(), w.double(), padding=1)
+    assert torch.allclose(y.double(), ref, atol=1e-4)
+
+
+def test_layer_validation_errors():
+    ts = W.build_transforms(3, 2, W.parse_points("0,1,-1,inf"))
+    with pytest.raises(ValueError):
+        W.conv2d_layer(ts, np.zeros((1, 2, 5, 5), np.float32), np.zeros((1, 3, 3, 3), np.float32))
+    with pytest.raises(ValueError):
+        W.conv2d_layer(ts, np.zeros((1, 2, 5, 5), np.float32), np.zeros((1, 2, 5, 5), np.float32))
+    with pytest.raises(ValueError):
+        W.conv2d_layer(ts, np.zeros((1, 2, 2, 2), np.float32), np.zeros((1, 2, 3, 3), np.float32), pad=0)
