@@ -240,16 +240,23 @@ def run_gpu(args, cfg):
     torch.cuda.synchronize()
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    n0 = _native.launch_count()
     with ClockSampler(local) as clk:
+        # keep the GPU busy with the same workload for ~1.5 s so the clock
+        # sampler sees the load the timed region runs under
+        t_end = time.perf_counter() + args.soak
+        while time.perf_counter() < t_end:
+            for _ in range(50):
+                step()
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        n0 = _native.launch_count()
         for i in range(args.steps):
             flush.zero_()  # evict L2 (outside the timed interval of the step)
             step(evs[i])
         torch.cuda.synchronize()
-    n_launch = _native.launch_count() - n0
+        n_launch = _native.launch_count() - n0
     if world > 1:
         dist.barrier()
     stage = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(4)] for i in range(args.steps)])
@@ -393,6 +400,7 @@ def main():
     ap.add_argument("--contraction", default="exact", choices=["exact", "ffma"])
     ap.add_argument("--cpu-images", type=int, default=32)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--soak", type=float, default=1.5, help="seconds of untimed load before the timed region")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

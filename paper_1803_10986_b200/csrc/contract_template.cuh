@@ -25,10 +25,11 @@
 //              occupied slots from the smallest block upwards.
 // Padded channels (c >= C) carry -0 products and leave every sum unchanged.
 //
-// Data movement: one thread issues cp.async.bulk (TMA bulk copies, SASS UBLKCP)
-// of every BM- and BN-wide channel row of a stage into shared memory, tracked by
-// an mbarrier per stage (complete_tx); the CTA consumes stage s while the next
-// WINO_STAGES-1 stages are in flight.
+// Data movement: a producer warp issues cp.async.bulk (TMA bulk copies, SASS
+// UBLKCP) of every BM- and BN-wide channel row of a stage into shared memory,
+// tracked by a "full" mbarrier per stage (complete_tx); consumer warps release
+// a stage through its "empty" mbarrier, so up to WINO_STAGES stages are in
+// flight and the main loop has no CTA-wide barrier.
 
 #define DT WINO_DT
 #define BM (WINO_THM * WINO_TM)
@@ -79,45 +80,66 @@ static __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsi
         : "memory");
 }
 
-extern "C" __global__ void __launch_bounds__(NTHR) wino_contract(const DT* __restrict__ U,
-                                                               const DT* __restrict__ V,
-                                                               DT* __restrict__ M, long long Kp,
-                                                               long long Tp, long long Cp) {
+static __device__ __forceinline__ void mbar_arrive(u64* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Warp-specialised: warps 0 .. NCW-1 consume (register-blocked FP32/FP64
+// math), the last warp produces (bulk copies).  full[s] completes when the
+// stage's bytes have landed; empty[s] when every consumer warp has finished
+// reading it.  No CTA-wide barrier in the main loop.
+#define NCW (NTHR / 32)
+extern "C" __global__ void __launch_bounds__(NTHR + 32) wino_contract(const DT* __restrict__ U,
+                                                                    const DT* __restrict__ V,
+                                                                    DT* __restrict__ M, long long Kp,
+                                                                    long long Tp, long long Cp) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     DT* sU = reinterpret_cast<DT*>(smem_raw);      // [STAGES][BK][BM]
     DT* sV = sU + WINO_STAGES * WINO_BK * BM;      // [STAGES][BK][BN]
-    u64* bar = reinterpret_cast<u64*>(sV + WINO_STAGES * WINO_BK * BN);
+    u64* full = reinterpret_cast<u64*>(sV + WINO_STAGES * WINO_BK * BN);
+    u64* empty = full + WINO_STAGES;
 
     const int tid = threadIdx.x;
-    const int tn = tid % WINO_THN;
-    const int tm = tid / WINO_THN;
+    const int warp = tid >> 5, lane = tid & 31;
     const long long p = blockIdx.z;
     const long long k0 = (long long)blockIdx.y * BM;
     const long long t0 = (long long)blockIdx.x * BN;
-    const DT* gU = U + p * Cp * Kp + k0;
-    const DT* gV = V + p * Cp * Tp + t0;
     const int nk = (int)(Cp / WINO_BK);
 
     if (tid == 0) {
 #pragma unroll
-        for (int s = 0; s < WINO_STAGES; ++s) mbar_init(&bar[s], 1);
+        for (int s = 0; s < WINO_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
-    auto issue = [&](int kt) {
-        const int s = kt % WINO_STAGES;
-        mbar_expect_tx(&bar[s], (unsigned)(WINO_BK * (BM + BN) * sizeof(DT)));
+    if (warp == NCW) {
+        // ---------------- producer warp: lane r copies channel row r of U and V
+        const DT* gU = U + p * Cp * Kp + k0;
+        const DT* gV = V + p * Cp * Tp + t0;
 #pragma unroll 1
-        for (int r = 0; r < WINO_BK; ++r) {
-            const long long c = (long long)kt * WINO_BK + r;
-            bulk_g2s(sU + (s * WINO_BK + r) * BM, gU + c * Kp, BM * sizeof(DT), &bar[s]);
-            bulk_g2s(sV + (s * WINO_BK + r) * BN, gV + c * Tp, BN * sizeof(DT), &bar[s]);
+        for (int kt = 0; kt < nk; ++kt) {
+            const int s = kt % WINO_STAGES;
+            if (kt >= WINO_STAGES) mbar_wait(&empty[s], (unsigned)(((kt / WINO_STAGES) - 1) & 1));
+            if (lane == 0) mbar_expect_tx(&full[s], (unsigned)(WINO_BK * (BM + BN) * sizeof(DT)));
+            __syncwarp();
+            for (int r = lane; r < 2 * WINO_BK; r += 32) {
+                const int row = r % WINO_BK;
+                const long long c = (long long)kt * WINO_BK + row;
+                if (r < WINO_BK)
+                    bulk_g2s(sU + (s * WINO_BK + row) * BM, gU + c * Kp, BM * sizeof(DT), &full[s]);
+                else
+                    bulk_g2s(sV + (s * WINO_BK + row) * BN, gV + c * Tp, BN * sizeof(DT), &full[s]);
+            }
         }
-    };
-    if (tid == 0) {
-        for (int kt = 0; kt < WINO_STAGES - 1 && kt < nk; ++kt) issue(kt);
+        return;
     }
+
+    const int tn = tid % WINO_THN;
+    const int tm = tid / WINO_THN;
 
 #if WINO_SUM == 0
     DT acc[WINO_TM][WINO_TN];
@@ -141,10 +163,8 @@ extern "C" __global__ void __launch_bounds__(NTHR) wino_contract(const DT* __res
 
 #pragma unroll 1
     for (int kt = 0; kt < nk; ++kt) {
-        __syncthreads();  // every thread is done with the stage refilled below
-        if (tid == 0 && kt + WINO_STAGES - 1 < nk) issue(kt + WINO_STAGES - 1);
         const int s = kt % WINO_STAGES;
-        mbar_wait(&bar[s], (unsigned)((kt / WINO_STAGES) & 1));
+        mbar_wait(&full[s], (unsigned)((kt / WINO_STAGES) & 1));
         const DT* cu = sU + s * WINO_BK * BM;
         const DT* cv = sV + s * WINO_BK * BN;
 #pragma unroll
@@ -216,6 +236,8 @@ extern "C" __global__ void __launch_bounds__(NTHR) wino_contract(const DT* __res
             }
 #endif
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
     }
 
 #if WINO_SUM == 1 || WINO_SUM == 3

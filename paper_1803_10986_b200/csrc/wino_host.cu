@@ -303,11 +303,11 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
     p->ty.uv_double = dbl64;
     p->ty.y_double = precision != WINO_FP32;
     if (dbl64)
-        p->gemm = {4, 4, 16, 16, 8, 4};
+        p->gemm = {4, 4, 16, 16, 16, 4};
     else if (channel_sum == WINO_SUM_PAIRWISE)
-        p->gemm = {4, 4, 16, 16, 8, 4};
+        p->gemm = {4, 4, 16, 16, 16, 4};
     else
-        p->gemm = {8, 8, 16, 16, 8, 4};
+        p->gemm = {8, 8, 16, 16, 16, 4};
     const std::string tag = "r" + std::to_string(r) + "m" + std::to_string(m) + "p" + std::to_string(precision);
     p->layer.name = "wino_layer_" + tag + ".cu";
     p->layer.source = wino::gen_layer_source(r, m, p->G, p->BT, p->AT, p->ty);
@@ -385,9 +385,9 @@ int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, con
     const wino::GemmCfg& g = plan->gemm;
     long long Kp = L.Kp, Tp = L.Tp, Cp = L.Cp;
     void* args[] = {(void*)&U, (void*)&V, &M, &Kp, &Tp, &Cp};
-    const unsigned smem = (unsigned)(g.stages * g.bk * (g.bm() + g.bn()) * L.elem_bytes_uv + g.stages * 8);
+    const unsigned smem = (unsigned)(g.stages * g.bk * (g.bm() + g.bn()) * L.elem_bytes_uv + 2 * g.stages * 8);
     return wino::launch(f, dim3((unsigned)(Tp / g.bn()), (unsigned)(Kp / g.bm()), (unsigned)L.P),
-                        dim3(g.threads()), smem, stream, args, "contract");
+                        dim3(g.threads() + 32), smem, stream, args, "contract");
 }
 
 int wino_output_transform(wino_plan* plan, const wino_layer_shape* s, const void* M, void* y, void* stream) {
