@@ -77,14 +77,18 @@ typedef struct {
 } wino_layer_shape;
 
 /* Device layout of the Winograd-domain tensors for one layer (HBM):
- *   U [P][Cp][Kp]  filter transform      (P = alpha^2)
- *   V [P][Cp][Tp]  input-tile transform  (T = N * th * tw tiles, t = (n, i, j))
- *   M [P][Kp][Tp]  channel contraction
+ *   U [P][Kp/bm][Cp][bm]  filter transform, blocked by the contraction's
+ *                         k-tile (P = alpha^2)
+ *   V [P][Tp/bn][Cp][bn]  input-tile transform, blocked by the t-tile
+ *                         (T = N * th * tw tiles, t = (n, i, j))
+ *   M [P][Kp][Tp]         channel contraction
+ * so one pipeline stage of a contraction tile is one contiguous block.
  * Cp/Kp/Tp are padded to the contraction kernel's tile sizes; padded channels
  * hold +0 (U) and -0 (V) so their products are -0 and leave every sum
  * bit-identical. */
 typedef struct {
     int32_t P, th, tw, Ho, Wo;
+    int32_t bm, bn; /* U / V block widths */
     int64_t T, Tp, Cp, Kp;
     int32_t elem_bytes_uv;  /* 4 (fp32, mixed) or 8 (fp64) */
     int32_t elem_bytes_y;   /* 4 (fp32) or 8 (mixed, fp64) */

@@ -37,7 +37,7 @@ class LayerShape(ctypes.Structure):
 
 class LayerLayout(ctypes.Structure):
     _fields_ = [("P", c_int32), ("th", c_int32), ("tw", c_int32), ("Ho", c_int32), ("Wo", c_int32),
-                ("T", c_int64), ("Tp", c_int64), ("Cp", c_int64), ("Kp", c_int64),
+                ("bm", c_int32), ("bn", c_int32), ("T", c_int64), ("Tp", c_int64), ("Cp", c_int64), ("Kp", c_int64),
                 ("elem_bytes_uv", c_int32), ("elem_bytes_y", c_int32),
                 ("u_bytes", c_size_t), ("v_bytes", c_size_t), ("m_bytes", c_size_t),
                 ("workspace_bytes", c_size_t)]

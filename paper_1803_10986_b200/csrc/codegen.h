@@ -36,8 +36,11 @@ struct GenTypes {
 // validate the stack discipline of a program; returns "" or an error message
 std::string validate(const MatProg& m, int expect_rows, int expect_cols, const char* name);
 
+// U and V are written in the contraction's blocked layout:
+//   U[p][k / bm][c][k % bm],  V[p][t / bn][c][t % bn]
+// so one pipeline stage of a contraction tile is a single contiguous block.
 std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
-                             const GenTypes& ty);
+                             const GenTypes& ty, int bm, int bn);
 std::string gen_tile_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
                             const GenTypes& ty);
 

@@ -26,7 +26,7 @@
 // Padded channels (c >= C) carry -0 products and leave every sum unchanged.
 //
 // Data movement: a producer warp issues cp.async.bulk (TMA bulk copies, SASS
-// UBLKCP) of every BM- and BN-wide channel row of a stage into shared memory,
+// UBLKCP) of the stage's contiguous U and V blocks into shared memory,
 // tracked by a "full" mbarrier per stage (complete_tx); consumer warps release
 // a stage through its "empty" mbarrier, so up to WINO_STAGES stages are in
 // flight and the main loop has no CTA-wide barrier.
@@ -89,7 +89,12 @@ static __device__ __forceinline__ void mbar_arrive(u64* bar) {
 // stage's bytes have landed; empty[s] when every consumer warp has finished
 // reading it.  No CTA-wide barrier in the main loop.
 #define NCW (NTHR / 32)
-extern "C" __global__ void __launch_bounds__(NTHR + 32) wino_contract(const DT* __restrict__ U,
+#if WINO_MAXREG > 0
+#define WINO_REGS __maxnreg__(WINO_MAXREG)
+#else
+#define WINO_REGS __launch_bounds__(NTHR + 32)
+#endif
+extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U,
                                                                     const DT* __restrict__ V,
                                                                     DT* __restrict__ M, long long Kp,
                                                                     long long Tp, long long Cp) {
@@ -117,22 +122,19 @@ extern "C" __global__ void __launch_bounds__(NTHR + 32) wino_contract(const DT* 
     __syncthreads();
 
     if (warp == NCW) {
-        // ---------------- producer warp: lane r copies channel row r of U and V
-        const DT* gU = U + p * Cp * Kp + k0;
-        const DT* gV = V + p * Cp * Tp + t0;
+        // ---------------- producer warp.  U and V are stored blocked
+        // (U[p][k/BM][c][k%BM], V[p][t/BN][c][t%BN]) so a stage of this tile is
+        // one contiguous block per operand: two bulk copies per stage.
+        if (lane == 0) {
+            const DT* gU = U + p * Cp * Kp + (long long)blockIdx.y * Cp * BM;
+            const DT* gV = V + p * Cp * Tp + (long long)blockIdx.x * Cp * BN;
 #pragma unroll 1
-        for (int kt = 0; kt < nk; ++kt) {
-            const int s = kt % WINO_STAGES;
-            if (kt >= WINO_STAGES) mbar_wait(&empty[s], (unsigned)(((kt / WINO_STAGES) - 1) & 1));
-            if (lane == 0) mbar_expect_tx(&full[s], (unsigned)(WINO_BK * (BM + BN) * sizeof(DT)));
-            __syncwarp();
-            for (int r = lane; r < 2 * WINO_BK; r += 32) {
-                const int row = r % WINO_BK;
-                const long long c = (long long)kt * WINO_BK + row;
-                if (r < WINO_BK)
-                    bulk_g2s(sU + (s * WINO_BK + row) * BM, gU + c * Kp, BM * sizeof(DT), &full[s]);
-                else
-                    bulk_g2s(sV + (s * WINO_BK + row) * BN, gV + c * Tp, BN * sizeof(DT), &full[s]);
+            for (int kt = 0; kt < nk; ++kt) {
+                const int s = kt % WINO_STAGES;
+                if (kt >= WINO_STAGES) mbar_wait(&empty[s], (unsigned)(((kt / WINO_STAGES) - 1) & 1));
+                mbar_expect_tx(&full[s], (unsigned)(WINO_BK * (BM + BN) * sizeof(DT)));
+                bulk_g2s(sU + s * WINO_BK * BM, gU + (long long)kt * WINO_BK * BM, WINO_BK * BM * sizeof(DT), &full[s]);
+                bulk_g2s(sV + s * WINO_BK * BN, gV + (long long)kt * WINO_BK * BN, WINO_BK * BN * sizeof(DT), &full[s]);
             }
         }
         return;

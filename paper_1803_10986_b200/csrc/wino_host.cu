@@ -10,6 +10,8 @@
 #include <nvrtc.h>
 
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -85,13 +87,15 @@ struct Compiled {
     std::string log;
 };
 
-static int nvrtc_compile(const std::string& src, const std::string& name, Compiled* out) {
+static int nvrtc_compile(const std::string& src, const std::string& name, Compiled* out, int maxreg = 0) {
     nvrtcProgram prog;
     nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), name.c_str(), 0, nullptr, nullptr);
     if (r != NVRTC_SUCCESS) return fail(WINO_ECOMPILE, std::string("nvrtcCreateProgram: ") + nvrtcGetErrorString(r));
-    const char* opts[] = {"-arch=sm_100a", "-fmad=false", "-lineinfo", "-std=c++17", "-default-device",
-                          "--ptxas-options=-v"};
-    r = nvrtcCompileProgram(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
+    std::vector<const char*> opts = {"-arch=sm_100a", "-fmad=false", "-lineinfo", "-std=c++17", "-default-device",
+                                     "--ptxas-options=-v"};
+    std::string mr = "-maxrregcount=" + std::to_string(maxreg);
+    if (maxreg > 0) opts.push_back(mr.c_str());
+    r = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
     size_t ls = 0;
     nvrtcGetProgramLogSize(prog, &ls);
     out->log.assign(ls, '\0');
@@ -111,6 +115,7 @@ static int nvrtc_compile(const std::string& src, const std::string& name, Compil
 // A generated module: source, cubin, and per-device loaded CUmodule/functions.
 struct Module {
     std::string name, source;
+    int maxreg = 0;  // NVRTC -maxrregcount (0 = compiler default)
     Compiled bin;
     bool compiled = false;
     std::mutex mu;
@@ -120,7 +125,7 @@ struct Module {
     int ensure_compiled() {
         std::lock_guard<std::mutex> g(mu);
         if (compiled) return WINO_OK;
-        int rc = nvrtc_compile(source, name, &bin);
+        int rc = nvrtc_compile(source, name, &bin, maxreg);
         if (rc == WINO_OK) compiled = true;
         return rc;
     }
@@ -175,7 +180,7 @@ static const char* kContractTemplate =
     ;
 
 struct GemmCfg {
-    int tm, tn, thm, thn, bk, stages;
+    int tm, tn, thm, thn, bk, stages, maxreg;
     int bm() const { return thm * tm; }
     int bn() const { return thn * tn; }
     int threads() const { return thm * thn; }
@@ -210,7 +215,7 @@ struct wino_plan {
            << "\n#define WINO_TM " << gemm.tm << "\n#define WINO_TN " << gemm.tn << "\n#define WINO_THM " << gemm.thm
            << "\n#define WINO_THN " << gemm.thn << "\n#define WINO_BK " << gemm.bk << "\n#define WINO_STAGES "
            << gemm.stages << "\n#define WINO_SUM " << sum_mode() << "\n#define WINO_LEVELS "
-           << (levels > 0 ? levels : 1) << "\n"
+           << (levels > 0 ? levels : 1) << "\n#define WINO_MAXREG " << gemm.maxreg << "\n"
            << wino::kContractTemplate;
         mod->source = os.str();
         mod->name = "wino_contract_s" + std::to_string(sum_mode()) + "_L" + std::to_string(levels) + ".cu";
@@ -245,6 +250,8 @@ int layout_of(const wino_plan* p, const wino_layer_shape* s, wino_layer_layout* 
     if (Ho < 1 || Wo < 1) return wino::fail(WINO_EINVAL, "input smaller than kernel");
     std::memset(L, 0, sizeof *L);
     L->P = p->n * p->n;
+    L->bm = p->gemm.bm();
+    L->bn = p->gemm.bn();
     L->Ho = Ho;
     L->Wo = Wo;
     L->th = (Ho + p->m - 1) / p->m;
@@ -302,15 +309,24 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
     p->ty.in_double = dbl64;
     p->ty.uv_double = dbl64;
     p->ty.y_double = precision != WINO_FP32;
+    // Tile configs {tm, tn, thm, thn, bk, stages, maxreg} picked by tools/contract_bench.py
+    // sweeps on B200 (profiles/): 4 consumer warps + 1 producer warp per CTA,
+    // so three CTAs (15 warps) fit per SM within the per-SMSP register file.
     if (dbl64)
-        p->gemm = {4, 4, 16, 16, 16, 4};
+        p->gemm = {4, 4, 8, 16, 16, 4, 0};
     else if (channel_sum == WINO_SUM_PAIRWISE)
-        p->gemm = {4, 4, 16, 16, 16, 4};
+        p->gemm = {4, 4, 8, 16, 32, 4, 168};
     else
-        p->gemm = {8, 8, 16, 16, 16, 4};
+        p->gemm = {8, 8, 16, 8, 16, 4, 0};
+    if (const char* env = getenv("WINO_GEMM")) {  // tuning override: tm,tn,thm,thn,bk,stages,maxreg
+        wino::GemmCfg g{};
+        if (sscanf(env, "%d,%d,%d,%d,%d,%d,%d", &g.tm, &g.tn, &g.thm, &g.thn, &g.bk, &g.stages, &g.maxreg) == 7 &&
+            g.bk % 8 == 0 && g.tm % 4 == 0 && g.tn % 4 == 0)
+            p->gemm = g;
+    }
     const std::string tag = "r" + std::to_string(r) + "m" + std::to_string(m) + "p" + std::to_string(precision);
     p->layer.name = "wino_layer_" + tag + ".cu";
-    p->layer.source = wino::gen_layer_source(r, m, p->G, p->BT, p->AT, p->ty);
+    p->layer.source = wino::gen_layer_source(r, m, p->G, p->BT, p->AT, p->ty, p->gemm.bm(), p->gemm.bn());
     p->tile.name = "wino_tile_" + tag + ".cu";
     p->tile.source = wino::gen_tile_source(r, m, p->G, p->BT, p->AT, p->ty);
     int rc = p->layer.ensure_compiled();

@@ -93,6 +93,16 @@ class LayerOp:
                                                          D.ptr(V), D.stream_handle()), "input_transform")
         return V
 
+    def unblock_u(self, U):
+        """blocked U[P][Kp/bm][Cp][bm] -> U[P][Cp][Kp]"""
+        L = self.layout
+        return U.reshape(L.P, L.Kp // L.bm, L.Cp, L.bm).permute(0, 2, 1, 3).reshape(L.P, L.Cp, L.Kp)
+
+    def unblock_v(self, V):
+        """blocked V[P][Tp/bn][Cp][bn] -> V[P][Cp][Tp]"""
+        L = self.layout
+        return V.reshape(L.P, L.Tp // L.bn, L.Cp, L.bn).permute(0, 2, 1, 3).reshape(L.P, L.Cp, L.Tp)
+
     def contract(self, U, V):
         L = self.layout
         M = D.torch.empty((L.P, L.Kp, L.Tp), dtype=self._uv_dtype(), device="cuda")

@@ -72,8 +72,8 @@ def test_stages_match_oracle_pieces():
     cfg = W.ConvConfig()
     op = W.layer_op(ts, cfg, 2, 5, 9, 9, 3, 1)
     L = op.layout
-    U = op.filter_transform(torch.from_numpy(w).cuda()).cpu().numpy()
-    V = op.input_transform(torch.from_numpy(x).cuda()).cpu().numpy()
+    U = op.unblock_u(op.filter_transform(torch.from_numpy(w).cuda())).cpu().numpy()
+    V = op.unblock_v(op.input_transform(torch.from_numpy(x).cuda())).cpu().numpy()
     u_or = O.apply_2d(trip, "G", "huffman", "fp32", w)                     # [K, C, n, n]
     assert G.same_bits(U[:, :5, :3].reshape(6, 6, 5, 3).transpose(3, 2, 0, 1).copy(), u_or)
     assert np.all(U[:, 5:, :] == 0) and not np.any(np.signbit(U[:, 5:, :]))

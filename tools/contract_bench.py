@@ -1,0 +1,76 @@
+"""Contraction-kernel (K3) micro-benchmark / tuner: times wino_contract alone
+for a layer shape under several tile configurations (WINO_GEMM overrides).
+
+  python tools/contract_bench.py --shape 32,128,28,128 --m 2 --cs linear \
+      --variants "8,8,16,16,16,4,96;8,8,16,16,32,3,96"
+"""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_1803_10986_b200 as W  # noqa: E402
+from paper_1803_10986_b200 import _native, pointsets  # noqa: E402
+
+
+def run(shape, m, r, prec, cs, contraction, variant, reps):
+    if variant:
+        os.environ["WINO_GEMM"] = variant
+    else:
+        os.environ.pop("WINO_GEMM", None)
+    N, C, H, K = shape
+    ts = W.build_transforms(r, m, W.parse_points(pointsets.curated_text(m + r - 1, 2) if r == 3 else
+                                                 pointsets.curated_text(m + r - 1, 2)))
+    op = W.layer_op(ts, W.ConvConfig(prec, "huffman", cs), N, C, H, H, K, 1 if r == 3 else 2, contraction)
+    L = op.layout
+    dt = torch.float64 if prec == "fp64" else torch.float32
+    U = torch.randn((L.P, L.Cp, L.Kp), dtype=dt, device="cuda")
+    V = torch.randn((L.P, L.Cp, L.Tp), dtype=dt, device="cuda")
+    M = torch.empty((L.P, L.Kp, L.Tp), dtype=dt, device="cuda")
+    lib = _native.lib()
+    s = torch.cuda.current_stream().cuda_stream
+
+    def go():
+        _native.check(lib.wino_contract(op.plan.handle, ctypes.byref(op.shape), _native.as_ptr(U),
+                                        _native.as_ptr(V), _native.as_ptr(M), s))
+    for _ in range(3):
+        go()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        go()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    flops = 2 * L.P * L.T * C * K
+    return {"variant": variant or "default", "shape": shape, "m": m, "prec": prec, "cs": cs,
+            "contraction": contraction, "us": ms * 1e3, "tflops": flops / ms / 1e9}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--shape", default="32,128,28,128")
+    ap.add_argument("--m", type=int, default=2)
+    ap.add_argument("--r", type=int, default=3)
+    ap.add_argument("--prec", default="fp32")
+    ap.add_argument("--cs", default="linear")
+    ap.add_argument("--contraction", default="exact")
+    ap.add_argument("--variants", default="")
+    ap.add_argument("--reps", type=int, default=20)
+    a = ap.parse_args()
+    shape = tuple(int(v) for v in a.shape.split(","))
+    for v in ([""] + [x for x in a.variants.split(";") if x]):
+        try:
+            print(json.dumps(run(shape, a.m, a.r, a.prec, a.cs, a.contraction, v, a.reps)), flush=True)
+        except Exception as exc:  # keep sweeping
+            print(json.dumps({"variant": v, "error": str(exc)[:300]}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
