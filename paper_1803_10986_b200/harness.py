@@ -98,7 +98,8 @@ def _chunk_size(trials: int, dims: int, n: int, channels: int) -> int:
     return max(1, min(trials, (64 << 20) // max(per_trial, 1)))
 
 
-def _measure_variants(spec, dims, cfg, trials, seed, channels, variants):
+def _measure_variants(spec, dims, cfg, trials, seed, channels, variants, t0=0):
+    """Trials t0 .. t0+trials-1 (t0 > 0 when a rank evaluates a shard)."""
     direct = isinstance(spec, DirectSpec)
     n_h, n_o, n = spec.n_h, spec.n_o, spec.n
     n_out = n_o ** dims
@@ -108,7 +109,7 @@ def _measure_variants(spec, dims, cfg, trials, seed, channels, variants):
     chunk = _chunk_size(trials, dims, n, channels)
     for s in range(0, trials, chunk):
         B = min(trials, s + chunk) - s
-        h, x = _draw(seed, s, B, dims, n_h, n, channels)
+        h, x = _draw(seed, t0 + s, B, dims, n_h, n, channels)
         ref = _reduce(_direct(h, x, dims, 1), -(dims + 1), "linear")           # fp64 reference
         if direct:
             prods = _direct(h, x, dims, 1 if cfg.precision == "fp64" else 0)

@@ -1,0 +1,64 @@
+"""World-size-2 gloo tests of the multi-GPU host logic (run on CPU)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1803_10986_b200 import distributed as Dd
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, size, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    try:
+        # per-image stats of a 10-image job sharded 2 ways
+        rng = np.random.default_rng(0)
+        full = rng.uniform(0, 1, (10, 4))
+        full[:, 2] = 49.0
+        a, b = Dd.shard_range(10, rank, size)
+        got = Dd.gather_ordered(torch.from_numpy(full[a:b].copy())).numpy()
+        # per-trial vector with uneven shards
+        trials = np.arange(7, dtype=np.float64) * 0.5
+        a2, b2 = Dd.shard_range(7, rank, size)
+        counts = [Dd.shard_range(7, r, size)[1] - Dd.shard_range(7, r, size)[0] for r in range(size)]
+        pt = Dd.gather_ordered(torch.from_numpy(trials[a2:b2].copy()), counts).numpy()
+        mx = Dd.max_over_ranks(float(rank + 3))
+        out[rank] = (got.tobytes() == full.tobytes(), pt.tobytes() == trials.tobytes(), mx,
+                     Dd.combine_layer_stats(got))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world_size_2_gather_and_max():
+    size = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(size, port, out), nprocs=size, join=True)
+    ref = Dd.combine_layer_stats(np.random.default_rng(0).uniform(0, 1, (10, 4)) * [1, 1, 0, 1] + [0, 0, 49, 0])
+    for r in range(size):
+        ok_stats, ok_trials, mx, comb = out[r]
+        assert ok_stats and ok_trials and mx == 4.0
+        assert comb == ref  # identical, bit for bit, to the single-process result
+
+
+def test_shard_range_partitions():
+    for total in (0, 1, 7, 32, 5000):
+        for size in (1, 2, 3, 4, 8):
+            spans = [Dd.shard_range(total, r, size) for r in range(size)]
+            assert spans[0][0] == 0 and spans[-1][1] == total
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(size - 1))
+            assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1
+    assert list(Dd.weak_image_indices(32, 3)) == list(range(96, 128))
+    with pytest.raises(ValueError):
+        Dd.shard_range(10, 2, 2)
