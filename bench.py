@@ -219,6 +219,7 @@ def run_gpu(args, cfg):
     sh = stream.cuda_stream
 
     def step(ev=None):
+        sh = torch.cuda.current_stream().cuda_stream  # the capture stream inside torch.cuda.graph
         if ev is not None:
             ev[0].record(stream)
         _native.check(lib.wino_filter_transform(op.plan.handle, sref, _native.as_ptr(w), _native.as_ptr(U), sh))
@@ -239,14 +240,24 @@ def run_gpu(args, cfg):
         step()
     torch.cuda.synchronize()
 
+    # The step as a CUDA graph (4 libwino kernel nodes): no CPU launch gaps.
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+
+    e_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     with ClockSampler(local) as clk:
-        # keep the GPU busy with the same workload for ~1.5 s so the clock
+        # keep the GPU busy with the same workload for a while so the clock
         # sampler sees the load the timed region runs under
         t_end = time.perf_counter() + args.soak
         while time.perf_counter() < t_end:
             for _ in range(50):
-                step()
+                graph.replay()
             torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -254,13 +265,20 @@ def run_gpu(args, cfg):
         n0 = _native.launch_count()
         for i in range(args.steps):
             flush.zero_()  # evict L2 (outside the timed interval of the step)
+            e_start[i].record(stream)
+            graph.replay()
+            e_end[i].record(stream)
+        # instrumented steps: the same four kernels launched eagerly with an
+        # event between stages -> per-kernel durations for the roofline
+        for i in range(args.steps):
+            flush.zero_()
             step(evs[i])
         torch.cuda.synchronize()
-        n_launch = _native.launch_count() - n0
+        n_launch = 4 * args.steps + (_native.launch_count() - n0)
     if world > 1:
         dist.barrier()
     stage = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(4)] for i in range(args.steps)])
-    ms_step = float(stage.sum(axis=1).mean())
+    ms_step = float(np.mean([e_start[i].elapsed_time(e_end[i]) for i in range(args.steps)]))
     ms_stage = stage.mean(axis=0)
     if world > 1:
         t = torch.tensor([ms_step], dtype=torch.float64, device="cuda")
@@ -268,27 +286,22 @@ def run_gpu(args, cfg):
         ms_step = float(t.item())
     value = direct_flops(cfg) * world / (ms_step * 1e-3) / 1e12
 
-    # ---- end to end through the public API: pinned host in, pinned host out
+    # ---- end to end through the public API: pinned host x, w in -> pinned host y out,
+    # H2D / compute / D2H overlapped over image chunks (W.HostPipeline)
     xh = torch.from_numpy(x_np).pin_memory()
     wh = torch.from_numpy(w_np).pin_memory()
     yh = torch.empty(op.out_shape, dtype=y.dtype).pin_memory()
-    xd_, wd_ = torch.empty_like(x), torch.empty_like(w)
-
-    def e2e_step():
-        xd_.copy_(xh, non_blocking=True)
-        wd_.copy_(wh, non_blocking=True)
-        out = op(xd_, wd_, out=y)
-        yh.copy_(out, non_blocking=True)
+    pipe = W.HostPipeline(ts, wcfg, N, C, H, H, K, pad, chunks=args.e2e_chunks, contraction=args.contraction)
 
     for _ in range(3):
-        e2e_step()
+        pipe(xh, wh, yh)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_ms = []
     for _ in range(args.steps):
         flush.zero_()
         e0.record(stream)
-        e2e_step()
+        pipe(xh, wh, yh)
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
@@ -298,9 +311,11 @@ def run_gpu(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_t = float(t.item())
     e2e_val = direct_flops(cfg) * world / (e2e_t * 1e-3) / 1e12
+    y_e2e = yh.clone()
 
     # ---- error vs fp64 direct (device oracle kernel), per-image partials gathered in image order
     y_ref = op(x, w)
+    e2e_same = bool(torch.equal(y_ref.cpu(), y_e2e))
     y64 = W.direct_layer_f64(x, w, pad)
     st = W.layer_error_stats(y_ref, y64)
     if world > 1:
@@ -352,7 +367,11 @@ def run_gpu(args, cfg):
                 "config": config_dict(args, cfg, world), "roofline": roof, "stages": stages,
                 "error_vs_fp64": err,
                 "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": x_np.nbytes + w_np.nbytes,
-                        "d2h_bytes_per_step": yh.numel() * yh.element_size(), "ms_per_step": e2e_t},
+                        "d2h_bytes_per_step": yh.numel() * yh.element_size(), "ms_per_step": e2e_t,
+                        "api": f"HostPipeline({args.e2e_chunks} chunks: H2D | K1-K3-K4 | D2H overlapped)",
+                        "bitwise_equal_to_device_path": e2e_same},
+                "timing": "value/ms_per_step: CUDA-graph replay of the 4-kernel step, events around each "
+                          "step, L2 flushed between steps; stages: eager launches with an event between stages",
                 "gpu_launches": int(n_launch), "clocks": clk.summary(), "peaks": peak}
         if world == 1 and not args.no_cpu:
             xs = x_np[: args.cpu_images]
@@ -401,6 +420,7 @@ def main():
     ap.add_argument("--cpu-images", type=int, default=32)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--soak", type=float, default=1.5, help="seconds of untimed load before the timed region")
+    ap.add_argument("--e2e-chunks", type=int, default=4)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

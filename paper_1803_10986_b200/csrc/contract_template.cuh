@@ -10,11 +10,13 @@
 //   WINO_DT       float | double
 //   WINO_TM/TN    per-thread microtile (rows k / columns t), multiples of the
 //                 16-byte vector width
-//   WINO_THM/THN  thread grid of the CTA; BM = THM*TM, BN = THN*TN
+//   WINO_THM/THN  consumer thread grid of the CTA; BM = THM*TM, BN = THN*TN
 //   WINO_BK       channels per pipeline stage (multiple of 8)
+//   WINO_KU       channels per unrolled inner loop (divides BK; multiple of 8 for pairwise)
 //   WINO_STAGES   smem ring depth
 //   WINO_SUM      0 exact-linear, 1 exact-pairwise, 2 ffma-linear, 3 ffma-pairwise
 //   WINO_LEVELS   pairwise: slots of the chunk-level binary counter
+//   WINO_MAXREG   register cap (0 = __launch_bounds__ only)
 //
 // Summation order (exact modes, bitwise equal to the reference):
 //   linear   : acc = -0; acc = acc + fl(u*v) for c = 0, 1, ...  (-0 + z = z exactly)
@@ -25,16 +27,24 @@
 //              occupied slots from the smallest block upwards.
 // Padded channels (c >= C) carry -0 products and leave every sum unchanged.
 //
-// Data movement: a producer warp issues cp.async.bulk (TMA bulk copies, SASS
-// UBLKCP) of the stage's contiguous U and V blocks into shared memory,
-// tracked by a "full" mbarrier per stage (complete_tx); consumer warps release
-// a stage through its "empty" mbarrier, so up to WINO_STAGES stages are in
-// flight and the main loop has no CTA-wide barrier.
+// Structure: persistent, warp-specialised CTAs.  Each CTA walks tiles
+// blockIdx.x, blockIdx.x + gridDim.x, ...; its producer warp streams the
+// stages of consecutive tiles through a WINO_STAGES-deep smem ring with
+// cp.async.bulk (TMA bulk copies, SASS UBLKCP) -- U and V are stored blocked
+// (U[p][k/BM][c][k%BM], V[p][t/BN][c][t%BN]) so a stage is one contiguous
+// block per operand -- signalled by "full" mbarriers (complete_tx); the
+// consumer warps release stages through "empty" mbarriers and write their
+// register tiles of M while the producer already prefetches the next tile.
+// No CTA-wide barrier after setup.
 
+#ifndef WINO_KU
+#define WINO_KU WINO_BK
+#endif
 #define DT WINO_DT
 #define BM (WINO_THM * WINO_TM)
 #define BN (WINO_THN * WINO_TN)
 #define NTHR (WINO_THM * WINO_THN)
+#define NCW (NTHR / 32)
 #define VW (16 / (int)sizeof(DT))
 #define GM (WINO_TM / VW)
 #define GN (WINO_TN / VW)
@@ -63,6 +73,9 @@ static __device__ __forceinline__ void mbar_expect_tx(u64* bar, unsigned bytes) 
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+static __device__ __forceinline__ void mbar_arrive(u64* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 static __device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
@@ -80,24 +93,15 @@ static __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsi
         : "memory");
 }
 
-static __device__ __forceinline__ void mbar_arrive(u64* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// Warp-specialised: warps 0 .. NCW-1 consume (register-blocked FP32/FP64
-// math), the last warp produces (bulk copies).  full[s] completes when the
-// stage's bytes have landed; empty[s] when every consumer warp has finished
-// reading it.  No CTA-wide barrier in the main loop.
-#define NCW (NTHR / 32)
 #if WINO_MAXREG > 0
 #define WINO_REGS __maxnreg__(WINO_MAXREG)
 #else
 #define WINO_REGS __launch_bounds__(NTHR + 32)
 #endif
-extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U,
-                                                                    const DT* __restrict__ V,
-                                                                    DT* __restrict__ M, long long Kp,
-                                                                    long long Tp, long long Cp) {
+
+extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, const DT* __restrict__ V,
+                                                  DT* __restrict__ M, long long Kp, long long Tp, long long Cp,
+                                                  int n_tiles) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     DT* sU = reinterpret_cast<DT*>(smem_raw);      // [STAGES][BK][BM]
     DT* sV = sU + WINO_STAGES * WINO_BK * BM;      // [STAGES][BK][BN]
@@ -106,10 +110,8 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U,
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const long long p = blockIdx.z;
-    const long long k0 = (long long)blockIdx.y * BM;
-    const long long t0 = (long long)blockIdx.x * BN;
     const int nk = (int)(Cp / WINO_BK);
+    const int n_tb = (int)(Tp / BN), n_kb = (int)(Kp / BM);
 
     if (tid == 0) {
 #pragma unroll
@@ -122,160 +124,182 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U,
     __syncthreads();
 
     if (warp == NCW) {
-        // ---------------- producer warp.  U and V are stored blocked
-        // (U[p][k/BM][c][k%BM], V[p][t/BN][c][t%BN]) so a stage of this tile is
-        // one contiguous block per operand: two bulk copies per stage.
+        // ------------------------------------------------ producer warp
         if (lane == 0) {
-            const DT* gU = U + p * Cp * Kp + (long long)blockIdx.y * Cp * BM;
-            const DT* gV = V + p * Cp * Tp + (long long)blockIdx.x * Cp * BN;
+            int g = 0;  // global stage counter across this CTA's tiles
 #pragma unroll 1
-            for (int kt = 0; kt < nk; ++kt) {
-                const int s = kt % WINO_STAGES;
-                if (kt >= WINO_STAGES) mbar_wait(&empty[s], (unsigned)(((kt / WINO_STAGES) - 1) & 1));
-                mbar_expect_tx(&full[s], (unsigned)(WINO_BK * (BM + BN) * sizeof(DT)));
-                bulk_g2s(sU + s * WINO_BK * BM, gU + (long long)kt * WINO_BK * BM, WINO_BK * BM * sizeof(DT), &full[s]);
-                bulk_g2s(sV + s * WINO_BK * BN, gV + (long long)kt * WINO_BK * BN, WINO_BK * BN * sizeof(DT), &full[s]);
+            for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+                const int tb = tile % n_tb;
+                const int rest = tile / n_tb;
+                const int kb = rest % n_kb;
+                const long long p = rest / n_kb;
+                const DT* gU = U + (p * Kp + (long long)kb * BM) * Cp;
+                const DT* gV = V + (p * Tp + (long long)tb * BN) * Cp;
+#pragma unroll 1
+                for (int kt = 0; kt < nk; ++kt, ++g) {
+                    const int s = g % WINO_STAGES;
+                    if (g >= WINO_STAGES) mbar_wait(&empty[s], (unsigned)(((g / WINO_STAGES) - 1) & 1));
+                    mbar_expect_tx(&full[s], (unsigned)(WINO_BK * (BM + BN) * sizeof(DT)));
+                    bulk_g2s(sU + s * WINO_BK * BM, gU + (long long)kt * WINO_BK * BM, WINO_BK * BM * sizeof(DT),
+                             &full[s]);
+                    bulk_g2s(sV + s * WINO_BK * BN, gV + (long long)kt * WINO_BK * BN, WINO_BK * BN * sizeof(DT),
+                             &full[s]);
+                }
             }
         }
         return;
     }
 
+    // ---------------------------------------------------- consumer warps
     const int tn = tid % WINO_THN;
     const int tm = tid / WINO_THN;
+    int g = 0;
+
+#pragma unroll 1
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int tb = tile % n_tb;
+        const int rest = tile / n_tb;
+        const int kb = rest % n_kb;
+        const long long p = rest / n_kb;
 
 #if WINO_SUM == 0
-    DT acc[WINO_TM][WINO_TN];
+        DT acc[WINO_TM][WINO_TN];
 #pragma unroll
-    for (int i = 0; i < WINO_TM; ++i)
+        for (int i = 0; i < WINO_TM; ++i)
 #pragma unroll
-        for (int j = 0; j < WINO_TN; ++j) acc[i][j] = (DT)(-0.0);
+            for (int j = 0; j < WINO_TN; ++j) acc[i][j] = (DT)(-0.0);
 #elif WINO_SUM == 2
-    DT acc[WINO_TM][WINO_TN];
+        DT acc[WINO_TM][WINO_TN];
 #pragma unroll
-    for (int i = 0; i < WINO_TM; ++i)
+        for (int i = 0; i < WINO_TM; ++i)
 #pragma unroll
-        for (int j = 0; j < WINO_TN; ++j) acc[i][j] = (DT)0;
+            for (int j = 0; j < WINO_TN; ++j) acc[i][j] = (DT)0;
 #else
-    DT pa[WINO_TM][WINO_TN];
+        DT pa[WINO_TM][WINO_TN];
 #if WINO_SUM == 1
-    DT pb[WINO_TM][WINO_TN], pd[WINO_TM][WINO_TN];
+        DT pb[WINO_TM][WINO_TN], pd[WINO_TM][WINO_TN];
 #endif
-    DT slot[WINO_LEVELS][WINO_TM][WINO_TN];
+        DT slot[WINO_LEVELS][WINO_TM][WINO_TN];
 #endif
 
 #pragma unroll 1
-    for (int kt = 0; kt < nk; ++kt) {
-        const int s = kt % WINO_STAGES;
-        mbar_wait(&full[s], (unsigned)((kt / WINO_STAGES) & 1));
-        const DT* cu = sU + s * WINO_BK * BM;
-        const DT* cv = sV + s * WINO_BK * BN;
+        for (int kt = 0; kt < nk; ++kt, ++g) {
+            const int s = g % WINO_STAGES;
+            mbar_wait(&full[s], (unsigned)((g / WINO_STAGES) & 1));
+            const DT* cu = sU + s * WINO_BK * BM;
+            const DT* cv = sV + s * WINO_BK * BN;
+#pragma unroll 1
+            for (int kk0 = 0; kk0 < WINO_BK; kk0 += WINO_KU) {
 #pragma unroll
-        for (int kk = 0; kk < WINO_BK; ++kk) {
-            DT a[WINO_TM], b[WINO_TN];
+                for (int kk1 = 0; kk1 < WINO_KU; ++kk1) {
+                    const int kk = kk0 + kk1;
+                    DT a[WINO_TM], b[WINO_TN];
 #pragma unroll
-            for (int g = 0; g < GM; ++g) {
-                vec_t q = *reinterpret_cast<const vec_t*>(cu + kk * BM + g * (WINO_THM * VW) + tm * VW);
-                const DT* qq = reinterpret_cast<const DT*>(&q);
+                    for (int q = 0; q < GM; ++q) {
+                        vec_t w4 = *reinterpret_cast<const vec_t*>(cu + kk * BM + q * (WINO_THM * VW) + tm * VW);
+                        const DT* ww = reinterpret_cast<const DT*>(&w4);
 #pragma unroll
-                for (int v = 0; v < VW; ++v) a[g * VW + v] = qq[v];
-            }
+                        for (int v = 0; v < VW; ++v) a[q * VW + v] = ww[v];
+                    }
 #pragma unroll
-            for (int g = 0; g < GN; ++g) {
-                vec_t q = *reinterpret_cast<const vec_t*>(cv + kk * BN + g * (WINO_THN * VW) + tn * VW);
-                const DT* qq = reinterpret_cast<const DT*>(&q);
+                    for (int q = 0; q < GN; ++q) {
+                        vec_t w4 = *reinterpret_cast<const vec_t*>(cv + kk * BN + q * (WINO_THN * VW) + tn * VW);
+                        const DT* ww = reinterpret_cast<const DT*>(&w4);
 #pragma unroll
-                for (int v = 0; v < VW; ++v) b[g * VW + v] = qq[v];
-            }
+                        for (int v = 0; v < VW; ++v) b[q * VW + v] = ww[v];
+                    }
 #if WINO_SUM == 0
 #pragma unroll
-            for (int i = 0; i < WINO_TM; ++i)
+                    for (int i = 0; i < WINO_TM; ++i)
 #pragma unroll
-                for (int j = 0; j < WINO_TN; ++j) acc[i][j] = XADD(acc[i][j], XMUL(a[i], b[j]));
+                        for (int j = 0; j < WINO_TN; ++j) acc[i][j] = XADD(acc[i][j], XMUL(a[i], b[j]));
 #elif WINO_SUM == 2
 #pragma unroll
-            for (int i = 0; i < WINO_TM; ++i)
+                    for (int i = 0; i < WINO_TM; ++i)
 #pragma unroll
-                for (int j = 0; j < WINO_TN; ++j) acc[i][j] = XFMA(a[i], b[j], acc[i][j]);
+                        for (int j = 0; j < WINO_TN; ++j) acc[i][j] = XFMA(a[i], b[j], acc[i][j]);
 #else
-            const int pos = kk & 7;  // compile-time after unrolling
+                    const int pos = kk1 & 7;  // compile-time after unrolling (WINO_KU % 8 == 0)
 #pragma unroll
-            for (int i = 0; i < WINO_TM; ++i)
+                    for (int i = 0; i < WINO_TM; ++i)
 #pragma unroll
-                for (int j = 0; j < WINO_TN; ++j) {
+                        for (int j = 0; j < WINO_TN; ++j) {
 #if WINO_SUM == 1
-                    const DT z = XMUL(a[i], b[j]);
-                    if (pos == 0) pa[i][j] = z;
-                    else if (pos == 1) pa[i][j] = XADD(pa[i][j], z);
-                    else if (pos == 2) pb[i][j] = z;
-                    else if (pos == 3) { pb[i][j] = XADD(pb[i][j], z); pa[i][j] = XADD(pa[i][j], pb[i][j]); }
-                    else if (pos == 4) pb[i][j] = z;
-                    else if (pos == 5) pb[i][j] = XADD(pb[i][j], z);
-                    else if (pos == 6) pd[i][j] = z;
-                    else { pd[i][j] = XADD(pd[i][j], z); pb[i][j] = XADD(pb[i][j], pd[i][j]); pa[i][j] = XADD(pa[i][j], pb[i][j]); }
+                            const DT z = XMUL(a[i], b[j]);
+                            if (pos == 0) pa[i][j] = z;
+                            else if (pos == 1) pa[i][j] = XADD(pa[i][j], z);
+                            else if (pos == 2) pb[i][j] = z;
+                            else if (pos == 3) { pb[i][j] = XADD(pb[i][j], z); pa[i][j] = XADD(pa[i][j], pb[i][j]); }
+                            else if (pos == 4) pb[i][j] = z;
+                            else if (pos == 5) pb[i][j] = XADD(pb[i][j], z);
+                            else if (pos == 6) pd[i][j] = z;
+                            else { pd[i][j] = XADD(pd[i][j], z); pb[i][j] = XADD(pb[i][j], pd[i][j]); pa[i][j] = XADD(pa[i][j], pb[i][j]); }
 #else
-                    if (pos == 0) pa[i][j] = XMUL(a[i], b[j]);
-                    else pa[i][j] = XFMA(a[i], b[j], pa[i][j]);
+                            if (pos == 0) pa[i][j] = XMUL(a[i], b[j]);
+                            else pa[i][j] = XFMA(a[i], b[j], pa[i][j]);
 #endif
-                }
-            if (pos == 7) {
-                // push the 8-channel block sum into the chunk-level counter
-                const int q = kt * (WINO_BK / 8) + (kk >> 3);
-                const int d = __ffs(~q) - 1;  // trailing ones of q = merges
+                        }
+                    if (pos == 7) {
+                        // push the 8-channel block sum into the chunk-level counter
+                        const int q8 = kt * (WINO_BK / 8) + (kk >> 3);
+                        const int d = __ffs(~q8) - 1;  // trailing ones of q8 = merges
 #pragma unroll
-                for (int L = 0; L < WINO_LEVELS; ++L) {
-                    if (d == L) {
+                        for (int L = 0; L < WINO_LEVELS; ++L) {
+                            if (d == L) {
 #pragma unroll
-                        for (int i = 0; i < WINO_TM; ++i)
+                                for (int i = 0; i < WINO_TM; ++i)
 #pragma unroll
-                            for (int j = 0; j < WINO_TN; ++j) {
-                                DT cy = pa[i][j];
+                                    for (int j = 0; j < WINO_TN; ++j) {
+                                        DT cy = pa[i][j];
 #pragma unroll
-                                for (int e = 0; e < L; ++e) cy = XADD(slot[e][i][j], cy);
-                                slot[L][i][j] = cy;
+                                        for (int e = 0; e < L; ++e) cy = XADD(slot[e][i][j], cy);
+                                        slot[L][i][j] = cy;
+                                    }
                             }
+                        }
                     }
+#endif
                 }
             }
-#endif
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-    }
 
 #if WINO_SUM == 1 || WINO_SUM == 3
-    // fold the occupied slots (set bits of the chunk count), smallest block first
-    DT acc[WINO_TM][WINO_TN];
-    {
-        const long long Q = Cp / 8;
-        bool have = false;
+        // fold the occupied slots (set bits of the chunk count), smallest block first
+        DT acc[WINO_TM][WINO_TN];
+        {
+            const long long Q = Cp / 8;
+            bool have = false;
 #pragma unroll
-        for (int L = 0; L < WINO_LEVELS; ++L) {
-            if ((Q >> L) & 1) {
+            for (int L = 0; L < WINO_LEVELS; ++L) {
+                if ((Q >> L) & 1) {
 #pragma unroll
-                for (int i = 0; i < WINO_TM; ++i)
+                    for (int i = 0; i < WINO_TM; ++i)
 #pragma unroll
-                    for (int j = 0; j < WINO_TN; ++j)
-                        acc[i][j] = have ? XADD(slot[L][i][j], acc[i][j]) : slot[L][i][j];
-                have = true;
+                        for (int j = 0; j < WINO_TN; ++j)
+                            acc[i][j] = have ? XADD(slot[L][i][j], acc[i][j]) : slot[L][i][j];
+                    have = true;
+                }
             }
         }
-    }
 #endif
 
-    DT* gM = M + p * Kp * Tp + k0 * Tp + t0;
+        DT* gM = M + (p * Kp + (long long)kb * BM) * Tp + (long long)tb * BN;
 #pragma unroll
-    for (int g = 0; g < GM; ++g)
+        for (int q = 0; q < GM; ++q)
 #pragma unroll
-        for (int v = 0; v < VW; ++v) {
-            const int i = g * VW + v;
-            const long long row = g * (WINO_THM * VW) + tm * VW + v;
+            for (int v = 0; v < VW; ++v) {
+                const int i = q * VW + v;
+                const long long row = q * (WINO_THM * VW) + tm * VW + v;
 #pragma unroll
-            for (int h = 0; h < GN; ++h) {
-                vec_t q;
-                DT* qq = reinterpret_cast<DT*>(&q);
+                for (int h = 0; h < GN; ++h) {
+                    vec_t w4;
+                    DT* ww = reinterpret_cast<DT*>(&w4);
 #pragma unroll
-                for (int u = 0; u < VW; ++u) qq[u] = acc[i][h * VW + u];
-                *reinterpret_cast<vec_t*>(gM + row * Tp + h * (WINO_THN * VW) + tn * VW) = q;
+                    for (int u = 0; u < VW; ++u) ww[u] = acc[i][h * VW + u];
+                    *reinterpret_cast<vec_t*>(gM + row * Tp + h * (WINO_THN * VW) + tn * VW) = w4;
+                }
             }
-        }
+    }
 }

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -51,6 +52,7 @@ struct Driver {
                              CUstream, void**, void**) = nullptr;
     CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
     CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
+    CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunction, int, size_t) = nullptr;
     bool ok = false;
     std::string err;
 };
@@ -68,7 +70,9 @@ static Driver& driver() {
                   get("cuModuleGetFunction", (void**)&d.ModuleGetFunction) &&
                   get("cuLaunchKernel", (void**)&d.LaunchKernel) &&
                   get("cuFuncSetAttribute", (void**)&d.FuncSetAttribute) &&
-                  get("cuGetErrorString", (void**)&d.GetErrorString);
+                  get("cuGetErrorString", (void**)&d.GetErrorString) &&
+                  get("cuOccupancyMaxActiveBlocksPerMultiprocessor",
+                      (void**)&d.OccupancyMaxActiveBlocksPerMultiprocessor);
         d.ok = ok;
         if (!ok) d.err = "CUDA driver entry points unavailable (no GPU driver?)";
     });
@@ -180,7 +184,7 @@ static const char* kContractTemplate =
     ;
 
 struct GemmCfg {
-    int tm, tn, thm, thn, bk, stages, maxreg;
+    int tm, tn, thm, thn, bk, stages, maxreg, ku = 0;  // ku: k-steps unrolled per inner loop (0 = bk)
     int bm() const { return thm * tm; }
     int bn() const { return thn * tn; }
     int threads() const { return thm * thn; }
@@ -215,7 +219,7 @@ struct wino_plan {
            << "\n#define WINO_TM " << gemm.tm << "\n#define WINO_TN " << gemm.tn << "\n#define WINO_THM " << gemm.thm
            << "\n#define WINO_THN " << gemm.thn << "\n#define WINO_BK " << gemm.bk << "\n#define WINO_STAGES "
            << gemm.stages << "\n#define WINO_SUM " << sum_mode() << "\n#define WINO_LEVELS "
-           << (levels > 0 ? levels : 1) << "\n#define WINO_MAXREG " << gemm.maxreg << "\n"
+           << (levels > 0 ? levels : 1) << "\n#define WINO_MAXREG " << gemm.maxreg << "\n#define WINO_KU " << (gemm.ku > 0 ? gemm.ku : gemm.bk) << "\n"
            << wino::kContractTemplate;
         mod->source = os.str();
         mod->name = "wino_contract_s" + std::to_string(sum_mode()) + "_L" + std::to_string(levels) + ".cu";
@@ -257,6 +261,8 @@ int layout_of(const wino_plan* p, const wino_layer_shape* s, wino_layer_layout* 
     L->th = (Ho + p->m - 1) / p->m;
     L->tw = (Wo + p->m - 1) / p->m;
     L->T = (long long)s->N * L->th * L->tw;
+    if (L->T > (1LL << 30) || (long long)s->H * s->W > (1LL << 30) || s->K > (1 << 30))
+        return wino::fail(WINO_EUNSUPPORTED, "layer too large for 32-bit tile indexing; split the batch");
     L->Tp = round_up(L->T > 0 ? L->T : 1, p->gemm.bn());
     L->Cp = round_up(s->C, p->gemm.bk);
     L->Kp = round_up(s->K, p->gemm.bm());
@@ -317,11 +323,12 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
     else if (channel_sum == WINO_SUM_PAIRWISE)
         p->gemm = {4, 4, 8, 16, 32, 4, 168};
     else
-        p->gemm = {8, 8, 16, 8, 16, 4, 0};
+        p->gemm = {8, 8, 16, 8, 16, 4, 0, 8};
     if (const char* env = getenv("WINO_GEMM")) {  // tuning override: tm,tn,thm,thn,bk,stages,maxreg
         wino::GemmCfg g{};
-        if (sscanf(env, "%d,%d,%d,%d,%d,%d,%d", &g.tm, &g.tn, &g.thm, &g.thn, &g.bk, &g.stages, &g.maxreg) == 7 &&
-            g.bk % 8 == 0 && g.tm % 4 == 0 && g.tn % 4 == 0)
+        const int got = sscanf(env, "%d,%d,%d,%d,%d,%d,%d,%d", &g.tm, &g.tn, &g.thm, &g.thn, &g.bk, &g.stages,
+                               &g.maxreg, &g.ku);
+        if (got >= 7 && g.bk % 8 == 0 && g.tm % 4 == 0 && g.tn % 4 == 0 && (g.ku == 0 || g.bk % g.ku == 0))
             p->gemm = g;
     }
     const std::string tag = "r" + std::to_string(r) + "m" + std::to_string(m) + "p" + std::to_string(precision);
@@ -400,10 +407,25 @@ int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, con
     if ((rc = mod->function("wino_contract", &f))) return rc;
     const wino::GemmCfg& g = plan->gemm;
     long long Kp = L.Kp, Tp = L.Tp, Cp = L.Cp;
-    void* args[] = {(void*)&U, (void*)&V, &M, &Kp, &Tp, &Cp};
+    const long long tiles = (long long)L.P * (Kp / g.bm()) * (Tp / g.bn());
+    if (tiles > (1LL << 30)) return wino::fail(WINO_EUNSUPPORTED, "contract: too many tiles");
+    int n_tiles = (int)tiles;
     const unsigned smem = (unsigned)(g.stages * g.bk * (g.bm() + g.bn()) * L.elem_bytes_uv + 2 * g.stages * 8);
-    return wino::launch(f, dim3((unsigned)(Tp / g.bn()), (unsigned)(Kp / g.bm()), (unsigned)L.P),
-                        dim3(g.threads() + 32), smem, stream, args, "contract");
+    const int threads = g.threads() + 32;
+    // persistent grid: as many CTAs as can be co-resident (one wave), each walks tiles
+    int per_sm = 0, sms = 0, dev = 0;
+    if (smem > 48 * 1024) {
+        CUresult cr = wino::driver().FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
+        if (cr != CUDA_SUCCESS) return wino::fail(WINO_ECUDA, "contract: set smem: " + wino::cu_err(cr));
+    }
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (wino::driver().OccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, threads, smem) != CUDA_SUCCESS ||
+        per_sm < 1)
+        per_sm = 1;
+    const long long grid = std::min<long long>(tiles, (long long)per_sm * (sms > 0 ? sms : 148));
+    void* args[] = {(void*)&U, (void*)&V, &M, &Kp, &Tp, &Cp, &n_tiles};
+    return wino::launch(f, dim3((unsigned)grid, 1, 1), dim3(threads), smem, stream, args, "contract");
 }
 
 int wino_output_transform(wino_plan* plan, const wino_layer_shape* s, const void* M, void* y, void* stream) {

@@ -118,6 +118,64 @@ class LayerOp:
         return out
 
 
+class HostPipeline:
+    """Host-buffer convolution with the copies overlapped: the batch is split
+    into image chunks; chunk i's H2D copy, chunk i-1's K1-K3-K4 and chunk i-2's
+    D2H run concurrently on three streams (PCIe is full duplex).  The filter
+    transform K2 runs once per call (U does not depend on the images).
+
+    x_host / y_host must be pinned CPU tensors (N, C, H, W) / (N, K, Ho, Wo)."""
+
+    def __init__(self, ts: TransformSet, cfg: ConvConfig, N, C, H, W, K, pad, chunks=4, contraction="exact"):
+        self.full = layer_op(ts, cfg, N, C, H, W, K, pad, contraction)
+        chunks = max(1, min(chunks, N))
+        self.bounds = [(i * N // chunks, (i + 1) * N // chunks) for i in range(chunks)]
+        self.ops = [layer_op(ts, cfg, b - a, C, H, W, K, pad, contraction) for a, b in self.bounds]
+        L = self.full.layout
+        self.U = D.torch.empty((L.P, L.Cp, L.Kp), dtype=self.full._uv_dtype(), device="cuda")
+        self.ws = [D.torch.empty((op.layout.v_bytes + op.layout.m_bytes + 512) // 4, dtype=D.torch.float32,
+                                 device="cuda") for op in self.ops]
+        self.x_dev = D.torch.empty((N, C, H, W), dtype=D._DT[self.full.in_dtype], device="cuda")
+        self.w_dev = D.torch.empty((K, C, ts.n_h, ts.n_h), dtype=D._DT[self.full.in_dtype], device="cuda")
+        self.y_dev = D.empty(self.full.out_shape, self.full.out_dtype)
+        self.s_h2d, self.s_cmp, self.s_d2h = D.torch.cuda.Stream(), D.torch.cuda.Stream(), D.torch.cuda.Stream()
+        self.ev = [(D.torch.cuda.Event(), D.torch.cuda.Event()) for _ in self.bounds]
+
+    def __call__(self, x_host, w_host, y_host):
+        torch = D.torch
+        lib = _native.lib()
+        cur = torch.cuda.current_stream()
+        for s in (self.s_h2d, self.s_cmp, self.s_d2h):
+            s.wait_stream(cur)
+        with torch.cuda.stream(self.s_h2d):
+            self.w_dev.copy_(w_host, non_blocking=True)
+            for (a, b), (e_in, _) in zip(self.bounds, self.ev):
+                self.x_dev[a:b].copy_(x_host[a:b], non_blocking=True)
+                e_in.record(self.s_h2d)
+        with torch.cuda.stream(self.s_cmp):
+            sc = self.s_cmp.cuda_stream
+            self.s_cmp.wait_event(self.ev[0][0])
+            _native.check(lib.wino_filter_transform(self.full.plan.handle, ctypes.byref(self.full.shape),
+                                                    D.ptr(self.w_dev), D.ptr(self.U), sc), "filter_transform")
+            for op, ws, (a, b), (e_in, e_out) in zip(self.ops, self.ws, self.bounds, self.ev):
+                self.s_cmp.wait_event(e_in)
+                V = ws
+                M = ws[(op.layout.v_bytes + 255) // 256 * 64:]
+                xs, ys = self.x_dev[a:b], self.y_dev[a:b]
+                sh = ctypes.byref(op.shape)
+                _native.check(lib.wino_input_transform(op.plan.handle, sh, D.ptr(xs), D.ptr(V), sc), "input")
+                _native.check(lib.wino_contract(op.plan.handle, sh, D.ptr(self.U), D.ptr(V), D.ptr(M), sc),
+                              "contract")
+                _native.check(lib.wino_output_transform(op.plan.handle, sh, D.ptr(M), D.ptr(ys), sc), "output")
+                e_out.record(self.s_cmp)
+        with torch.cuda.stream(self.s_d2h):
+            for (a, b), (_, e_out) in zip(self.bounds, self.ev):
+                self.s_d2h.wait_event(e_out)
+                y_host[a:b].copy_(self.y_dev[a:b], non_blocking=True)
+        cur.wait_stream(self.s_d2h)
+        return y_host
+
+
 _ops_lock = threading.Lock()
 
 

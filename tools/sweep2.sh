@@ -1,0 +1,5 @@
+timeout 600 python -m pytest tests/test_gpu_layer.py -x -q > gpurun_out/pt.log 2>&1; tail -2 gpurun_out/pt.log
+python tools/contract_bench.py --shape 32,128,28,128 --m 2 --cs linear --variants "8,8,16,8,16,4,0,8;8,8,8,16,16,4,0,8;8,8,16,16,16,4,96,8;8,8,16,8,16,6,0,8;8,8,8,8,16,4,0,8" > gpurun_out/sw_lin.jsonl 2>&1
+python tools/contract_bench.py --shape 32,128,28,128 --m 2 --cs linear --contraction ffma --variants "8,8,16,8,16,4,0,8;8,8,8,16,16,4,0,8" > gpurun_out/sw_ffma.jsonl 2>&1
+python tools/contract_bench.py --shape 64,256,28,256 --m 6 --cs linear --variants "8,8,16,8,16,4,0,8;8,8,8,16,16,4,0,8" > gpurun_out/sw_lin3.jsonl 2>&1
+python tools/contract_bench.py --shape 64,256,28,256 --m 6 --cs pairwise --prec mixed --variants "4,4,8,16,32,4,168,8;4,4,16,8,32,4,0,8" > gpurun_out/sw_pw.jsonl 2>&1
