@@ -386,6 +386,127 @@ def run_gpu(args, cfg):
         dist.destroy_process_group()
 
 
+def run_vgg(args):
+    """BASELINE config 5: VGG-16 conv stack, F(6x6,3x3) P8, pairwise, fp32, global batch
+    sharded across ranks (strong scaling); step = one 13-layer forward."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1803_10986_b200 as W
+    from paper_1803_10986_b200 import _native
+    from paper_1803_10986_b200.distributed import shard_range
+    from paper_1803_10986_b200.stack import VGG16, ConvStack, he_normal_weights
+
+    pts = "0,-1,1,1/2,-1/2,2,-2,inf"
+    ts = W.build_transforms(3, 6, W.parse_points(pts))
+    a, b = shard_range(args.vgg_batch, rank, world)
+    n = b - a
+    st = ConvStack(ts, W.ConvConfig("fp32", "huffman", "pairwise"), VGG16, n, 224,
+                   contraction=args.contraction)
+    st.set_weights(he_normal_weights(VGG16, 3))
+    x = torch.empty((n, 3, 224, 224), dtype=torch.float32, device="cuda")
+    for i in range(n):  # synthetic U[-1,1] images keyed by global image index
+        x[i].copy_(torch.from_numpy(synth((3, 224, 224), 2024, a + i, "uniform")))
+    for _ in range(max(3, args.warmup)):
+        st.forward(x)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        st.forward(x)
+    graph.replay()
+    torch.cuda.synchronize()
+    es = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for e0, e1 in es:  # inputs and activations >> L2: no flush needed
+            e0.record()
+            graph.replay()
+            e1.record()
+        torch.cuda.synchronize()
+    ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in es]))
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_flops = st.direct_flops * world if world == 1 else None
+    flops_all = 0
+    for op_ in st.ops:
+        flops_all += op_.direct_flops
+    # whole-job direct-eq flops: every rank's shard (equal or +-1 image)
+    gflops = torch.tensor([float(flops_all)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(gflops)
+    value = float(gflops.item()) / (ms * 1e-3) / 1e12
+    # per-kernel shares from an instrumented forward (events around each contraction)
+    lib = _native.lib()
+    import ctypes
+    c_ms = 0.0
+    c_flops = 0
+    other_ms = 0.0
+    cur = x
+    s = torch.cuda.current_stream().cuda_stream
+    for i, op_ in enumerate(st.ops):
+        L = op_.layout
+        ws = st.workspace
+        al = lambda v: (v + 255) // 256 * 256
+        U = ws.data_ptr()
+        V = U + al(L.u_bytes)
+        M = V + al(L.v_bytes)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+        _native.check(lib.wino_filter_transform(op_.plan.handle, ctypes.byref(op_.shape),
+                                                _native.as_ptr(st.weights[i]), ctypes.c_void_p(U), s))
+        _native.check(lib.wino_input_transform(op_.plan.handle, ctypes.byref(op_.shape), _native.as_ptr(cur),
+                                               ctypes.c_void_p(V), s))
+        ev[1].record()
+        _native.check(lib.wino_contract(op_.plan.handle, ctypes.byref(op_.shape), ctypes.c_void_p(U),
+                                        ctypes.c_void_p(V), ctypes.c_void_p(M), s))
+        ev[2].record()
+        _native.check(lib.wino_output_transform(op_.plan.handle, ctypes.byref(op_.shape), ctypes.c_void_p(M),
+                                                _native.as_ptr(st.conv_out[i]), s))
+        C, K, h, w_, pool = st.shapes[i]
+        _native.check(lib.wino_relu_pool(0, op_.N * K, L.Ho, L.Wo, 1 if pool else 0,
+                                         _native.as_ptr(st.conv_out[i]), _native.as_ptr(st.act[i]), s))
+        ev[3].record()
+        torch.cuda.synchronize()
+        c_ms += ev[1].elapsed_time(ev[2])
+        other_ms += ev[0].elapsed_time(ev[1]) + ev[2].elapsed_time(ev[3])
+        c_flops += op_.contraction_flops
+        cur = st.act[i]
+    peak = measure_peaks(lib, _native, torch)
+    ach = c_flops / (c_ms * 1e-3) / 1e12
+    errs = st.layer_errors(x, images=args.err_images) if not args.no_err else None
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (seeded Philox U[-1,1] 224x224x3 images, He-normal filters)",
+                "config": {"workload": "vgg16", "winograd": "F(6x6,3x3)", "points": pts,
+                           "global_batch": args.vgg_batch, "batch_per_gpu": n, "precision": "fp32",
+                           "dot_order": "huffman", "channel_sum": "pairwise", "contraction": args.contraction,
+                           "layers": 13, "pools_after": [2, 4, 7, 10],
+                           "l2": "inputs/activations >> L2 (no flush)",
+                           "parallelism": f"dp{world} (batch sharded)"},
+                "roofline": {"kernel": "wino_contract (13 layers)", "bound": "fp32", "achieved": ach,
+                             "peak": peak["ffma_tflops"], "unit": "TFLOP/s", "frac": ach / peak["ffma_tflops"],
+                             "traffic": None, "exact_ceiling_tflops": peak["fmul_fadd_tflops"],
+                             "frac_of_exact_ceiling": ach / peak["fmul_fadd_tflops"],
+                             "share_of_step": c_ms / (c_ms + other_ms)},
+                "per_layer_error_vs_fp64": errs, "gpu_launches": 5 * 13 * args.steps,
+                "clocks": clk.summary(), "peaks": peak}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def measure_peaks(lib, _native, torch):
     import ctypes
     out = torch.zeros(4, dtype=torch.float32, device="cuda")
@@ -415,13 +536,22 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS) + ["vgg16"])
+    ap.add_argument("--vgg-batch", type=int, default=256)
+    ap.add_argument("--err-images", type=int, default=8)
+    ap.add_argument("--no-err", action="store_true")
     ap.add_argument("--contraction", default="exact", choices=["exact", "ffma"])
     ap.add_argument("--cpu-images", type=int, default=32)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--soak", type=float, default=1.5, help="seconds of untimed load before the timed region")
     ap.add_argument("--e2e-chunks", type=int, default=4)
     args = ap.parse_args()
+    if args.config == "vgg16":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "vgg16 CPU reference: use --config cfg2"}))
+            return
+        run_vgg(args)
+        return
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)

@@ -164,6 +164,12 @@ int wino_direct_products(int dims, int dtype, int in_dtype, int64_t B, int C, in
 int wino_program_eval(int dtype, const void* ops, int nops, int cols, int64_t count,
                       const void* in, void* out, void* stream);
 
+/* ReLU, optionally fused with a 2x2/stride-2 max-pool, over planes[H][W]
+ * (dtype 0 = f32, 1 = f64) -- the activation between layers of the VGG-16
+ * conv stack (BASELINE.json config 5; not part of the reference toolkit). */
+int wino_relu_pool(int dtype, int64_t planes, int H, int W, int pool, const void* in, void* out,
+                   void* stream);
+
 /* ---- fp64 oracle side and error statistics ------------------------------ */
 /* Layer fp64 direct correlation (taps row-major per channel, channels left to
  * right; zero padding), x/w f32 -> y64 f64. */

@@ -496,3 +496,24 @@ def synthetic(shape, seed, idx, dist="uniform"):
     if dist == "normal":
         return g.standard_normal(shape, dtype=np.float32)
     raise ValueError(dist)
+
+
+def relu_pool(y, pool):
+    """ReLU then optional 2x2/stride-2 max-pool (between VGG conv layers)."""
+    y = np.maximum(np.asarray(y), np.float32(0))
+    if not pool:
+        return y
+    N, K, H, W = y.shape
+    y = y[:, :, : H // 2 * 2, : W // 2 * 2].reshape(N, K, H // 2, 2, W // 2, 2)
+    return y.max(axis=(3, 5))
+
+
+def stack_forward(trip, x, weights, layers, pad=1, order="huffman", csum="pairwise"):
+    """Oracle of paper_1803_10986_b200.stack.ConvStack (fp32): conv outputs per layer."""
+    outs = []
+    cur = x
+    for w, (_, _, pool) in zip(weights, layers):
+        y = layer_conv2d(trip, cur, w, pad, "fp32", order, csum)
+        outs.append(y)
+        cur = relu_pool(y, pool)
+    return outs, cur

@@ -65,6 +65,7 @@ SIGNATURES = [
     ("wino_direct_products", c_int, [c_int, c_int, c_int, c_int64, c_int, c_int, c_int, c_void_p, c_void_p,
                                      c_void_p, c_void_p]),
     ("wino_program_eval", c_int, [c_int, c_void_p, c_int, c_int, c_int64, c_void_p, c_void_p, c_void_p]),
+    ("wino_relu_pool", c_int, [c_int, c_int64, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     ("wino_direct_layer_f64", c_int, [POINTER(LayerShape), c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("wino_layer_error_stats", c_int, [c_int64, c_int64, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("wino_trial_inputs", c_int, [c_uint64, c_int64, c_int64, c_int, c_int, c_int, c_int, c_void_p, c_void_p,

@@ -302,6 +302,30 @@ __global__ void peak_probe_kernel(int mode, int iters, float seedf, float* __res
     if (s == 12345.678f) out[0] = s;  // keep the chains alive
 }
 
+
+// ---------------------------------------------------------------- ReLU (+ 2x2 max-pool)
+// Between the convolution layers of the VGG-16 stack (BASELINE config 5):
+// out = max over the 2x2 window of max(y, 0) (pool = 1) or max(y, 0) (pool = 0).
+template <typename T>
+__global__ void relu_pool_kernel(long long planes, int H, int W, int pool, const T* __restrict__ in,
+                                 T* __restrict__ out) {
+    const int Ho = pool ? H / 2 : H, Wo = pool ? W / 2 : W;
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= planes * Ho * Wo) return;
+    const long long pl = idx / ((long long)Ho * Wo);
+    const int r = (int)(idx - pl * Ho * Wo);
+    const int i = r / Wo, j = r - i * Wo;
+    const T* src = in + pl * H * W;
+    T v;
+    if (pool) {
+        const T* q = src + (2 * i) * W + 2 * j;
+        v = max(max(q[0], q[1]), max(q[W], q[W + 1]));
+    } else {
+        v = src[i * W + j];
+    }
+    out[idx] = v > (T)0 ? v : (T)0;
+}
+
 inline unsigned blocks_for(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
@@ -368,6 +392,21 @@ int wino_peak_probe(int mode, int blocks, int iters, float* out, void* stream) {
     if (mode < 0 || mode > 3 || blocks < 1 || iters < 1) return wino::fail(WINO_EINVAL, "peak_probe: bad arguments");
     peak_probe_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(mode, iters, 1.0f, out);
     return wino::after_launch("peak_probe");
+}
+
+
+int wino_relu_pool(int dtype, int64_t planes, int H, int W, int pool, const void* in, void* out, void* stream) {
+    if ((dtype != 0 && dtype != 1) || planes < 0 || H < 1 || W < 1 || (pool && (H < 2 || W < 2)))
+        return wino::fail(WINO_EINVAL, "relu_pool: bad arguments");
+    const long long n = planes * (long long)(pool ? H / 2 : H) * (pool ? W / 2 : W);
+    if (n == 0) return WINO_OK;
+    if (dtype == 0)
+        relu_pool_kernel<float><<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(planes, H, W, pool,
+                                                                                   (const float*)in, (float*)out);
+    else
+        relu_pool_kernel<double><<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(planes, H, W, pool,
+                                                                                    (const double*)in, (double*)out);
+    return wino::after_launch("relu_pool");
 }
 
 int wino_direct_layer_f64(const wino_layer_shape* sh, int r, const float* x, const float* w, double* y64,

@@ -1,2 +1,2 @@
-python bench.py --steps 20 --warmup 5 --no-cpu --soak 0.5 > gpurun_out/bench.log 2>&1; tail -c 3000 gpurun_out/bench.log
-python tools/contract_bench.py --shape 32,128,28,128 --m 2 --cs linear --variants "8,16,16,8,16,4,0,8;16,8,8,16,16,4,0,8" > gpurun_out/sw_a.jsonl 2>&1
+timeout 600 python -m pytest tests/test_gpu_stack.py -x -q > gpurun_out/pt_stack.log 2>&1; tail -3 gpurun_out/pt_stack.log
+timeout 600 python bench.py --config vgg16 --steps 5 --warmup 2 > gpurun_out/bench_vgg.log 2>&1; tail -c 2500 gpurun_out/bench_vgg.log
