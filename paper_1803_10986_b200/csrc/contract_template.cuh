@@ -40,6 +40,9 @@
 #ifndef WINO_KU
 #define WINO_KU WINO_BK
 #endif
+#ifndef WINO_DBUF
+#define WINO_DBUF (WINO_SUM == 1 || WINO_SUM == 3)  // explicit fragment double buffer (pairwise)
+#endif
 #define DT WINO_DT
 #define BM (WINO_THM * WINO_TM)
 #define BN (WINO_THN * WINO_TN)
@@ -83,6 +86,19 @@ static __device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
         "@!P1 bra WINO_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
+        : "memory");
+}
+// Producer-side wait: the producer is normally STAGES-1 stages ahead and waits
+// most of the time; a polling loop there costs issue slots of the consumer
+// warp sharing its SMSP.  try_wait with a suspend-time hint parks the thread
+// in hardware until the phase completes (or the hint expires).
+static __device__ __forceinline__ void mbar_wait_sleep(u64* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WINO_SLEEP_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra WINO_SLEEP_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000u)
         : "memory");
 }
 static __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, u64* bar) {
@@ -138,7 +154,7 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
 #pragma unroll 1
                 for (int kt = 0; kt < nk; ++kt, ++g) {
                     const int s = g % WINO_STAGES;
-                    if (g >= WINO_STAGES) mbar_wait(&empty[s], (unsigned)(((g / WINO_STAGES) - 1) & 1));
+                    if (g >= WINO_STAGES) mbar_wait_sleep(&empty[s], (unsigned)(((g / WINO_STAGES) - 1) & 1));
                     mbar_expect_tx(&full[s], (unsigned)(WINO_BK * (BM + BN) * sizeof(DT)));
                     bulk_g2s(sU + s * WINO_BK * BM, gU + (long long)kt * WINO_BK * BM, WINO_BK * BM * sizeof(DT),
                              &full[s]);
@@ -179,6 +195,10 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
 #if WINO_SUM == 1
         DT pb[WINO_TM][WINO_TN], pd[WINO_TM][WINO_TN];
 #endif
+        // Z: static counter inside a stage (a stage = WINO_BK/8 chunks of 8 channels);
+        // slot: dynamic counter over stages (slot j holds 2^j stages)
+#define ZL (WINO_BK == 8 ? 1 : WINO_BK == 16 ? 1 : WINO_BK == 32 ? 2 : 3)
+        DT zs[ZL][WINO_TM][WINO_TN];
         DT slot[WINO_LEVELS][WINO_TM][WINO_TN];
 #endif
 
@@ -188,26 +208,46 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
             mbar_wait(&full[s], (unsigned)((g / WINO_STAGES) & 1));
             const DT* cu = sU + s * WINO_BK * BM;
             const DT* cv = sV + s * WINO_BK * BN;
-#pragma unroll 1
-            for (int kk0 = 0; kk0 < WINO_BK; kk0 += WINO_KU) {
+#if WINO_SUM == 1 || WINO_SUM == 3
 #pragma unroll
-                for (int kk1 = 0; kk1 < WINO_KU; ++kk1) {
-                    const int kk = kk0 + kk1;
-                    DT a[WINO_TM], b[WINO_TN];
+#else
+#pragma unroll 1
+#endif
+            for (int kk0 = 0; kk0 < WINO_BK; kk0 += WINO_KU) {
+                // register double buffer: fragments of k-step kk+1 are loaded
+                // while k-step kk is multiplied
+                DT fa[2][WINO_TM], fb[2][WINO_TN];
+                auto load_frag = [&](int buf, int kk) {
 #pragma unroll
                     for (int q = 0; q < GM; ++q) {
                         vec_t w4 = *reinterpret_cast<const vec_t*>(cu + kk * BM + q * (WINO_THM * VW) + tm * VW);
                         const DT* ww = reinterpret_cast<const DT*>(&w4);
 #pragma unroll
-                        for (int v = 0; v < VW; ++v) a[q * VW + v] = ww[v];
+                        for (int v = 0; v < VW; ++v) fa[buf][q * VW + v] = ww[v];
                     }
 #pragma unroll
                     for (int q = 0; q < GN; ++q) {
                         vec_t w4 = *reinterpret_cast<const vec_t*>(cv + kk * BN + q * (WINO_THN * VW) + tn * VW);
                         const DT* ww = reinterpret_cast<const DT*>(&w4);
 #pragma unroll
-                        for (int v = 0; v < VW; ++v) b[q * VW + v] = ww[v];
+                        for (int v = 0; v < VW; ++v) fb[buf][q * VW + v] = ww[v];
                     }
+                };
+#if WINO_DBUF
+                load_frag(0, kk0);
+#endif
+#pragma unroll
+                for (int kk1 = 0; kk1 < WINO_KU; ++kk1) {
+                    const int kk = kk0 + kk1;
+#if WINO_DBUF
+                    if (kk1 + 1 < WINO_KU) load_frag((kk1 + 1) & 1, kk + 1);
+                    const DT* a = fa[kk1 & 1];
+                    const DT* b = fb[kk1 & 1];
+#else
+                    load_frag(0, kk);
+                    const DT* a = fa[0];
+                    const DT* b = fb[0];
+#endif
 #if WINO_SUM == 0
 #pragma unroll
                     for (int i = 0; i < WINO_TM; ++i)
@@ -240,21 +280,42 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
 #endif
                         }
                     if (pos == 7) {
-                        // push the 8-channel block sum into the chunk-level counter
-                        const int q8 = kt * (WINO_BK / 8) + (kk >> 3);
-                        const int d = __ffs(~q8) - 1;  // trailing ones of q8 = merges
+                        // chunk c of this stage is complete (c compile-time): static
+                        // counter inside the stage, dynamic counter over stages
+                        const int c = kk >> 3;
+                        constexpr int NCH = WINO_BK / 8;
+                        const int dc = __ffs(~c) - 1;  // trailing ones of c (constant-folded)
 #pragma unroll
-                        for (int L = 0; L < WINO_LEVELS; ++L) {
-                            if (d == L) {
+                        for (int i = 0; i < WINO_TM; ++i)
 #pragma unroll
-                                for (int i = 0; i < WINO_TM; ++i)
+                            for (int j = 0; j < WINO_TN; ++j) {
+                                DT cy = pa[i][j];
 #pragma unroll
-                                    for (int j = 0; j < WINO_TN; ++j) {
-                                        DT cy = pa[i][j];
+                                for (int e = 0; e < ZL; ++e)
+                                    if (e < dc) cy = XADD(zs[e][i][j], cy);
+                                if (c != NCH - 1) {
 #pragma unroll
-                                        for (int e = 0; e < L; ++e) cy = XADD(slot[e][i][j], cy);
-                                        slot[L][i][j] = cy;
-                                    }
+                                    for (int e = 0; e < ZL; ++e)
+                                        if (e == dc) zs[e][i][j] = cy;
+                                } else {
+                                    pa[i][j] = cy;  // the whole stage's block sum
+                                }
+                            }
+                        if (c == NCH - 1) {
+                            const int d = __ffs(~kt) - 1;  // trailing ones of the stage index
+#pragma unroll
+                            for (int L = 0; L < WINO_LEVELS; ++L) {
+                                if (d == L) {
+#pragma unroll
+                                    for (int i = 0; i < WINO_TM; ++i)
+#pragma unroll
+                                        for (int j = 0; j < WINO_TN; ++j) {
+                                            DT cy = pa[i][j];
+#pragma unroll
+                                            for (int e = 0; e < L; ++e) cy = XADD(slot[e][i][j], cy);
+                                            slot[L][i][j] = cy;
+                                        }
+                                }
                             }
                         }
                     }
@@ -269,7 +330,7 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
         // fold the occupied slots (set bits of the chunk count), smallest block first
         DT acc[WINO_TM][WINO_TN];
         {
-            const long long Q = Cp / 8;
+            const long long Q = Cp / WINO_BK;  // number of stages = counter pushes
             bool have = false;
 #pragma unroll
             for (int L = 0; L < WINO_LEVELS; ++L) {

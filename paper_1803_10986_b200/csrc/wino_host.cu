@@ -206,7 +206,7 @@ struct wino_plan {
 
     wino::Module* contract_module(long long Cp) {
         int levels = 1;
-        const long long Q = Cp / 8;
+        const long long Q = Cp / gemm.bk;  // pairwise: the dynamic counter runs over stages
         while ((1LL << levels) <= Q) ++levels;  // bit_length(Q)
         if (chsum != WINO_SUM_PAIRWISE) levels = 0;
         std::lock_guard<std::mutex> g(mu);
@@ -321,7 +321,7 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
     if (dbl64)
         p->gemm = {4, 4, 8, 16, 16, 4, 0};
     else if (channel_sum == WINO_SUM_PAIRWISE)
-        p->gemm = {4, 4, 8, 16, 32, 4, 168};
+        p->gemm = {4, 4, 8, 16, 32, 4, 168, 8};
     else
         p->gemm = {8, 8, 16, 8, 16, 4, 0, 8};
     if (const char* env = getenv("WINO_GEMM")) {  // tuning override: tm,tn,thm,thn,bk,stages,maxreg
