@@ -278,6 +278,16 @@ int layout_of(const wino_plan* p, const wino_layer_shape* s, wino_layer_layout* 
 
 inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
+// K1 / K4 block size (must match codegen.cpp): 128 tiles, halved while the
+// P x TB smem staging buffer exceeds 64 KB.
+int xform_block(const wino_plan* p, int* smem) {
+    const int P = p->n * p->n, es = p->ty.uv_double ? 8 : 4;
+    int tb = 128;
+    while (tb > 32 && (long long)P * tb * es > 64 * 1024) tb /= 2;
+    *smem = P * tb * es;
+    return tb;
+}
+
 }  // namespace
 
 // ================================================================== C-ABI
@@ -388,12 +398,16 @@ int wino_input_transform(wino_plan* plan, const wino_layer_shape* s, const void*
     wino_layer_layout L;
     int rc = layout_of(plan, s, &L);
     if (rc) return rc;
+    if ((uintptr_t)V & 15) return wino::fail(WINO_EINVAL, "input_transform: V must be 16-byte aligned");
     CUfunction f;
     if ((rc = plan->layer.function("wino_input_xform", &f))) return rc;
     int C = s->C, H = s->H, W = s->W, pad = s->pad, th = L.th, tw = L.tw;
     long long T = L.T, Tp = L.Tp, Cp = L.Cp;
+    int smem = 0;
+    const int tb = xform_block(plan, &smem);
     void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp};
-    return wino::launch(f, dim3(cdiv(Tp, 128), (unsigned)Cp, 1), dim3(128), 0, stream, args, "input_transform");
+    return wino::launch(f, dim3(cdiv(Tp, tb), (unsigned)Cp, 1), dim3(tb), (unsigned)smem, stream, args,
+                        "input_transform");
 }
 
 int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, const void* V, void* M, void* stream) {
@@ -432,12 +446,16 @@ int wino_output_transform(wino_plan* plan, const wino_layer_shape* s, const void
     wino_layer_layout L;
     int rc = layout_of(plan, s, &L);
     if (rc) return rc;
+    if ((uintptr_t)M & 15) return wino::fail(WINO_EINVAL, "output_transform: M must be 16-byte aligned");
     CUfunction f;
     if ((rc = plan->layer.function("wino_output_xform", &f))) return rc;
     int K = s->K, Ho = L.Ho, Wo = L.Wo, th = L.th, tw = L.tw;
     long long T = L.T, Tp = L.Tp, Kp = L.Kp;
+    int smem = 0;
+    const int tb = xform_block(plan, &smem);
     void* args[] = {(void*)&M, &y, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp};
-    return wino::launch(f, dim3(cdiv(T, 128), (unsigned)K, 1), dim3(128), 0, stream, args, "output_transform");
+    return wino::launch(f, dim3(cdiv(T, tb), (unsigned)K, 1), dim3(tb), (unsigned)smem, stream, args,
+                        "output_transform");
 }
 
 int wino_conv2d(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w, void* y, void* workspace,
