@@ -540,7 +540,7 @@ def main():
     ap.add_argument("--vgg-batch", type=int, default=256)
     ap.add_argument("--err-images", type=int, default=8)
     ap.add_argument("--no-err", action="store_true")
-    ap.add_argument("--contraction", default="exact", choices=["exact", "ffma"])
+    ap.add_argument("--contraction", default="exact", choices=["exact", "ffma", "tc_bf16", "tc_fp16"])
     ap.add_argument("--cpu-images", type=int, default=32)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--soak", type=float, default=1.5, help="seconds of untimed load before the timed region")

@@ -48,6 +48,11 @@ extern "C" {
  * (faster, NOT bitwise, reported with its own error statistics). */
 #define WINO_CONTRACT_EXACT 0
 #define WINO_CONTRACT_FFMA 1
+/* tensor-core modes (tcgen05.mma kind::f16): U and V rounded to BF16 / FP16,
+ * FP32 accumulation in TMEM -- NOT bitwise, reported with their own error;
+ * precision must be fp32 or mixed. */
+#define WINO_CONTRACT_TC_BF16 2
+#define WINO_CONTRACT_TC_FP16 3
 
 /* One postfix op of a row program (reference engine.py:153-208 compiled
  * programs, flattened): LEAF pushes coeff * in[col] (one rounded product;

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwino.so"
 WINO_OK, WINO_EINVAL, WINO_EUNSUPPORTED, WINO_ECUDA, WINO_ECOMPILE = 0, -1, -2, -3, -4
 PRECISION_CODE = {"fp32": 0, "fp64": 1, "mixed": 2}
 SUM_CODE = {"linear": 0, "pairwise": 1}
-CONTRACT_CODE = {"exact": 0, "ffma": 1}
+CONTRACT_CODE = {"exact": 0, "ffma": 1, "tc_bf16": 2, "tc_fp16": 3}
 
 
 class WinoOp(ctypes.Structure):

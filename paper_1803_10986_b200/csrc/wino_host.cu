@@ -304,7 +304,10 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
     if (r < 1 || m < 1) return wino::fail(WINO_EINVAL, "kernel and output sizes must be >= 1");
     if (precision < 0 || precision > 2) return wino::fail(WINO_EINVAL, "precision must be fp32, fp64 or mixed");
     if (channel_sum < 0 || channel_sum > 1) return wino::fail(WINO_EINVAL, "channel_sum must be linear or pairwise");
-    if (contract_mode < 0 || contract_mode > 1) return wino::fail(WINO_EINVAL, "contract mode must be exact or ffma");
+    if (contract_mode < 0 || contract_mode > 3)
+        return wino::fail(WINO_EINVAL, "contract mode must be exact, ffma, tc_bf16 or tc_fp16");
+    if (contract_mode >= WINO_CONTRACT_TC_BF16 && precision == WINO_FP64)
+        return wino::fail(WINO_EINVAL, "tensor-core contraction needs fp32 or mixed precision");
     const int n = r + m - 1;
     if (n > 16) return wino::fail(WINO_EUNSUPPORTED, "alpha = r + m - 1 > 16 is not generated");
     auto p = std::make_unique<wino_plan>();
@@ -328,7 +331,9 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
     // Tile configs {tm, tn, thm, thn, bk, stages, maxreg} picked by tools/contract_bench.py
     // sweeps on B200 (profiles/): 4 consumer warps + 1 producer warp per CTA,
     // so three CTAs (15 warps) fit per SM within the per-SMSP register file.
-    if (dbl64)
+    if (contract_mode >= WINO_CONTRACT_TC_BF16)
+        p->gemm = {8, 8, 16, 16, 32, 3, 0};  // only the 128/128/32 blocking matters (tc_contract.cu)
+    else if (dbl64)
         p->gemm = {4, 4, 8, 16, 16, 4, 0};
     else if (channel_sum == WINO_SUM_PAIRWISE)
         p->gemm = {4, 4, 8, 16, 32, 4, 168, 8};
@@ -416,6 +421,9 @@ int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, con
     if (rc) return rc;
     if (((uintptr_t)U | (uintptr_t)V | (uintptr_t)M) & 15)
         return wino::fail(WINO_EINVAL, "contract: U, V, M must be 16-byte aligned");
+    if (plan->mode >= WINO_CONTRACT_TC_BF16)
+        return wino::tc_contract_launch(U, V, M, L.Kp, L.Tp, L.Cp, L.P, plan->mode == WINO_CONTRACT_TC_FP16,
+                                        stream);
     wino::Module* mod = plan->contract_module(L.Cp);
     CUfunction f;
     if ((rc = mod->function("wino_contract", &f))) return rc;

@@ -10,4 +10,7 @@ int fail(int code, const std::string& msg);
 // check the last CUDA launch, count it, translate errors
 int after_launch(const char* what);
 void count_launch();
+// K3t: tcgen05 tensor-core contraction (tc_contract.cu)
+int tc_contract_launch(const void* U, const void* V, void* M, long long Kp, long long Tp, long long Cp, int P,
+                       int fp16, void* stream);
 }  // namespace wino

@@ -1,0 +1,43 @@
+"""Tensor-core contraction mode (tcgen05, BF16/FP16 operands, FP32 accumulate):
+not bitwise by design -- checked against an fp64 GEMM of the 16-bit-rounded
+operands (layout correctness) and against the fp64 direct convolution (error)."""
+import numpy as np
+import pytest
+
+from oracle import wino_oracle as O
+
+pytestmark = pytest.mark.gpu
+W = pytest.importorskip("paper_1803_10986_b200")
+torch = pytest.importorskip("torch")
+
+
+@pytest.mark.parametrize("mode,dt", [("tc_bf16", torch.bfloat16), ("tc_fp16", torch.float16)])
+def test_tc_contraction_matches_rounded_gemm(mode, dt):
+    ts = W.build_transforms(3, 4, W.parse_points("0,1,-1,1/2,-1/2,inf"))
+    op = W.layer_op(ts, W.ConvConfig(), 3, 70, 20, 20, 150, 1, contraction=mode)
+    L = op.layout
+    U = torch.randn((L.P, L.Cp, L.Kp), device="cuda")
+    V = torch.randn((L.P, L.Cp, L.Tp), device="cuda")
+    M = op.contract(U, V)
+    Uu = op.unblock_u(U).to(dt).double()
+    Vu = op.unblock_v(V).to(dt).double()
+    ref = torch.einsum("pck,pct->pkt", Uu, Vu)
+    err = (M.double() - ref).abs().max().item()
+    scale = torch.einsum("pck,pct->pkt", Uu.abs(), Vu.abs()).max().item()
+    assert err <= 1e-5 * scale, (err, scale)
+
+
+@pytest.mark.parametrize("mode", ["tc_bf16", "tc_fp16"])
+def test_tc_layer_error_vs_fp64(mode):
+    pts = "0,-1,1,1/2,-1/2,2,-2,inf"
+    ts = W.build_transforms(3, 6, W.parse_points(pts))
+    x = O.synthetic((4, 64, 28, 28), 3, 0)
+    w = O.synthetic((96, 64, 3, 3), 3, 1) * np.float32(0.06)
+    y = W.conv2d_layer(ts, x, w, W.ConvConfig(), pad=1, contraction=mode)
+    y64 = O.layer_direct_fp64(x, w, 1)
+    rel = np.abs(y.astype(np.float64) - y64).sum() / np.abs(y64).sum()
+    # measured on B200: BF16 3.9e-2, FP16 ~3e-3 (F(6,3) transforms amplify the 16-bit operand rounding)
+    assert rel < (6e-2 if mode == "tc_bf16" else 6e-3), rel
+    yx = W.conv2d_layer(ts, x, w, W.ConvConfig(), pad=1)
+    rel_exact = np.abs(yx.astype(np.float64) - y64).sum() / np.abs(y64).sum()
+    assert rel_exact < rel
