@@ -222,11 +222,11 @@ def run_gpu(args, cfg):
         sh = torch.cuda.current_stream().cuda_stream  # the capture stream inside torch.cuda.graph
         if ev is not None:
             ev[0].record(stream)
-        _native.check(lib.wino_filter_transform(op.plan.handle, sref, _native.as_ptr(w), _native.as_ptr(U), sh))
+        # K1 + K2 in one launch (wino_transforms); the second event pair is empty
+        _native.check(lib.wino_transforms(op.plan.handle, sref, _native.as_ptr(x), _native.as_ptr(w),
+                                          _native.as_ptr(U), _native.as_ptr(V), sh))
         if ev is not None:
             ev[1].record(stream)
-        _native.check(lib.wino_input_transform(op.plan.handle, sref, _native.as_ptr(x), _native.as_ptr(V), sh))
-        if ev is not None:
             ev[2].record(stream)
         _native.check(lib.wino_contract(op.plan.handle, sref, _native.as_ptr(U), _native.as_ptr(V),
                                         _native.as_ptr(M), sh))
@@ -274,7 +274,7 @@ def run_gpu(args, cfg):
             flush.zero_()
             step(evs[i])
         torch.cuda.synchronize()
-        n_launch = 4 * args.steps + (_native.launch_count() - n0)
+        n_launch = 3 * args.steps + (_native.launch_count() - n0)
     if world > 1:
         dist.barrier()
     stage = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(4)] for i in range(args.steps)])
@@ -345,12 +345,15 @@ def run_gpu(args, cfg):
     except Exception:
         pass
     eb = L.elem_bytes_uv
-    stage_bytes = [4 * K * C * r * r + eb * L.P * C * K,
-                   4 * N * C * H * H + eb * L.P * L.T * C,
+    stage_bytes = [4 * K * C * r * r + eb * L.P * C * K + 4 * N * C * H * H + eb * L.P * L.T * C,
+                   None,
                    None,
                    eb * L.P * L.T * K + (4 if prec == "fp32" else 8) * N * K * L.Ho * L.Wo]
     stages = {}
-    for j, name in enumerate(["filter_transform", "input_transform", "contract", "output_transform"]):
+    for j, name in enumerate(["transforms (K1 input + K2 filter, one launch)", None, "contract",
+                              "output_transform"]):
+        if name is None:
+            continue
         d = {"ms": float(ms_stage[j])}
         if stage_bytes[j] is not None:
             d["gbs"] = stage_bytes[j] / (ms_stage[j] * 1e-3) / 1e9

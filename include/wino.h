@@ -129,6 +129,9 @@ int wino_filter_transform(wino_plan* plan, const wino_layer_shape* s, const void
 /* K1: V = (B^T d) B per (tile, c), tile gather + zero padding fused -- engine.py:410,412 */
 int wino_input_transform(wino_plan* plan, const wino_layer_shape* s, const void* x,
                          void* V, void* stream);
+/* K1 + K2 in one launch (the filter transform's blocks ride along) */
+int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w,
+                    void* U, void* V, void* stream);
 /* K3: M_p = sum_c U_p[c] * V_p[c] for the alpha^2 points, channel order
  * linear or pairwise (halving tree) -- engine.py:415, 252-278, 336-338 */
 int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, const void* V,

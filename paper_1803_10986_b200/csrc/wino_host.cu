@@ -395,8 +395,29 @@ int wino_filter_transform(wino_plan* plan, const wino_layer_shape* s, const void
     if ((rc = plan->layer.function("wino_filter_xform", &f))) return rc;
     int K = s->K, C = s->C;
     long long Kp = L.Kp, Cp = L.Cp;
+    int smem = 0;
+    const int tb = xform_block(plan, &smem);
     void* args[] = {(void*)&w, &U, &K, &C, &Kp, &Cp};
-    return wino::launch(f, dim3(cdiv(Kp, 128), (unsigned)Cp, 1), dim3(128), 0, stream, args, "filter_transform");
+    return wino::launch(f, dim3(cdiv(Kp, tb), (unsigned)Cp, 1), dim3(tb), 0, stream, args, "filter_transform");
+}
+
+int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w, void* U, void* V,
+                    void* stream) {
+    wino_layer_layout L;
+    int rc = layout_of(plan, s, &L);
+    if (rc) return rc;
+    if ((uintptr_t)V & 15) return wino::fail(WINO_EINVAL, "transforms: V must be 16-byte aligned");
+    CUfunction f;
+    if ((rc = plan->layer.function("wino_transforms", &f))) return rc;
+    int C = s->C, H = s->H, W = s->W, pad = s->pad, th = L.th, tw = L.tw, K = s->K;
+    long long T = L.T, Tp = L.Tp, Cp = L.Cp, Kp = L.Kp;
+    int smem = 0;
+    const int tb = xform_block(plan, &smem);
+    int n_tb = (int)cdiv(Tp, tb), n_kb = (int)cdiv(Kp, tb);
+    const long long blocks = (long long)n_tb * Cp + (long long)n_kb * Cp;
+    if (blocks >= (1LL << 31)) return wino::fail(WINO_EUNSUPPORTED, "transforms: grid too large");
+    void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &n_tb, (void*)&w, &U, &K, &Kp, &n_kb};
+    return wino::launch(f, dim3((unsigned)blocks, 1, 1), dim3(tb), (unsigned)smem, stream, args, "transforms");
 }
 
 int wino_input_transform(wino_plan* plan, const wino_layer_shape* s, const void* x, void* V, void* stream) {
@@ -478,8 +499,7 @@ int wino_conv2d(wino_plan* plan, const wino_layer_shape* s, const void* x, const
     char* U = (char*)workspace;
     char* V = U + al(L.u_bytes);
     char* M = V + al(L.v_bytes);
-    if ((rc = wino_filter_transform(plan, s, w, U, stream))) return rc;
-    if ((rc = wino_input_transform(plan, s, x, V, stream))) return rc;
+    if ((rc = wino_transforms(plan, s, x, w, U, V, stream))) return rc;
     if ((rc = wino_contract(plan, s, U, V, M, stream))) return rc;
     return wino_output_transform(plan, s, M, y, stream);
 }

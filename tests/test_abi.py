@@ -91,7 +91,7 @@ def test_generated_source_is_straight_line_and_deterministic(built):
     s1, s2 = p1.source(0), p2.source(0)
     assert s1 == s2
     assert "__fmul_rn" in s1 and "__fadd_rn" in s1
-    body = s1.split("wino_input_xform")[1].split("} else {", 1)[1].split("__syncthreads", 1)[0]
+    body = s1.split("void input_body")[1].split("} else {", 1)[1].split("__syncthreads", 1)[0]
     assert "__ldg" in body and "for (" not in body  # the transform is fully unrolled straight-line code
 
 
