@@ -239,6 +239,12 @@ def run_gpu(args, cfg):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
+    if args.ncu:
+        # profiling mode (ncu launch lists / captures): the K steps eagerly, nothing else
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize()
+        return
 
     # The step as a CUDA graph (4 libwino kernel nodes): no CPU launch gaps.
     graph = torch.cuda.CUDAGraph()
@@ -331,19 +337,22 @@ def run_gpu(args, cfg):
     flops_c = 2 * L.P * L.T * C * K
     ach = flops_c / (ms_stage[2] * 1e-3) / 1e12
     exact = args.contraction == "exact"
-    pk = peak["ffma_tflops"]
-    roof = {"kernel": "wino_contract", "bound": "fp32", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
-            "frac": ach / pk, "traffic": None,
-            "peak_source": "measured in this run: libwino wino_peak_probe FFMA (8 chains x 148*8 CTAs)",
-            "exact_ceiling_tflops": peak["fmul_fadd_tflops"] if exact else None,
-            "frac_of_exact_ceiling": ach / peak["fmul_fadd_tflops"] if exact else None,
-            "flops_per_launch": flops_c, "share_of_step": float(ms_stage[2] / ms_stage.sum())}
-    hbm = 6553.9
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            hbm = json.load(fh)["hbm_gbs"]
-    except Exception:
-        pass
+    mp = measured_peaks()
+    hbm = mp["hbm_gbs"]
+    if args.contraction.startswith("tc_"):
+        pk = mp["bf16_tflops"]
+        roof = {"kernel": "tc_contract_kernel (tcgen05.mma kind::f16)", "bound": "tensor", "achieved": ach,
+                "peak": pk, "unit": "TFLOP/s", "frac": ach / pk, "traffic": None,
+                "peak_source": mp["source"] + " bf16 dense (burst)"}
+    else:
+        pk = peak["ffma_tflops"]
+        roof = {"kernel": "wino_contract", "bound": "fp32", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+                "frac": ach / pk, "traffic": traffic_of("wino_contract", args.config, args.contraction),
+                "peak_source": "measured in this run: libwino wino_peak_probe FFMA (8 chains x 148*8 CTAs); "
+                               "MEASURED_PEAKS.json has no FP32 figure",
+                "exact_ceiling_tflops": peak["fmul_fadd_tflops"] if exact else None,
+                "frac_of_exact_ceiling": ach / peak["fmul_fadd_tflops"] if exact else None}
+    roof.update({"flops_per_launch": flops_c, "share_of_step": float(ms_stage[2] / ms_stage.sum())})
     eb = L.elem_bytes_uv
     stage_bytes = [4 * K * C * r * r + eb * L.P * C * K + 4 * N * C * H * H + eb * L.P * L.T * C,
                    None,
@@ -498,16 +507,46 @@ def run_vgg(args):
                            "layers": 13, "pools_after": [2, 4, 7, 10],
                            "l2": "inputs/activations >> L2 (no flush)",
                            "parallelism": f"dp{world} (batch sharded)"},
-                "roofline": {"kernel": "wino_contract (13 layers)", "bound": "fp32", "achieved": ach,
-                             "peak": peak["ffma_tflops"], "unit": "TFLOP/s", "frac": ach / peak["ffma_tflops"],
-                             "traffic": None, "exact_ceiling_tflops": peak["fmul_fadd_tflops"],
-                             "frac_of_exact_ceiling": ach / peak["fmul_fadd_tflops"],
-                             "share_of_step": c_ms / (c_ms + other_ms)},
+                "roofline": vgg_roof(args, ach, peak, c_ms / (c_ms + other_ms)),
                 "per_layer_error_vs_fp64": errs, "gpu_launches": 5 * 13 * args.steps,
                 "clocks": clk.summary(), "peaks": peak}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def measured_peaks():
+    """Roofline denominators from the driver-written MEASURED_PEAKS.json, else
+    the B200_PROFILING.md fallback (6.65 TB/s, 1.59 PFLOP/s bf16)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "source": "MEASURED_PEAKS.json (measured)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "B200_PROFILING.md fallback"}
+
+
+def traffic_of(kernel, config, contraction):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
+    --set full capture summary (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(f"{config}/{contraction}/{kernel}")
+    except Exception:
+        return None
+
+
+def vgg_roof(args, ach, peak, share):
+    if args.contraction.startswith("tc_"):
+        mp = measured_peaks()
+        return {"kernel": "tc_contract_kernel (13 layers)", "bound": "tensor", "achieved": ach,
+                "peak": mp["bf16_tflops"], "unit": "TFLOP/s", "frac": ach / mp["bf16_tflops"], "traffic": None,
+                "peak_source": mp["source"] + " bf16 dense (burst)", "share_of_step": share}
+    return {"kernel": "wino_contract (13 layers)", "bound": "fp32", "achieved": ach, "peak": peak["ffma_tflops"],
+            "unit": "TFLOP/s", "frac": ach / peak["ffma_tflops"], "traffic": None,
+            "exact_ceiling_tflops": peak["fmul_fadd_tflops"],
+            "frac_of_exact_ceiling": ach / peak["fmul_fadd_tflops"], "share_of_step": share}
 
 
 def measure_peaks(lib, _native, torch):
@@ -548,6 +587,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--soak", type=float, default=1.5, help="seconds of untimed load before the timed region")
     ap.add_argument("--e2e-chunks", type=int, default=4)
+    ap.add_argument("--ncu", action="store_true", help="profiling mode: warm-up + K eager steps only, no output")
     args = ap.parse_args()
     if args.config == "vgg16":
         if args.impl == "reference":
