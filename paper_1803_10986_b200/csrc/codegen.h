@@ -41,6 +41,9 @@ std::string validate(const MatProg& m, int expect_rows, int expect_cols, const c
 // so one pipeline stage of a contraction tile is a single contiguous block.
 std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
                              const GenTypes& ty, int bm, int bn);
+// tensor-core variant: 16-bit U/V in the UMMA K-major core-matrix layout (see codegen.cpp)
+std::string gen_layer_source_tc(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
+                                const GenTypes& ty, bool fp16);
 std::string gen_tile_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
                             const GenTypes& ty);
 

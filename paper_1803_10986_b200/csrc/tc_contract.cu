@@ -7,16 +7,17 @@
 //
 //   M_p[k][t] = sum_c U_p[c][k] * V_p[c][t]     (per Winograd point p)
 //
-// One persistent CTA per SM walks 128x128 output tiles (p, k-block, t-block):
-//   warp 4      producer: cp.async.bulk of the fp32 stage blocks of U and V
-//               (32 channels x 128) into a 3-deep smem ring (mbarrier complete_tx)
-//   warps 0-3   convert each fp32 stage to BF16/FP16 in the canonical UMMA
-//               K-major no-swizzle layout (8x8 core matrices, 128 B each),
-//               then fence.proxy.async so the tensor core sees them
-//   warp 5      one elected thread issues tcgen05.mma (M=128, N=128, K=16) into
-//               one of two 128-column TMEM accumulators and tcgen05.commit's
-//               the completion to mbarriers (operand buffer free / tile done)
-//   warps 6-9   epilogue: tcgen05.ld TMEM -> registers -> M (fp32) while the
+// U and V are produced by the generated transforms directly as 16-bit operands
+// in the canonical UMMA K-major no-swizzle layout (8x8 core matrices, 128 B
+// each), blocked so that one (tile, 32-channel stage) operand is one
+// contiguous 8 KB block.  One persistent CTA per SM walks 128x128 output
+// tiles (p, k-block, t-block):
+//   warp 0      producer: two cp.async.bulk (8 KB each) per stage into a
+//               6-deep smem ring (mbarrier complete_tx)
+//   warp 1      one elected thread issues tcgen05.mma (M=128, N=128, K=16) into
+//               one of two 128-column TMEM accumulators; tcgen05.commit frees
+//               the smem stage / publishes the finished accumulator
+//   warps 2-5   epilogue: tcgen05.ld TMEM -> registers -> M (fp32) while the
 //               next tile accumulates into the other TMEM buffer
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -101,40 +102,24 @@ __device__ __forceinline__ uint32_t pack2(float a, float b, int fp16) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// fp32 stage [TBK][W] (row c, W contiguous) -> 16-bit canonical K-major
-// no-swizzle core matrices (8 rows w x 8 channels c = 128 B): byte offset
-// (c/8)*LBO + (w/8)*128 + (w%8)*16 + (c%8)*2.  Thread u reads the 8 channels
-// of column w (consecutive threads -> consecutive w: conflict-free loads) and
-// writes one 16-byte row (consecutive threads -> consecutive rows).
-template <int W, int LBO>
-__device__ __forceinline__ void convert_stage(const float* __restrict__ src, unsigned char* dst, int tid, int fp16) {
-    constexpr int UNITS = W * (TBK / 8);
-#pragma unroll
-    for (int u = tid; u < UNITS; u += 128) {
-        const int w = u % W, kc = u / W;
-        const float* col = src + (kc * 8) * W + w;
-        uint4 o;
-        o.x = pack2(col[0 * W], col[1 * W], fp16);
-        o.y = pack2(col[2 * W], col[3 * W], fp16);
-        o.z = pack2(col[4 * W], col[5 * W], fp16);
-        o.w = pack2(col[6 * W], col[7 * W], fp16);
-        *reinterpret_cast<uint4*>(dst + kc * LBO + (w / 8) * 128 + (w % 8) * 16) = o;
-    }
-}
+// U and V arrive as 16-bit operands already in the canonical K-major
+// no-swizzle UMMA layout (written by the generated transforms, see
+// codegen.cpp gen_layer_source_tc): X16[p][rowblock][c/32][(c/8)%4][row/8][row%8][c%8],
+// so a (tile, 32-channel stage) operand is one contiguous 8 KB block.
+constexpr int kOpStage = TBK * TBM * 2;  // bytes of one operand stage (A or B)
+constexpr int OSTAGES = 6;
 
-__global__ void __launch_bounds__(320, 1) tc_contract_kernel(const float* __restrict__ U, const float* __restrict__ V,
+__global__ void __launch_bounds__(192, 1) tc_contract_kernel(const unsigned short* __restrict__ U,
+                                                             const unsigned short* __restrict__ V,
                                                              float* __restrict__ M, long long Kp, long long Tp,
                                                              long long Cp, int n_tiles, int fp16) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    float* f32 = reinterpret_cast<float*>(smem);                              // [TSTAGES][TBK][TBM + TBN]
-    unsigned char* hbuf = smem + TSTAGES * kF32Stage;                         // [THBUF][A | B]
-    u64* bars = reinterpret_cast<u64*>(hbuf + THBUF * kHStage);
-    u64* f_full = bars;                  // [TSTAGES]
-    u64* f_empty = f_full + TSTAGES;     // [TSTAGES]
-    u64* h_full = f_empty + TSTAGES;     // [THBUF]
-    u64* h_empty = h_full + THBUF;       // [THBUF]
-    u64* acc_full = h_empty + THBUF;    // [2] TMEM accumulator buffers
-    u64* acc_empty = acc_full + 2;      // [2]
+    unsigned char* ops = smem;                                   // [OSTAGES][A | B]
+    u64* bars = reinterpret_cast<u64*>(ops + OSTAGES * 2 * kOpStage);
+    u64* full = bars;                 // [OSTAGES] operands landed (complete_tx)
+    u64* empty = full + OSTAGES;      // [OSTAGES] MMAs reading the stage done (tcgen05.commit)
+    u64* acc_full = empty + OSTAGES;  // [2] accumulator buffer complete
+    u64* acc_empty = acc_full + 2;    // [2] accumulator buffer drained (4 epilogue warps)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -142,13 +127,9 @@ __global__ void __launch_bounds__(320, 1) tc_contract_kernel(const float* __rest
     const int n_tb = (int)(Tp / TBN), n_kb = (int)(Kp / TBM);
 
     if (tid == 0) {
-        for (int s = 0; s < TSTAGES; ++s) {
-            bar_init(&f_full[s], 1);
-            bar_init(&f_empty[s], 4);
-        }
-        for (int s = 0; s < THBUF; ++s) {
-            bar_init(&h_full[s], 4);
-            bar_init(&h_empty[s], 1);
+        for (int s = 0; s < OSTAGES; ++s) {
+            bar_init(&full[s], 1);
+            bar_init(&empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
             bar_init(&acc_full[s], 1);
@@ -156,7 +137,7 @@ __global__ void __launch_bounds__(320, 1) tc_contract_kernel(const float* __rest
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 0) {  // TMEM: 2 x 128 fp32 columns x 128 lanes (double-buffered accumulator)
+    if (warp == 1) {  // TMEM: 2 x 128 fp32 columns x 128 lanes (double-buffered accumulator)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
                      "r"(256u)
                      : "memory");
@@ -167,26 +148,26 @@ __global__ void __launch_bounds__(320, 1) tc_contract_kernel(const float* __rest
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 4) {
+    if (warp == 0) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
             int g = 0;
             for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
                 const int tb = tile % n_tb, rest = tile / n_tb, kb = rest % n_kb;
                 const long long p = rest / n_kb;
-                const float* gU = U + (p * Kp + (long long)kb * TBM) * Cp;
-                const float* gV = V + (p * Tp + (long long)tb * TBN) * Cp;
+                const unsigned short* gU = U + (p * Kp + (long long)kb * TBM) * Cp;
+                const unsigned short* gV = V + (p * Tp + (long long)tb * TBN) * Cp;
                 for (int kt = 0; kt < nk; ++kt, ++g) {
-                    const int s = g % TSTAGES;
-                    if (g >= TSTAGES) bar_wait(&f_empty[s], (unsigned)(((g / TSTAGES) - 1) & 1));
-                    float* dst = f32 + (size_t)s * (kF32Stage / 4);
-                    bar_expect(&f_full[s], (unsigned)kF32Stage);
-                    bulk_g2s(dst, gU + (long long)kt * TBK * TBM, TBK * TBM * 4, &f_full[s]);
-                    bulk_g2s(dst + TBK * TBM, gV + (long long)kt * TBK * TBN, TBK * TBN * 4, &f_full[s]);
+                    const int s = g % OSTAGES;
+                    if (g >= OSTAGES) bar_wait(&empty[s], (unsigned)(((g / OSTAGES) - 1) & 1));
+                    unsigned char* dst = ops + s * 2 * kOpStage;
+                    bar_expect(&full[s], (unsigned)(2 * kOpStage));
+                    bulk_g2s(dst, gU + (long long)kt * TBK * TBM, kOpStage, &full[s]);
+                    bulk_g2s(dst + kOpStage, gV + (long long)kt * TBK * TBN, kOpStage, &full[s]);
                 }
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0) {
             const unsigned idesc = instr_desc(fp16);
@@ -197,44 +178,24 @@ __global__ void __launch_bounds__(320, 1) tc_contract_kernel(const float* __rest
                 tc_fence_after();
                 const unsigned tacc = tmem + (unsigned)(ab * TBN);
                 for (int kt = 0; kt < nk; ++kt, ++g) {
-                    const int h = g % THBUF;
-                    bar_wait(&h_full[h], (unsigned)((g / THBUF) & 1));
+                    const int s = g % OSTAGES;
+                    bar_wait(&full[s], (unsigned)((g / OSTAGES) & 1));
                     tc_fence_after();
-                    const unsigned a0 = su32(hbuf + h * kHStage);
-                    const unsigned b0 = a0 + TBK * TBM * 2;
+                    const unsigned a0 = su32(ops + s * 2 * kOpStage);
+                    const unsigned b0 = a0 + kOpStage;
 #pragma unroll
                     for (int ks = 0; ks < TBK / 16; ++ks) {
                         const u64 da = smem_desc(a0 + ks * 2 * LBO_A, LBO_A, 128);
                         const u64 db = smem_desc(b0 + ks * 2 * LBO_B, LBO_B, 128);
                         mma_f16(tacc, da, db, idesc, (kt | ks) ? 1u : 0u);
                     }
-                    mma_commit(&h_empty[h]);  // operand buffer h free once these MMAs finish
+                    mma_commit(&empty[s]);  // stage s free once these MMAs finish
                 }
                 mma_commit(&acc_full[ab]);  // accumulator buffer ab complete
             }
         }
-    } else if (warp < 4) {
-        // ------------------------------------------------------------ converters
-        int g = 0;
-        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-            for (int kt = 0; kt < nk; ++kt, ++g) {
-                const int s = g % TSTAGES, h = g % THBUF;
-                bar_wait(&f_full[s], (unsigned)((g / TSTAGES) & 1));
-                if (g >= THBUF) bar_wait(&h_empty[h], (unsigned)(((g / THBUF) - 1) & 1));
-                const float* src = f32 + (size_t)s * (kF32Stage / 4);
-                unsigned char* dst = hbuf + h * kHStage;
-                convert_stage<TBM, LBO_A>(src, dst, tid, fp16);
-                convert_stage<TBN, LBO_B>(src + TBK * TBM, dst + TBK * TBM * 2, tid, fp16);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
-                __syncwarp();
-                if (lane == 0) {
-                    bar_arrive(&h_full[h]);
-                    bar_arrive(&f_empty[s]);
-                }
-            }
-        }
     } else {
-        // ------------------------------------------------------------ epilogue warps 6..9
+        // ------------------------------------------------------------ epilogue warps 2..5
         // TMEM lane quarter (warp % 4) = rows k of this warp
         const int q4 = warp & 3;
         int it = 0;
@@ -273,7 +234,7 @@ __global__ void __launch_bounds__(320, 1) tc_contract_kernel(const float* __rest
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) {
+    if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256u) : "memory");
     }
@@ -288,7 +249,7 @@ int tc_contract_launch(const void* U, const void* V, void* M, long long Kp, long
     if (Kp % TBM || Tp % TBN || Cp % TBK) return fail(WINO_EINVAL, "tc_contract: layout not padded to 128/128/32");
     const long long tiles = (long long)P * (Kp / TBM) * (Tp / TBN);
     if (tiles > (1LL << 30)) return fail(WINO_EUNSUPPORTED, "tc_contract: too many tiles");
-    const size_t smem = (size_t)TSTAGES * kF32Stage + (size_t)THBUF * kHStage + 256;
+    const size_t smem = (size_t)OSTAGES * 2 * kOpStage + 256;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(tc_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -298,8 +259,9 @@ int tc_contract_launch(const void* U, const void* V, void* M, long long Kp, long
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = (int)(tiles < sms ? tiles : sms);
-    tc_contract_kernel<<<grid, 320, smem, (cudaStream_t)stream>>>((const float*)U, (const float*)V, (float*)M, Kp,
-                                                                 Tp, Cp, (int)tiles, fp16);
+    tc_contract_kernel<<<grid, 192, smem, (cudaStream_t)stream>>>((const unsigned short*)U,
+                                                                 (const unsigned short*)V, (float*)M, Kp, Tp, Cp,
+                                                                 (int)tiles, fp16);
     return after_launch("tc_contract");
 }
 

@@ -266,11 +266,12 @@ int layout_of(const wino_plan* p, const wino_layer_shape* s, wino_layer_layout* 
     L->Tp = round_up(L->T > 0 ? L->T : 1, p->gemm.bn());
     L->Cp = round_up(s->C, p->gemm.bk);
     L->Kp = round_up(s->K, p->gemm.bm());
-    L->elem_bytes_uv = p->ty.uv_double ? 8 : 4;
+    const bool tc = p->mode >= WINO_CONTRACT_TC_BF16;
+    L->elem_bytes_uv = tc ? 2 : p->ty.uv_double ? 8 : 4;  // tc: 16-bit U/V, fp32 M
     L->elem_bytes_y = p->ty.y_double ? 8 : 4;
     L->u_bytes = (size_t)L->P * L->Cp * L->Kp * L->elem_bytes_uv;
     L->v_bytes = (size_t)L->P * L->Cp * L->Tp * L->elem_bytes_uv;
-    L->m_bytes = (size_t)L->P * L->Kp * L->Tp * L->elem_bytes_uv;
+    L->m_bytes = (size_t)L->P * L->Kp * L->Tp * (tc ? 4 : L->elem_bytes_uv);
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     L->workspace_bytes = al(L->u_bytes) + al(L->v_bytes) + al(L->m_bytes);
     return WINO_OK;
@@ -281,7 +282,7 @@ inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) /
 // K1 / K4 block size (must match codegen.cpp): 128 tiles, halved while the
 // P x TB smem staging buffer exceeds 64 KB.
 int xform_block(const wino_plan* p, int* smem) {
-    const int P = p->n * p->n, es = p->ty.uv_double ? 8 : 4;
+    const int P = p->n * p->n, es = (p->ty.uv_double && p->mode < WINO_CONTRACT_TC_BF16) ? 8 : 4;
     int tb = 128;
     while (tb > 32 && (long long)P * tb * es > 64 * 1024) tb /= 2;
     *smem = P * tb * es;
@@ -348,7 +349,10 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
     }
     const std::string tag = "r" + std::to_string(r) + "m" + std::to_string(m) + "p" + std::to_string(precision);
     p->layer.name = "wino_layer_" + tag + ".cu";
-    p->layer.source = wino::gen_layer_source(r, m, p->G, p->BT, p->AT, p->ty, p->gemm.bm(), p->gemm.bn());
+    p->layer.source = contract_mode >= WINO_CONTRACT_TC_BF16
+                          ? wino::gen_layer_source_tc(r, m, p->G, p->BT, p->AT, p->ty,
+                                                      contract_mode == WINO_CONTRACT_TC_FP16)
+                          : wino::gen_layer_source(r, m, p->G, p->BT, p->AT, p->ty, p->gemm.bm(), p->gemm.bn());
     p->tile.name = "wino_tile_" + tag + ".cu";
     p->tile.source = wino::gen_tile_source(r, m, p->G, p->BT, p->AT, p->ty);
     int rc = p->layer.ensure_compiled();
@@ -396,7 +400,7 @@ int wino_filter_transform(wino_plan* plan, const wino_layer_shape* s, const void
     int K = s->K, C = s->C;
     long long Kp = L.Kp, Cp = L.Cp;
     int smem = 0;
-    const int tb = xform_block(plan, &smem);
+    const int tb = plan->mode >= WINO_CONTRACT_TC_BF16 ? 64 : xform_block(plan, &smem);
     void* args[] = {(void*)&w, &U, &K, &C, &Kp, &Cp};
     return wino::launch(f, dim3(cdiv(Kp, tb), (unsigned)Cp, 1), dim3(tb), 0, stream, args, "filter_transform");
 }
@@ -412,9 +416,11 @@ int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, c
     int C = s->C, H = s->H, W = s->W, pad = s->pad, th = L.th, tw = L.tw, K = s->K;
     long long T = L.T, Tp = L.Tp, Cp = L.Cp, Kp = L.Kp;
     int smem = 0;
-    const int tb = xform_block(plan, &smem);
+    const bool tc = plan->mode >= WINO_CONTRACT_TC_BF16;
+    const int tb = tc ? 64 : xform_block(plan, &smem);
+    if (tc) smem = L.P * 64 * 8 * 2;
     int n_tb = (int)cdiv(Tp, tb), n_kb = (int)cdiv(Kp, tb);
-    const long long blocks = (long long)n_tb * Cp + (long long)n_kb * Cp;
+    const long long blocks = (long long)n_tb * (tc ? Cp / 8 : Cp) + (long long)n_kb * Cp;
     if (blocks >= (1LL << 31)) return wino::fail(WINO_EUNSUPPORTED, "transforms: grid too large");
     void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &n_tb, (void*)&w, &U, &K, &Kp, &n_kb};
     return wino::launch(f, dim3((unsigned)blocks, 1, 1), dim3(tb), (unsigned)smem, stream, args, "transforms");
@@ -430,8 +436,11 @@ int wino_input_transform(wino_plan* plan, const wino_layer_shape* s, const void*
     int C = s->C, H = s->H, W = s->W, pad = s->pad, th = L.th, tw = L.tw;
     long long T = L.T, Tp = L.Tp, Cp = L.Cp;
     int smem = 0;
-    const int tb = xform_block(plan, &smem);
     void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp};
+    if (plan->mode >= WINO_CONTRACT_TC_BF16)
+        return wino::launch(f, dim3(cdiv(Tp, 64), (unsigned)(Cp / 8), 1), dim3(64), (unsigned)(L.P * 64 * 16),
+                            stream, args, "input_transform");
+    const int tb = xform_block(plan, &smem);
     return wino::launch(f, dim3(cdiv(Tp, tb), (unsigned)Cp, 1), dim3(tb), (unsigned)smem, stream, args,
                         "input_transform");
 }

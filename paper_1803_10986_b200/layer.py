@@ -76,8 +76,19 @@ class LayerOp:
         return out
 
     # -- individual stages (tests, profiling) --------------------------------
+    @property
+    def tensor_core(self) -> bool:
+        return self.contraction.startswith("tc_")
+
     def _uv_dtype(self):
+        if self.contraction == "tc_bf16":
+            return D.torch.bfloat16
+        if self.contraction == "tc_fp16":
+            return D.torch.float16
         return D.torch.float64 if self.cfg.precision == "fp64" else D.torch.float32
+
+    def _m_dtype(self):
+        return D.torch.float32 if self.tensor_core else self._uv_dtype()
 
     def filter_transform(self, w):
         L = self.layout
@@ -93,19 +104,47 @@ class LayerOp:
                                                          D.ptr(V), D.stream_handle()), "input_transform")
         return V
 
-    def unblock_u(self, U):
-        """blocked U[P][Kp/bm][Cp][bm] -> U[P][Cp][Kp]"""
+    # Tensor-core modes keep U/V as 16-bit UMMA operands:
+    #   X16[p][row/128][c/32][(c/8)%4][(row%128)/8][row%8][c%8]
+    def _tc_unpack(self, X, R):
         L = self.layout
+        return X.reshape(L.P, R // 128, L.Cp // 32, 4, 16, 8, 8).permute(0, 2, 3, 6, 1, 4, 5).reshape(L.P, L.Cp, R)
+
+    def _tc_pack(self, X, R):
+        L = self.layout
+        return X.reshape(L.P, L.Cp // 32, 4, 8, R // 128, 16, 8).permute(0, 4, 1, 2, 5, 6, 3).contiguous()
+
+    def unblock_u(self, U):
+        """device layout of U -> dense U[P][Cp][Kp]"""
+        L = self.layout
+        if self.tensor_core:
+            return self._tc_unpack(U, L.Kp)
         return U.reshape(L.P, L.Kp // L.bm, L.Cp, L.bm).permute(0, 2, 1, 3).reshape(L.P, L.Cp, L.Kp)
 
     def unblock_v(self, V):
-        """blocked V[P][Tp/bn][Cp][bn] -> V[P][Cp][Tp]"""
+        """device layout of V -> dense V[P][Cp][Tp]"""
         L = self.layout
+        if self.tensor_core:
+            return self._tc_unpack(V, L.Tp)
         return V.reshape(L.P, L.Tp // L.bn, L.Cp, L.bn).permute(0, 2, 1, 3).reshape(L.P, L.Cp, L.Tp)
+
+    def block_u(self, U):
+        """dense U[P][Cp][Kp] -> device layout"""
+        L = self.layout
+        if self.tensor_core:
+            return self._tc_pack(U.to(self._uv_dtype()), L.Kp)
+        return U.reshape(L.P, L.Cp, L.Kp // L.bm, L.bm).permute(0, 2, 1, 3).contiguous()
+
+    def block_v(self, V):
+        """dense V[P][Cp][Tp] -> device layout"""
+        L = self.layout
+        if self.tensor_core:
+            return self._tc_pack(V.to(self._uv_dtype()), L.Tp)
+        return V.reshape(L.P, L.Cp, L.Tp // L.bn, L.bn).permute(0, 2, 1, 3).contiguous()
 
     def contract(self, U, V):
         L = self.layout
-        M = D.torch.empty((L.P, L.Kp, L.Tp), dtype=self._uv_dtype(), device="cuda")
+        M = D.torch.empty((L.P, L.Kp, L.Tp), dtype=self._m_dtype(), device="cuda")
         _native.check(_native.lib().wino_contract(self.plan.handle, ctypes.byref(self.shape), D.ptr(U), D.ptr(V),
                                                   D.ptr(M), D.stream_handle()), "contract")
         return M

@@ -16,15 +16,36 @@ def test_tc_contraction_matches_rounded_gemm(mode, dt):
     ts = W.build_transforms(3, 4, W.parse_points("0,1,-1,1/2,-1/2,inf"))
     op = W.layer_op(ts, W.ConvConfig(), 3, 70, 20, 20, 150, 1, contraction=mode)
     L = op.layout
-    U = torch.randn((L.P, L.Cp, L.Kp), device="cuda")
-    V = torch.randn((L.P, L.Cp, L.Tp), device="cuda")
+    Ud = torch.randn((L.P, L.Cp, L.Kp), device="cuda")
+    Vd = torch.randn((L.P, L.Cp, L.Tp), device="cuda")
+    U, V = op.block_u(Ud), op.block_v(Vd)
+    assert torch.equal(op.unblock_u(U), Ud.to(dt)) and torch.equal(op.unblock_v(V), Vd.to(dt))
     M = op.contract(U, V)
-    Uu = op.unblock_u(U).to(dt).double()
-    Vu = op.unblock_v(V).to(dt).double()
+    Uu = Ud.to(dt).double()
+    Vu = Vd.to(dt).double()
     ref = torch.einsum("pck,pct->pkt", Uu, Vu)
     err = (M.double() - ref).abs().max().item()
     scale = torch.einsum("pck,pct->pkt", Uu.abs(), Vu.abs()).max().item()
     assert err <= 1e-5 * scale, (err, scale)
+
+
+@pytest.mark.parametrize("mode", ["tc_bf16", "tc_fp16"])
+def test_tc_transforms_write_rounded_operands(mode):
+    """The tc transforms store exactly round16(fp32 exact transform) in the UMMA layout."""
+    pts = "0,1,-1,1/2,-1/2,inf"
+    ts = W.build_transforms(3, 4, W.parse_points(pts))
+    x = torch.from_numpy(O.synthetic((2, 13, 11, 11), 4, 0)).cuda()
+    w = torch.from_numpy(O.synthetic((9, 13, 3, 3), 4, 1)).cuda()
+    ex = W.layer_op(ts, W.ConvConfig(), 2, 13, 11, 11, 9, 1)
+    tc = W.layer_op(ts, W.ConvConfig(), 2, 13, 11, 11, 9, 1, contraction=mode)
+    dt = torch.bfloat16 if mode == "tc_bf16" else torch.float16
+    Le, Lt = ex.layout, tc.layout
+    ue = ex.unblock_u(ex.filter_transform(w))[:, :13, :9]
+    ut = tc.unblock_u(tc.filter_transform(w))[:, :13, :9]
+    assert torch.equal(ut, ue.to(dt))
+    ve = ex.unblock_v(ex.input_transform(x))[:, :13, :Le.T]
+    vt = tc.unblock_v(tc.input_transform(x))[:, :13, :Lt.T]
+    assert torch.equal(vt, ve.to(dt))
 
 
 @pytest.mark.parametrize("mode", ["tc_bf16", "tc_fp16"])
