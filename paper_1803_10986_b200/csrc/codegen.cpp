@@ -2,6 +2,7 @@
 #include "codegen.h"
 
 #include <cstdio>
+#include <map>
 #include <sstream>
 
 namespace wino {
@@ -29,20 +30,31 @@ class Emitter {
     }
 
     // Evaluate one row program over `in`; returns the name holding the result.
+    // Products fl(|c| * x) are shared between the rows of one pass (products of
+    // +c and -c differ only in sign: fl(-c*x) == -fl(c*x) exactly, and the sign
+    // is folded into the consuming add/sub).
     std::string row(const RowProg& p, const std::vector<std::string>& in) {
         if (p.ops.empty()) return dbl_ ? "0.0" : "0.0f";
         std::vector<Ref> st;
         for (const wino_op& op : p.ops) {
             if (op.kind == WINO_OP_LEAF) {
                 const std::string& x = in[op.col];
-                if (op.coeff == 1.0) {
-                    st.push_back({x, false});
-                } else if (op.coeff == -1.0) {
-                    st.push_back({x, true});
+                const double mag = op.coeff < 0 ? -op.coeff : op.coeff;
+                const bool neg = op.coeff < 0;
+                if (mag == 1.0) {
+                    st.push_back({x, neg});
                 } else {
-                    std::string t = fresh();
-                    os_ << "  const " << type() << " " << t << " = " << mul(lit(op.coeff), x) << ";\n";
-                    st.push_back({t, false});
+                    const std::string key = x + "*" + lit(mag);
+                    auto it = products_.find(key);
+                    std::string t;
+                    if (it != products_.end()) {
+                        t = it->second;
+                    } else {
+                        t = fresh();
+                        os_ << "  const " << type() << " " << t << " = " << mul(lit(mag), x) << ";\n";
+                        products_[key] = t;
+                    }
+                    st.push_back({t, neg});
                 }
             } else {
                 Ref b = st.back();
@@ -111,6 +123,7 @@ class Emitter {
     std::ostringstream& os_;
     bool dbl_;
     int& ctr_;
+    std::map<std::string, std::string> products_;  // "x*|c|" -> SSA name (per emitter)
 };
 
 const char* tname(bool d) { return d ? "double" : "float"; }

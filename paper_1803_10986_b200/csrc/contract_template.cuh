@@ -40,6 +40,9 @@
 #ifndef WINO_KU
 #define WINO_KU WINO_BK
 #endif
+#ifndef WINO_NOPROD
+#define WINO_NOPROD 0  // 1: no producer warp; the last consumer warp to release a stage refills it
+#endif
 #ifndef WINO_DBUF
 #define WINO_DBUF (WINO_SUM == 1 || WINO_SUM == 3)  // explicit fragment double buffer (pairwise)
 #endif
@@ -112,7 +115,7 @@ static __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsi
 #if WINO_MAXREG > 0
 #define WINO_REGS __maxnreg__(WINO_MAXREG)
 #else
-#define WINO_REGS __launch_bounds__(NTHR + 32)
+#define WINO_REGS __launch_bounds__(NTHR + (WINO_NOPROD ? 0 : 32))
 #endif
 
 extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, const DT* __restrict__ V,
@@ -129,17 +132,43 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
     const int nk = (int)(Cp / WINO_BK);
     const int n_tb = (int)(Tp / BN), n_kb = (int)(Kp / BM);
 
+#if WINO_NOPROD
+    unsigned* cnt = reinterpret_cast<unsigned*>(empty);  // per-stage release counters
+    auto issue = [&](int gg) {
+        const int it = gg / nk, kt = gg - it * nk;
+        const int tile = blockIdx.x + it * gridDim.x;
+        if (tile >= n_tiles) return;
+        const int tb = tile % n_tb;
+        const int rest = tile / n_tb;
+        const int kb = rest % n_kb;
+        const long long p = rest / n_kb;
+        const int s = gg % WINO_STAGES;
+        const DT* gU = U + (p * Kp + (long long)kb * BM) * Cp + (long long)kt * WINO_BK * BM;
+        const DT* gV = V + (p * Tp + (long long)tb * BN) * Cp + (long long)kt * WINO_BK * BN;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&full[s], (unsigned)(WINO_BK * (BM + BN) * sizeof(DT)));
+        bulk_g2s(sU + s * WINO_BK * BM, gU, WINO_BK * BM * sizeof(DT), &full[s]);
+        bulk_g2s(sV + s * WINO_BK * BN, gV, WINO_BK * BN * sizeof(DT), &full[s]);
+    };
+#endif
     if (tid == 0) {
 #pragma unroll
         for (int s = 0; s < WINO_STAGES; ++s) {
             mbar_init(&full[s], 1);
+#if WINO_NOPROD
+            cnt[2 * s] = 0;
+#else
             mbar_init(&empty[s], NCW);
+#endif
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#if WINO_NOPROD
+        for (int gg = 0; gg < WINO_STAGES; ++gg) issue(gg);
+#endif
     }
     __syncthreads();
 
-    if (warp == NCW) {
+    if (!WINO_NOPROD && warp == NCW) {
         // ------------------------------------------------ producer warp
         if (lane == 0) {
             int g = 0;  // global stage counter across this CTA's tiles
@@ -323,7 +352,17 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
                 }
             }
             __syncwarp();
+#if WINO_NOPROD
+            if (lane == 0) {
+                // the last warp to release stage s refills it with stage g + STAGES
+                if (atomicAdd(&cnt[2 * s], 1u) == NCW - 1) {
+                    cnt[2 * s] = 0;
+                    issue(g + WINO_STAGES);
+                }
+            }
+#else
             if (lane == 0) mbar_arrive(&empty[s]);
+#endif
         }
 
 #if WINO_SUM == 1 || WINO_SUM == 3

@@ -185,9 +185,11 @@ static const char* kContractTemplate =
 
 struct GemmCfg {
     int tm, tn, thm, thn, bk, stages, maxreg, ku = 0;  // ku: k-steps unrolled per inner loop (0 = bk)
+    int noprod = 0;  // 1: no producer warp (last consumer warp to release a stage refills it)
     int bm() const { return thm * tm; }
     int bn() const { return thn * tn; }
     int threads() const { return thm * thn; }
+    int block() const { return thm * thn + (noprod ? 0 : 32); }
 };
 
 }  // namespace wino
@@ -219,7 +221,7 @@ struct wino_plan {
            << "\n#define WINO_TM " << gemm.tm << "\n#define WINO_TN " << gemm.tn << "\n#define WINO_THM " << gemm.thm
            << "\n#define WINO_THN " << gemm.thn << "\n#define WINO_BK " << gemm.bk << "\n#define WINO_STAGES "
            << gemm.stages << "\n#define WINO_SUM " << sum_mode() << "\n#define WINO_LEVELS "
-           << (levels > 0 ? levels : 1) << "\n#define WINO_MAXREG " << gemm.maxreg << "\n#define WINO_KU " << (gemm.ku > 0 ? gemm.ku : gemm.bk) << "\n"
+           << (levels > 0 ? levels : 1) << "\n#define WINO_MAXREG " << gemm.maxreg << "\n#define WINO_KU " << (gemm.ku > 0 ? gemm.ku : gemm.bk) << "\n#define WINO_NOPROD " << gemm.noprod << "\n"
            << wino::kContractTemplate;
         mod->source = os.str();
         mod->name = "wino_contract_s" + std::to_string(sum_mode()) + "_L" + std::to_string(levels) + ".cu";
@@ -342,8 +344,8 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
         p->gemm = {8, 8, 16, 8, 16, 4, 0, 8};
     if (const char* env = getenv("WINO_GEMM")) {  // tuning override: tm,tn,thm,thn,bk,stages,maxreg
         wino::GemmCfg g{};
-        const int got = sscanf(env, "%d,%d,%d,%d,%d,%d,%d,%d", &g.tm, &g.tn, &g.thm, &g.thn, &g.bk, &g.stages,
-                               &g.maxreg, &g.ku);
+        const int got = sscanf(env, "%d,%d,%d,%d,%d,%d,%d,%d,%d", &g.tm, &g.tn, &g.thm, &g.thn, &g.bk, &g.stages,
+                               &g.maxreg, &g.ku, &g.noprod);
         if (got >= 7 && g.bk % 8 == 0 && g.tm % 4 == 0 && g.tn % 4 == 0 && (g.ku == 0 || g.bk % g.ku == 0))
             p->gemm = g;
     }
@@ -463,7 +465,7 @@ int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, con
     if (tiles > (1LL << 30)) return wino::fail(WINO_EUNSUPPORTED, "contract: too many tiles");
     int n_tiles = (int)tiles;
     const unsigned smem = (unsigned)(g.stages * g.bk * (g.bm() + g.bn()) * L.elem_bytes_uv + 2 * g.stages * 8);
-    const int threads = g.threads() + 32;
+    const int threads = g.block();
     // persistent grid: as many CTAs as can be co-resident (one wave), each walks tiles
     int per_sm = 0, sms = 0, dev = 0;
     if (smem > 48 * 1024) {
