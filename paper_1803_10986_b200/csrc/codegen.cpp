@@ -174,14 +174,14 @@ std::string validate(const MatProg& m, int expect_rows, int expect_cols, const c
 // fp32 for the tensor-core modes).  The block stages M[.][k][t0 .. t0+TB) for
 // all P points through shared memory with 16-byte coalesced loads, then each
 // thread transforms one tile.
-static void emit_output_kernel(std::ostringstream& os, int r, int m, const MatProg& AT, const GenTypes& ty, int TB,
+static void emit_output_flat(std::ostringstream& os, int r, int m, const MatProg& AT, const GenTypes& ty, int TB,
                                int& ctr, const char* mt = "uv_t", int mes = 0) {
     const int n = r + m - 1, P = n * n;
     const int es = mes ? mes : (ty.uv_double ? 8 : 4);
     const int VEC = 16 / es;
     const char* VT = es == 8 ? "double2" : "float4";
     {
-        os << "extern \"C\" __global__ void __launch_bounds__(" << TB << ") wino_output_xform(\n"
+        os << "extern \"C\" __global__ void __launch_bounds__(" << TB << ") wino_output_flat(\n"
               "    const " << mt << "* __restrict__ Mm, y_t* __restrict__ y, int K, int Ho, int Wo, int th, int tw,\n"
               "    long long T, long long Tp, long long Kp) {\n"
               "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
@@ -230,6 +230,70 @@ static void emit_output_kernel(std::ostringstream& os, int r, int m, const MatPr
         }
         os << "  }\n}\n";
     }
+}
+static void emit_output_kernel(std::ostringstream& os, int r, int m, const MatProg& AT, const GenTypes& ty, int TB,
+                               int& ctr, const char* mt = "uv_t", int mes = 0) {
+    (void)TB;
+    (void)mes;
+    const int n = r + m - 1;
+    // Block = (band of R tile rows of one image) x (KB output channels); 128
+    // threads loop over its KB*R*tw tiles.  Each tile's m x m outputs are
+    // parked in shared memory as image rows, then the block writes the band's
+    // rows -- contiguous in y[img][k] -- with coalesced stores (per-thread m x m
+    // patches would scatter each warp store over ~m rows).
+    os << "extern \"C\" __global__ void __launch_bounds__(128, 4) wino_output_xform(\n"
+          "    const " << mt << "* __restrict__ Mm, y_t* __restrict__ y, int K, int Ho, int Wo, int th, int tw,\n"
+          "    long long T, long long Tp, long long Kp, int R, int KB) {\n"
+          "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
+          "  y_t* so = reinterpret_cast<y_t*>(smem_raw);  // [KB][R*m][Wo]\n"
+          "  const int band = blockIdx.x, kg = blockIdx.y, img = blockIdx.z;\n"
+       << "  const int rows = min(R * " << m << ", Ho - band * R * " << m << ");\n"
+          "  const int items = KB * R * tw;\n"
+          "  const long long plane = Kp * Tp;\n"
+          "  const int per = th * tw;\n"
+          "#pragma unroll 1\n"
+          "  for (int it = threadIdx.x; it < items; it += 128) {\n"
+          "    const int kk = it / (R * tw);\n"
+          "    const int rem = it - kk * (R * tw);\n"
+          "    const int til = rem / tw, tj = rem - til * tw;\n"
+          "    const int k = kg * KB + kk, ti = band * R + til;\n"
+          "    if (k >= K || ti >= th) continue;\n"
+          "    const " << mt << "* src = Mm + (long long)k * Tp + ((long long)img * per + ti * tw + tj);\n";
+    std::vector<std::vector<std::string>> mm(n, std::vector<std::string>(n));
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+            mm[a][b] = "m" + std::to_string(a) + "_" + std::to_string(b);
+            os << "    const ct_t " << mm[a][b] << " = (ct_t)__ldg(src + " << (a * n + b) << " * plane);\n";
+        }
+    Emitter em(os, ty.compute_double, ctr);
+    auto yv = em.apply2d(AT, mm);
+    os << "    y_t* d = so + ((long long)kk * R * " << m << " + til * " << m << ") * Wo + tj * " << m << ";\n"
+       << "    const int y0 = ti * " << m << ", x0 = tj * " << m << ";\n"
+       << "    if (y0 + " << m << " <= Ho && x0 + " << m << " <= Wo) {\n";
+    for (int a = 0; a < m; ++a)
+        for (int b = 0; b < m; ++b)
+            os << "      d[" << a << " * Wo + " << b << "] = " << store_cvt(ty.compute_double, ty.y_double, yv[a][b])
+               << ";\n";
+    os << "    } else {\n";
+    for (int a = 0; a < m; ++a) {
+        os << "      if (y0 + " << a << " < Ho) {\n";
+        for (int b = 0; b < m; ++b)
+            os << "        if (x0 + " << b << " < Wo) d[" << a << " * Wo + " << b
+               << "] = " << store_cvt(ty.compute_double, ty.y_double, yv[a][b]) << ";\n";
+        os << "      }\n";
+    }
+    os << "    }\n  }\n"
+          "  __syncthreads();\n"
+          "  // the band's rows of each output channel are contiguous in y\n"
+          "#pragma unroll 1\n"
+          "  for (int kk = 0; kk < KB; ++kk) {\n"
+          "    const int k = kg * KB + kk;\n"
+          "    if (k >= K) break;\n"
+       << "    y_t* dst = y + (((long long)img * K + k) * Ho + band * R * " << m << ") * Wo;\n"
+       << "    const y_t* sb = so + (long long)kk * R * " << m << " * Wo;\n"
+          "    const int cnt = rows * Wo;\n"
+          "    for (int i = threadIdx.x; i < cnt; i += 128) dst[i] = sb[i];\n"
+          "  }\n}\n";
 }
 
 std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
@@ -369,6 +433,12 @@ std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, 
           "}\n\n";
 
     emit_output_kernel(os, r, m, AT, ty, TB, ctr);
+    {
+        const int es4 = ty.uv_double ? 8 : 4;
+        int tbf = 128;
+        while (tbf > 32 && (long long)P * tbf * es4 > 64 * 1024) tbf /= 2;
+        emit_output_flat(os, r, m, AT, ty, tbf, ctr);
+    }
     return os.str();
 }
 
@@ -609,6 +679,7 @@ std::string gen_layer_source_tc(int r, int m, const MatProg& G, const MatProg& B
     int TB = 128;
     while (TB > 32 && (long long)P * TB * 4 > 64 * 1024) TB /= 2;
     emit_output_kernel(os, r, m, AT, ty, TB, ctr, "float", 4);
+    emit_output_flat(os, r, m, AT, ty, TB, ctr, "float", 4);
     return os.str();
 }
 

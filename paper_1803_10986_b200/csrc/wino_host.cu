@@ -486,16 +486,35 @@ int wino_output_transform(wino_plan* plan, const wino_layer_shape* s, const void
     wino_layer_layout L;
     int rc = layout_of(plan, s, &L);
     if (rc) return rc;
-    if ((uintptr_t)M & 15) return wino::fail(WINO_EINVAL, "output_transform: M must be 16-byte aligned");
     CUfunction f;
-    if ((rc = plan->layer.function("wino_output_xform", &f))) return rc;
     int K = s->K, Ho = L.Ho, Wo = L.Wo, th = L.th, tw = L.tw;
     long long T = L.T, Tp = L.Tp, Kp = L.Kp;
-    int smem = 0;
-    const int tb = xform_block(plan, &smem);
-    void* args[] = {(void*)&M, &y, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp};
-    return wino::launch(f, dim3(cdiv(T, tb), (unsigned)K, 1), dim3(tb), (unsigned)smem, stream, args,
-                        "output_transform");
+    if (plan->m <= 2) {
+        // small output blocks: one thread per (k, tile), M staged per 128 tiles,
+        // per-thread m x m stores (rows of m <= 2 values)
+        if ((rc = plan->layer.function("wino_output_flat", &f))) return rc;
+        int smem = 0;
+        const int tb = xform_block(plan, &smem);
+        void* fargs[] = {(void*)&M, &y, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp};
+        return wino::launch(f, dim3(cdiv(T, tb), (unsigned)K, 1), dim3(tb), (unsigned)smem, stream, fargs,
+                            "output_transform");
+    }
+    if ((rc = plan->layer.function("wino_output_xform", &f))) return rc;
+    // block = R tile rows of one image x KB output channels (~256 tiles), output
+    // band staged in smem (<= 96 KB)
+    const int es = L.elem_bytes_y, m = plan->m;
+    int R = th * tw <= 256 ? th : (256 / tw > 0 ? 256 / tw : 1);
+    int KB = th * tw <= 256 ? std::max(1, std::min(K, 256 / (th * tw))) : 1;
+    auto smem_of = [&](int kb, int rr) { return (long long)kb * rr * m * Wo * es; };
+    while (KB > 1 && smem_of(KB, R) > 96 * 1024) --KB;
+    while (R > 1 && smem_of(KB, R) > 96 * 1024) --R;
+    if (smem_of(KB, R) > 200 * 1024) return wino::fail(WINO_EUNSUPPORTED, "output_transform: image too wide");
+    const int nbands = (th + R - 1) / R;
+    const unsigned smem = (unsigned)smem_of(KB, R);
+    void* args[] = {(void*)&M, &y, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp, &R, &KB};
+    if (s->N > 65535) return wino::fail(WINO_EUNSUPPORTED, "output_transform: N > 65535");
+    return wino::launch(f, dim3((unsigned)nbands, (unsigned)((K + KB - 1) / KB), (unsigned)s->N), dim3(128), smem,
+                        stream, args, "output_transform");
 }
 
 int wino_conv2d(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w, void* y, void* workspace,
