@@ -296,6 +296,92 @@ static void emit_output_kernel(std::ostringstream& os, int r, int m, const MatPr
           "  }\n}\n";
 }
 
+// q = a / b for 0 <= a < 2^22 (rb = 1/b rounded): float estimate, then exact correction
+static const char* kIdivSmall =
+    "static __device__ __forceinline__ int idiv_small(int a, int b, float rb) {\n"
+    "  int q = (int)((float)a * rb);\n"
+    "  q -= (q * b > a);\n"
+    "  q += ((q + 1) * b <= a);\n"
+    "  return q;\n"
+    "}\n\n";
+
+// K1, gather form with direct stores: thread = one (tile, channel); the
+// alpha x alpha window is gathered from global memory (zero padding fused,
+// unpredicated interior path) and the P values are stored straight from
+// registers -- a warp's store of one p covers 32 consecutive t of the blocked
+// V, one aligned 128-byte line.  Grid (Cp, n_tb [+ n_kb filter rows]).
+static void emit_input_gather(std::ostringstream& os, int r, int m, const MatProg& BT, const GenTypes& ty, int bn,
+                              int TB, int& ctr) {
+    const int n = r + m - 1, P = n * n;
+    os << kIdivSmall;
+    os << "static __device__ __forceinline__ void input_gather_body(const in_t* __restrict__ x, uv_t* __restrict__ V,\n"
+          "    int C, int H, int W, int pad, int th, int tw, long long T, long long Tp, long long Cp,\n"
+          "    float rtw, float rth, int t0, int c) {\n"
+          "  const long long plane = Cp * Tp;\n"
+          "  const long long tt = (long long)t0 + threadIdx.x;\n"
+       << "  if (tt >= Tp) return;\n"
+       << "  uv_t* op = V + ((tt / " << bn << ") * Cp + c) * " << bn << " + (tt % " << bn << ");\n"
+       << "  if (c >= C || tt >= T) {\n"
+          "    const uv_t z = (c >= C) ? (uv_t)(-0.0) : (uv_t)0;\n"
+          "#pragma unroll\n"
+       << "    for (int p = 0; p < " << P << "; ++p) op[p * plane] = z;\n"
+          "    return;\n"
+          "  }\n"
+          "  const int g0 = t0 / tw, off0 = t0 - g0 * tw;\n"
+          "  const int img0 = g0 / th, ti0 = g0 - img0 * th;\n"
+          "  const int off = off0 + threadIdx.x;\n"
+          "  const int k = idiv_small(off, tw, rtw), tj = off - k * tw;\n"
+          "  const int di = idiv_small(ti0 + k, th, rth);\n"
+          "  const int ti = ti0 + k - di * th;\n"
+       << "  const int h0 = ti * " << m << " - pad, w0 = tj * " << m << " - pad;\n"
+       << "  const in_t* src = x + ((long long)(img0 + di) * C + c) * ((long long)H * W);\n";
+    std::vector<std::vector<std::string>> d(n, std::vector<std::string>(n));
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+            d[a][b] = "x" + std::to_string(a) + "_" + std::to_string(b);
+            os << "  ct_t " << d[a][b] << ";\n";
+        }
+    os << "  if (h0 >= 0 && w0 >= 0 && h0 + " << n << " <= H && w0 + " << n << " <= W) {\n"
+       << "    const in_t* rp = src + h0 * W + w0;\n";
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b)
+            os << "    " << d[a][b] << " = (ct_t)__ldg(rp + " << a << " * W + " << b << ");\n";
+    os << "  } else {\n";
+    for (int a = 0; a < n; ++a)
+        os << "    const bool r" << a << " = (unsigned)(h0 + " << a << ") < (unsigned)H;\n";
+    for (int b = 0; b < n; ++b)
+        os << "    const bool c" << b << " = (unsigned)(w0 + " << b << ") < (unsigned)W;\n";
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b)
+            os << "    " << d[a][b] << " = (r" << a << " && c" << b << ") ? (ct_t)__ldg(src + (h0 + " << a
+               << ") * W + (w0 + " << b << ")) : (ct_t)0;\n";
+    os << "  }\n";
+    Emitter em(os, ty.compute_double, ctr);
+    auto v = em.apply2d(BT, d);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j)
+            os << "  op[" << (i * n + j) << " * plane] = " << store_cvt(ty.compute_double, ty.uv_double, v[i][j])
+               << ";\n";
+    os << "}\n\n";
+    os << "extern \"C\" __global__ void __launch_bounds__(" << TB << ") wino_input_gather(\n"
+          "    const in_t* __restrict__ x, uv_t* __restrict__ V, int C, int H, int W, int pad, int th,\n"
+          "    int tw, long long T, long long Tp, long long Cp, int Wl, float rtw, float rth) {\n"
+       << "  input_gather_body(x, V, C, H, W, pad, th, tw, T, Tp, Cp, rtw, rth, blockIdx.y * " << TB
+       << ", blockIdx.x);\n"
+       << "}\n\n"
+       << "extern \"C\" __global__ void __launch_bounds__(" << TB << ") wino_transforms_gather(\n"
+          "    const in_t* __restrict__ x, uv_t* __restrict__ V, int C, int H, int W, int pad, int th,\n"
+          "    int tw, long long T, long long Tp, long long Cp, int n_tb,\n"
+          "    const in_t* __restrict__ w, uv_t* __restrict__ U, int K, long long Kp, int Wl, float rtw, float rth) {\n"
+          "  if ((int)blockIdx.y < n_tb) {\n"
+       << "    input_gather_body(x, V, C, H, W, pad, th, tw, T, Tp, Cp, rtw, rth, blockIdx.y * " << TB
+       << ", blockIdx.x);\n"
+       << "  } else {\n"
+       << "    filter_body(w, U, K, C, Kp, Cp, (blockIdx.y - n_tb) * " << TB << " + threadIdx.x, blockIdx.x);\n"
+          "  }\n"
+          "}\n\n";
+}
+
 std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
                              const GenTypes& ty, int bm, int bn) {
     const int n = r + m - 1, P = n * n;
@@ -419,19 +505,21 @@ std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, 
        << "extern \"C\" __global__ void __launch_bounds__(" << TB << ") wino_transforms(\n"
           "    const in_t* __restrict__ x, uv_t* __restrict__ V, int C, int H, int W, int pad, int th,\n"
           "    int tw, long long T, long long Tp, long long Cp, int n_tb,\n"
-          "    const in_t* __restrict__ w, uv_t* __restrict__ U, int K, long long Kp, int n_kb) {\n"
+          "    const in_t* __restrict__ w, uv_t* __restrict__ U, int K, long long Kp, int n_kb, int cfast) {\n"
           "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
           "  const int b = blockIdx.x;\n"
           "  const int n_in = n_tb * (int)Cp;\n"
           "  if (b < n_in) {\n"
-       << "    input_body(x, V, reinterpret_cast<uv_t*>(smem_raw), C, H, W, pad, th, tw, T, Tp, Cp, (b % n_tb) * "
-       << TB << ", b / n_tb);\n"
+          "    const int tb = cfast ? b / (int)Cp : b % n_tb, c = cfast ? b % (int)Cp : b / n_tb;\n"
+       << "    input_body(x, V, reinterpret_cast<uv_t*>(smem_raw), C, H, W, pad, th, tw, T, Tp, Cp, tb * "
+       << TB << ", c);\n"
           "  } else {\n"
           "    const int f = b - n_in;\n"
        << "    filter_body(w, U, K, C, Kp, Cp, (f % n_kb) * " << TB << " + threadIdx.x, f / n_kb);\n"
           "  }\n"
           "}\n\n";
 
+    emit_input_gather(os, r, m, BT, ty, bn, TB, ctr);
     emit_output_kernel(os, r, m, AT, ty, TB, ctr);
     {
         const int es4 = ty.uv_double ? 8 : 4;
@@ -665,13 +753,15 @@ std::string gen_layer_source_tc(int r, int m, const MatProg& G, const MatProg& B
           "extern \"C\" __global__ void __launch_bounds__(64) wino_transforms(\n"
           "    const in_t* __restrict__ x, unsigned short* __restrict__ V, int C, int H, int W, int pad, int th,\n"
           "    int tw, long long T, long long Tp, long long Cp, int n_tb,\n"
-          "    const in_t* __restrict__ w, unsigned short* __restrict__ U, int K, long long Kp, int n_kb) {\n"
+          "    const in_t* __restrict__ w, unsigned short* __restrict__ U, int K, long long Kp, int n_kb, int cfast) {\n"
           "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
           "  const int b = blockIdx.x;\n"
-          "  const int n_in = n_tb * (int)(Cp / 8);\n"
+          "  const int ncg = (int)(Cp / 8);\n"
+          "  const int n_in = n_tb * ncg;\n"
           "  if (b < n_in) {\n"
+          "    const int tb = cfast ? b / ncg : b % n_tb, cg = cfast ? b % ncg : b / n_tb;\n"
           "    input_tc(x, V, reinterpret_cast<unsigned short*>(smem_raw), C, H, W, pad, th, tw, T, Tp, Cp,\n"
-          "             (b % n_tb) * 64, (b / n_tb) * 8);\n"
+          "             tb * 64, cg * 8);\n"
           "  } else {\n"
           "    const int f = b - n_in;\n"
           "    filter_tc(w, U, K, C, Kp, Cp, (f % n_kb) * 64 + threadIdx.x, f / n_kb);\n"

@@ -291,6 +291,28 @@ int xform_block(const wino_plan* p, int* smem) {
     return tb;
 }
 
+// K1 variant: "gather" (codegen.cpp emit_input_gather: windows gathered from
+// global memory, values stored straight from registers; default) or "tile"
+// (input_body: values parked in smem, 16-byte stores; also the fallback when
+// the gather grid (Cp, n_tb + n_kb) exceeds 65535 rows).  WINO_K1=tile selects
+// the latter for A/B timing.
+// block order of the tile kernel: channel fastest (default) or tile chunk fastest (WINO_K1ORDER=t)
+int k1_cfast() {
+    static const int v = [] {
+        const char* e = std::getenv("WINO_K1ORDER");
+        return (e && std::string(e) == "t") ? 0 : 1;
+    }();
+    return v;
+}
+
+bool k1_gather() {
+    static const bool v = [] {
+        const char* e = std::getenv("WINO_K1");
+        return !(e && std::string(e) == "tile");
+    }();
+    return v;
+}
+
 }  // namespace
 
 // ================================================================== C-ABI
@@ -414,17 +436,26 @@ int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, c
     if (rc) return rc;
     if ((uintptr_t)V & 15) return wino::fail(WINO_EINVAL, "transforms: V must be 16-byte aligned");
     CUfunction f;
-    if ((rc = plan->layer.function("wino_transforms", &f))) return rc;
     int C = s->C, H = s->H, W = s->W, pad = s->pad, th = L.th, tw = L.tw, K = s->K;
     long long T = L.T, Tp = L.Tp, Cp = L.Cp, Kp = L.Kp;
     int smem = 0;
     const bool tc = plan->mode >= WINO_CONTRACT_TC_BF16;
+    if ((rc = plan->layer.function("wino_transforms", &f))) return rc;
     const int tb = tc ? 64 : xform_block(plan, &smem);
     if (tc) smem = L.P * 64 * 8 * 2;
     int n_tb = (int)cdiv(Tp, tb), n_kb = (int)cdiv(Kp, tb);
     const long long blocks = (long long)n_tb * (tc ? Cp / 8 : Cp) + (long long)n_kb * Cp;
     if (blocks >= (1LL << 31)) return wino::fail(WINO_EUNSUPPORTED, "transforms: grid too large");
-    void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &n_tb, (void*)&w, &U, &K, &Kp, &n_kb};
+    int cfast = k1_cfast(), Wl = 0;
+    if (!tc && k1_gather() && (long long)n_tb + n_kb <= 65535 && Cp <= 65535) {
+        CUfunction fg;
+        if ((rc = plan->layer.function("wino_transforms_gather", &fg))) return rc;
+        float rtw = 1.0f / tw, rth = 1.0f / th;
+        void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &n_tb, (void*)&w, &U, &K, &Kp,
+                        &Wl, &rtw, &rth};
+        return wino::launch(fg, dim3((unsigned)Cp, (unsigned)(n_tb + n_kb)), dim3(tb), 0, stream, args, "transforms");
+    }
+    void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &n_tb, (void*)&w, &U, &K, &Kp, &n_kb, &cfast};
     return wino::launch(f, dim3((unsigned)blocks, 1, 1), dim3(tb), (unsigned)smem, stream, args, "transforms");
 }
 
@@ -434,10 +465,20 @@ int wino_input_transform(wino_plan* plan, const wino_layer_shape* s, const void*
     if (rc) return rc;
     if ((uintptr_t)V & 15) return wino::fail(WINO_EINVAL, "input_transform: V must be 16-byte aligned");
     CUfunction f;
-    if ((rc = plan->layer.function("wino_input_xform", &f))) return rc;
     int C = s->C, H = s->H, W = s->W, pad = s->pad, th = L.th, tw = L.tw;
     long long T = L.T, Tp = L.Tp, Cp = L.Cp;
     int smem = 0;
+    if (plan->mode < WINO_CONTRACT_TC_BF16 && k1_gather()) {
+        const int tb = xform_block(plan, &smem);
+        int Wl = 0, n_tb = (int)cdiv(Tp, tb);
+        if (n_tb <= 65535 && Cp <= 65535) {
+            if ((rc = plan->layer.function("wino_input_gather", &f))) return rc;
+            float rtw = 1.0f / tw, rth = 1.0f / th;
+            void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &Wl, &rtw, &rth};
+            return wino::launch(f, dim3((unsigned)Cp, (unsigned)n_tb), dim3(tb), 0, stream, args, "input_transform");
+        }
+    }
+    if ((rc = plan->layer.function("wino_input_xform", &f))) return rc;
     void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp};
     if (plan->mode >= WINO_CONTRACT_TC_BF16)
         return wino::launch(f, dim3(cdiv(Tp, 64), (unsigned)(Cp / 8), 1), dim3(64), (unsigned)(L.P * 64 * 16),
