@@ -126,6 +126,15 @@ class Emitter {
     std::map<std::string, std::string> products_;  // "x*|c|" -> SSA name (per emitter)
 };
 
+// q = a / b for 0 <= a < 2^22 (rb = 1/b rounded): float estimate, then exact correction
+static const char* kIdivSmall =
+    "static __device__ __forceinline__ int idiv_small(int a, int b, float rb) {\n"
+    "  int q = (int)((float)a * rb);\n"
+    "  q -= (q * b > a);\n"
+    "  q += ((q + 1) * b <= a);\n"
+    "  return q;\n"
+    "}\n\n";
+
 const char* tname(bool d) { return d ? "double" : "float"; }
 
 // value conversion from compute type to a storage type
@@ -140,7 +149,8 @@ std::string header(const GenTypes& ty) {
        << "typedef " << tname(ty.in_double) << " in_t;\n"
        << "typedef " << tname(ty.compute_double) << " ct_t;\n"
        << "typedef " << tname(ty.uv_double) << " uv_t;\n"
-       << "typedef " << tname(ty.y_double) << " y_t;\n";
+       << "typedef " << tname(ty.y_double) << " y_t;\n"
+       << kIdivSmall;
     return os.str();
 }
 
@@ -296,15 +306,6 @@ static void emit_output_kernel(std::ostringstream& os, int r, int m, const MatPr
           "  }\n}\n";
 }
 
-// q = a / b for 0 <= a < 2^22 (rb = 1/b rounded): float estimate, then exact correction
-static const char* kIdivSmall =
-    "static __device__ __forceinline__ int idiv_small(int a, int b, float rb) {\n"
-    "  int q = (int)((float)a * rb);\n"
-    "  q -= (q * b > a);\n"
-    "  q += ((q + 1) * b <= a);\n"
-    "  return q;\n"
-    "}\n\n";
-
 // K1, gather form with direct stores: thread = one (tile, channel); the
 // alpha x alpha window is gathered from global memory (zero padding fused,
 // unpredicated interior path) and the P values are stored straight from
@@ -313,7 +314,6 @@ static const char* kIdivSmall =
 static void emit_input_gather(std::ostringstream& os, int r, int m, const MatProg& BT, const GenTypes& ty, int bn,
                               int TB, int& ctr) {
     const int n = r + m - 1, P = n * n;
-    os << kIdivSmall;
     os << "static __device__ __forceinline__ void input_gather_body(const in_t* __restrict__ x, uv_t* __restrict__ V,\n"
           "    int C, int H, int W, int pad, int th, int tw, long long T, long long Tp, long long Cp,\n"
           "    float rtw, float rth, int t0, int c) {\n"
@@ -380,6 +380,67 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
        << "    filter_body(w, U, K, C, Kp, Cp, (blockIdx.y - n_tb) * " << TB << " + threadIdx.x, blockIdx.x);\n"
           "  }\n"
           "}\n\n";
+}
+
+// K4, gather form: thread = (tile t, output channel k).  Its P values
+// M[p][k][t] are read straight from global memory (a warp's load of one p is
+// 32 consecutive t: one coalesced 128-byte line), transformed in registers and
+// the m x m block is stored to NCHW y -- as 8/16-byte pairs when m and Wo are
+// even, so a warp's row store covers a contiguous stretch of the output row.
+// Grid (ceil(T / TB), K).
+static void emit_output_gather(std::ostringstream& os, int r, int m, const MatProg& AT, const GenTypes& ty, int TB,
+                               int& ctr, const char* mt = "uv_t") {
+    const int n = r + m - 1;
+    const char* PT = ty.y_double ? "double2" : "float2";
+    os << "extern \"C\" __global__ void __launch_bounds__(" << TB << ") wino_output_gather(\n"
+          "    const " << mt << "* __restrict__ Mm, y_t* __restrict__ y, int K, int Ho, int Wo, int th, int tw,\n"
+          "    long long T, long long Tp, long long Kp, float rtw, float rth) {\n"
+       << "  const int t0 = blockIdx.x * " << TB << ";\n"
+          "  const int t = t0 + threadIdx.x;\n"
+          "  if (t >= T) return;\n"
+          "  const int k = blockIdx.y;\n"
+          "  const long long plane = Kp * Tp;\n"
+          "  const " << mt << "* src = Mm + (long long)k * Tp + t;\n";
+    std::vector<std::vector<std::string>> mm(n, std::vector<std::string>(n));
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+            mm[a][b] = "m" + std::to_string(a) + "_" + std::to_string(b);
+            os << "  const ct_t " << mm[a][b] << " = (ct_t)__ldg(src + " << (a * n + b) << " * plane);\n";
+        }
+    os << "  const int g0 = t0 / tw, off0 = t0 - g0 * tw;\n"
+          "  const int img0 = g0 / th, ti0 = g0 - img0 * th;\n"
+          "  const int off = off0 + threadIdx.x;\n"
+          "  const int kk = idiv_small(off, tw, rtw), tj = off - kk * tw;\n"
+          "  const int di = idiv_small(ti0 + kk, th, rth);\n"
+          "  const int ti = ti0 + kk - di * th;\n";
+    Emitter em(os, ty.compute_double, ctr);
+    auto yv = em.apply2d(AT, mm);
+    auto val = [&](int a, int b) { return store_cvt(ty.compute_double, ty.y_double, yv[a][b]); };
+    os << "  const int y0 = ti * " << m << ", x0 = tj * " << m << ";\n"
+       << "  y_t* dst = y + (((long long)(img0 + di) * K + k) * Ho + y0) * Wo + x0;\n"
+       << "  if (y0 + " << m << " <= Ho && x0 + " << m << " <= Wo) {\n";
+    if (m % 2 == 0) {
+        os << "    if ((Wo & 1) == 0) {\n";
+        for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; b += 2)
+                os << "      *reinterpret_cast<" << PT << "*>(dst + " << a << " * Wo + " << b << ") = make_" << PT
+                   << "(" << val(a, b) << ", " << val(a, b + 1) << ");\n";
+        os << "    } else {\n";
+        for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; ++b) os << "      dst[" << a << " * Wo + " << b << "] = " << val(a, b) << ";\n";
+        os << "    }\n";
+    } else {
+        for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; ++b) os << "    dst[" << a << " * Wo + " << b << "] = " << val(a, b) << ";\n";
+    }
+    os << "  } else {\n";
+    for (int a = 0; a < m; ++a) {
+        os << "    if (y0 + " << a << " < Ho) {\n";
+        for (int b = 0; b < m; ++b)
+            os << "      if (x0 + " << b << " < Wo) dst[" << a << " * Wo + " << b << "] = " << val(a, b) << ";\n";
+        os << "    }\n";
+    }
+    os << "  }\n}\n\n";
 }
 
 std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
@@ -526,6 +587,7 @@ std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, 
         int tbf = 128;
         while (tbf > 32 && (long long)P * tbf * es4 > 64 * 1024) tbf /= 2;
         emit_output_flat(os, r, m, AT, ty, tbf, ctr);
+        emit_output_gather(os, r, m, AT, ty, 128, ctr);
     }
     return os.str();
 }
@@ -770,6 +832,7 @@ std::string gen_layer_source_tc(int r, int m, const MatProg& G, const MatProg& B
     while (TB > 32 && (long long)P * TB * 4 > 64 * 1024) TB /= 2;
     emit_output_kernel(os, r, m, AT, ty, TB, ctr, "float", 4);
     emit_output_flat(os, r, m, AT, ty, TB, ctr, "float", 4);
+    emit_output_gather(os, r, m, AT, ty, 128, ctr, "float");
     return os.str();
 }
 

@@ -305,6 +305,17 @@ int k1_cfast() {
     return v;
 }
 
+// K4 variant: "gather" (codegen.cpp emit_output_gather; default) or the
+// smem-staged kernels (wino_output_flat for m <= 2, banded wino_output_xform
+// otherwise; WINO_K4=staged)
+bool k4_gather() {
+    static const bool v = [] {
+        const char* e = std::getenv("WINO_K4");
+        return !(e && std::string(e) == "staged");
+    }();
+    return v;
+}
+
 bool k1_gather() {
     static const bool v = [] {
         const char* e = std::getenv("WINO_K1");
@@ -530,6 +541,12 @@ int wino_output_transform(wino_plan* plan, const wino_layer_shape* s, const void
     CUfunction f;
     int K = s->K, Ho = L.Ho, Wo = L.Wo, th = L.th, tw = L.tw;
     long long T = L.T, Tp = L.Tp, Kp = L.Kp;
+    if (k4_gather() && K <= 65535) {
+        if ((rc = plan->layer.function("wino_output_gather", &f))) return rc;
+        float rtw = 1.0f / tw, rth = 1.0f / th;
+        void* gargs[] = {(void*)&M, &y, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp, &rtw, &rth};
+        return wino::launch(f, dim3(cdiv(T, 128), (unsigned)K, 1), dim3(128), 0, stream, gargs, "output_transform");
+    }
     if (plan->m <= 2) {
         // small output blocks: one thread per (k, tile), M staged per 128 tiles,
         // per-thread m x m stores (rows of m <= 2 values)
