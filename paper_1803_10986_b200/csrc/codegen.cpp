@@ -828,6 +828,180 @@ std::string gen_layer_source_tc(int r, int m, const MatProg& G, const MatProg& B
           "    const int f = b - n_in;\n"
           "    filter_tc(w, U, K, C, Kp, Cp, (f % n_kb) * 64 + threadIdx.x, f / n_kb);\n"
           "  }\n}\n\n";
+    // gather forms (default): warp = 4 tiles (or filters) x 8 channels, lane
+    // (c & 7) of row t -> a warp's 16-bit store of one p fills 4 consecutive
+    // 16-byte rows of the canonical layout (64 contiguous bytes, whole
+    // sectors) straight from registers, no smem park.  Block = 32 rows x 8
+    // channels; grid (row chunks [input, then filter], Cp / 8).
+    {
+        os << "static __device__ __forceinline__ void filter_tcg(const in_t* __restrict__ w, unsigned short* __restrict__ U,\n"
+              "    int K, int C, long long Kp, long long Cp, int k, int c) {\n"
+              "  const long long plane = Cp * Kp;\n"
+              "  unsigned short* o = U + tc_off(k, c, Cp);\n"
+              "  if (k >= K || c >= C) {\n"
+              "#pragma unroll\n"
+           << "    for (int p = 0; p < " << P << "; ++p) o[p * plane] = 0;\n"
+              "    return;\n  }\n"
+           << "  const in_t* src = w + ((long long)k * C + c) * " << r * r << ";\n";
+        std::vector<std::vector<std::string>> h(r, std::vector<std::string>(r));
+        for (int a = 0; a < r; ++a)
+            for (int b = 0; b < r; ++b) {
+                h[a][b] = "h" + std::to_string(a) + "_" + std::to_string(b);
+                os << "  const ct_t " << h[a][b] << " = (ct_t)__ldg(src + " << a * r + b << ");\n";
+            }
+        Emitter em(os, ty.compute_double, ctr);
+        auto u = em.apply2d(G, h);
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) os << "  o[" << (i * n + j) << " * plane] = " << cv << u[i][j] << "));\n";
+        os << "}\n\n";
+    }
+    {
+        os << "static __device__ __forceinline__ void input_tcg(const in_t* __restrict__ x, unsigned short* __restrict__ V,\n"
+              "    int C, int H, int W, int pad, int th, int tw, long long T, long long Tp, long long Cp,\n"
+              "    float rtw, float rth, int t0, int c) {\n"
+              "  const long long plane = Cp * Tp;\n"
+              "  const int tl = ((threadIdx.x >> 5) << 2) + ((threadIdx.x >> 3) & 3);\n"
+              "  const int t = t0 + tl;\n"
+              "  unsigned short* o = V + tc_off(t, c, Cp);\n"
+              "  if (c >= C || t >= T) {\n"
+              "#pragma unroll\n"
+           << "    for (int p = 0; p < " << P << "; ++p) o[p * plane] = 0;\n"
+              "    return;\n"
+              "  }\n"
+              "  const int g0 = t0 / tw, off0 = t0 - g0 * tw;\n"
+              "  const int img0 = g0 / th, ti0 = g0 - img0 * th;\n"
+              "  const int off = off0 + tl;\n"
+              "  const int kk = idiv_small(off, tw, rtw), tj = off - kk * tw;\n"
+              "  const int di = idiv_small(ti0 + kk, th, rth);\n"
+              "  const int ti = ti0 + kk - di * th;\n"
+           << "  const int h0 = ti * " << m << " - pad, w0 = tj * " << m << " - pad;\n"
+           << "  const in_t* src = x + ((long long)(img0 + di) * C + c) * ((long long)H * W);\n";
+        std::vector<std::vector<std::string>> d(n, std::vector<std::string>(n));
+        for (int a = 0; a < n; ++a)
+            for (int b = 0; b < n; ++b) {
+                d[a][b] = "x" + std::to_string(a) + "_" + std::to_string(b);
+                os << "  ct_t " << d[a][b] << ";\n";
+            }
+        os << "  if (h0 >= 0 && w0 >= 0 && h0 + " << n << " <= H && w0 + " << n << " <= W) {\n"
+           << "    const in_t* rp = src + h0 * W + w0;\n";
+        for (int a = 0; a < n; ++a)
+            for (int b = 0; b < n; ++b)
+                os << "    " << d[a][b] << " = (ct_t)__ldg(rp + " << a << " * W + " << b << ");\n";
+        os << "  } else {\n";
+        for (int a = 0; a < n; ++a)
+            os << "    const bool r" << a << " = (unsigned)(h0 + " << a << ") < (unsigned)H;\n";
+        for (int b = 0; b < n; ++b)
+            os << "    const bool c" << b << " = (unsigned)(w0 + " << b << ") < (unsigned)W;\n";
+        for (int a = 0; a < n; ++a)
+            for (int b = 0; b < n; ++b)
+                os << "    " << d[a][b] << " = (r" << a << " && c" << b << ") ? (ct_t)__ldg(src + (h0 + " << a
+                   << ") * W + (w0 + " << b << ")) : (ct_t)0;\n";
+        os << "  }\n";
+        Emitter em(os, ty.compute_double, ctr);
+        auto v = em.apply2d(BT, d);
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) os << "  o[" << (i * n + j) << " * plane] = " << cv << v[i][j] << "));\n";
+        os << "}\n\n";
+    }
+    // P <= 16: thread = one tile x 8 channels, the 8 transformed values of
+    // each p packed in registers and written as one 16-byte row of the
+    // canonical layout (a warp of 32 consecutive tiles stores 512 contiguous
+    // bytes); the window loads keep the one-channel-per-warp coalescing of
+    // the fp32 gather kernel.  Block = 128 tiles; grid (row chunks, Cp / 8).
+    if (P <= 16) {
+        os << "static __device__ __forceinline__ void input_tcg8(const in_t* __restrict__ x, unsigned short* __restrict__ V,\n"
+              "    int C, int H, int W, int pad, int th, int tw, long long T, long long Tp, long long Cp,\n"
+              "    float rtw, float rth, int t0, int c0) {\n"
+              "  const long long plane = Cp * Tp;\n"
+              "  const int t = t0 + threadIdx.x;\n"
+              "  uint4* o = reinterpret_cast<uint4*>(V + tc_off(t, c0, Cp));\n"
+           << "  unsigned pk[" << P << "][4];\n"
+           << "  if (t >= T) {\n"
+              "#pragma unroll\n"
+           << "    for (int p = 0; p < " << P << "; ++p) o[p * (plane >> 3)] = make_uint4(0u, 0u, 0u, 0u);\n"
+              "    return;\n"
+              "  }\n"
+              "  const int g0 = t0 / tw, off0 = t0 - g0 * tw;\n"
+              "  const int img0 = g0 / th, ti0 = g0 - img0 * th;\n"
+              "  const int off = off0 + threadIdx.x;\n"
+              "  const int kk = idiv_small(off, tw, rtw), tj = off - kk * tw;\n"
+              "  const int di = idiv_small(ti0 + kk, th, rth);\n"
+              "  const int ti = ti0 + kk - di * th;\n"
+           << "  const int h0 = ti * " << m << " - pad, w0 = tj * " << m << " - pad;\n"
+           << "  const bool inner = h0 >= 0 && w0 >= 0 && h0 + " << n << " <= H && w0 + " << n << " <= W;\n"
+           << "  const in_t* base = x + ((long long)(img0 + di) * C + c0) * ((long long)H * W);\n"
+              "#pragma unroll\n"
+              "  for (int cc = 0; cc < 8; ++cc) {\n"
+              "    const in_t* src = base + (long long)cc * H * W;\n"
+              "    const bool live = c0 + cc < C;\n";
+        std::vector<std::vector<std::string>> d(n, std::vector<std::string>(n));
+        for (int a = 0; a < n; ++a)
+            for (int b = 0; b < n; ++b) {
+                d[a][b] = "x" + std::to_string(a) + "_" + std::to_string(b);
+                os << "    ct_t " << d[a][b] << ";\n";
+            }
+        os << "    if (live && inner) {\n      const in_t* rp = src + h0 * W + w0;\n";
+        for (int a = 0; a < n; ++a)
+            for (int b = 0; b < n; ++b)
+                os << "      " << d[a][b] << " = (ct_t)__ldg(rp + " << a << " * W + " << b << ");\n";
+        os << "    } else {\n";
+        for (int a = 0; a < n; ++a)
+            os << "      const bool r" << a << " = live && (unsigned)(h0 + " << a << ") < (unsigned)H;\n";
+        for (int b = 0; b < n; ++b)
+            os << "      const bool c" << b << " = (unsigned)(w0 + " << b << ") < (unsigned)W;\n";
+        for (int a = 0; a < n; ++a)
+            for (int b = 0; b < n; ++b)
+                os << "      " << d[a][b] << " = (r" << a << " && c" << b << ") ? (ct_t)__ldg(src + (h0 + " << a
+                   << ") * W + (w0 + " << b << ")) : (ct_t)0;\n";
+        os << "    }\n";
+        Emitter em(os, ty.compute_double, ctr);
+        auto v = em.apply2d(BT, d);
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) {
+                const int p = i * n + j;
+                os << "    {\n      const unsigned hv = live ? (unsigned)" << cv << v[i][j] << ")) : 0u;\n"
+                   << "      if (cc & 1) pk[" << p << "][cc >> 1] |= hv << 16; else pk[" << p << "][cc >> 1] = hv;\n"
+                   << "    }\n";
+            }
+        os << "  }\n"
+              "#pragma unroll\n"
+           << "  for (int p = 0; p < " << P << "; ++p) o[p * (plane >> 3)] = make_uint4(pk[p][0], pk[p][1], pk[p][2], pk[p][3]);\n"
+              "}\n\n";
+        os << "extern \"C\" __global__ void __launch_bounds__(128) wino_input_tcg8(\n"
+              "    const in_t* __restrict__ x, unsigned short* __restrict__ V, int C, int H, int W, int pad, int th,\n"
+              "    int tw, long long T, long long Tp, long long Cp, float rtw, float rth) {\n"
+              "  input_tcg8(x, V, C, H, W, pad, th, tw, T, Tp, Cp, rtw, rth, blockIdx.x * 128, blockIdx.y * 8);\n"
+              "}\n\n"
+              "extern \"C\" __global__ void __launch_bounds__(128) wino_transforms_tcg8(\n"
+              "    const in_t* __restrict__ x, unsigned short* __restrict__ V, int C, int H, int W, int pad, int th,\n"
+              "    int tw, long long T, long long Tp, long long Cp, int n_tb,\n"
+              "    const in_t* __restrict__ w, unsigned short* __restrict__ U, int K, long long Kp, float rtw, float rth) {\n"
+              "  if ((int)blockIdx.x < n_tb) {\n"
+              "    input_tcg8(x, V, C, H, W, pad, th, tw, T, Tp, Cp, rtw, rth, blockIdx.x * 128, blockIdx.y * 8);\n"
+              "  } else {\n"
+              "    // filters: 4 per warp x 8 channels, as in wino_transforms_tcg (128 threads = 16 filters)\n"
+              "    const int k = ((int)blockIdx.x - n_tb) * 16 + ((threadIdx.x >> 5) << 2) + ((threadIdx.x >> 3) & 3);\n"
+              "    if (k < Kp) filter_tcg(w, U, K, C, Kp, Cp, k, blockIdx.y * 8 + (threadIdx.x & 7));\n"
+              "  }\n"
+              "}\n\n";
+    }
+    os << "extern \"C\" __global__ void __launch_bounds__(256) wino_input_tcg(\n"
+          "    const in_t* __restrict__ x, unsigned short* __restrict__ V, int C, int H, int W, int pad, int th,\n"
+          "    int tw, long long T, long long Tp, long long Cp, float rtw, float rth) {\n"
+          "  input_tcg(x, V, C, H, W, pad, th, tw, T, Tp, Cp, rtw, rth, blockIdx.x * 32, blockIdx.y * 8 + (threadIdx.x & 7));\n"
+          "}\n\n"
+          "extern \"C\" __global__ void __launch_bounds__(256) wino_transforms_tcg(\n"
+          "    const in_t* __restrict__ x, unsigned short* __restrict__ V, int C, int H, int W, int pad, int th,\n"
+          "    int tw, long long T, long long Tp, long long Cp, int n_tb,\n"
+          "    const in_t* __restrict__ w, unsigned short* __restrict__ U, int K, long long Kp, float rtw, float rth) {\n"
+          "  const int c = blockIdx.y * 8 + (threadIdx.x & 7);\n"
+          "  if ((int)blockIdx.x < n_tb) {\n"
+          "    input_tcg(x, V, C, H, W, pad, th, tw, T, Tp, Cp, rtw, rth, blockIdx.x * 32, c);\n"
+          "  } else {\n"
+          "    const int k = ((int)blockIdx.x - n_tb) * 32 + ((threadIdx.x >> 5) << 2) + ((threadIdx.x >> 3) & 3);\n"
+          "    if (k < Kp) filter_tcg(w, U, K, C, Kp, Cp, k, c);\n"
+          "  }\n"
+          "}\n\n";
     int TB = 128;
     while (TB > 32 && (long long)P * TB * 4 > 64 * 1024) TB /= 2;
     emit_output_kernel(os, r, m, AT, ty, TB, ctr, "float", 4);

@@ -316,6 +316,14 @@ bool k4_gather() {
     return v;
 }
 
+bool k1_no8() {  // WINO_K1TC=4x8: use the 4-tiles x 8-channels TC kernel also for P <= 16
+    static const bool v = [] {
+        const char* e = std::getenv("WINO_K1TC");
+        return e && std::string(e) == "4x8";
+    }();
+    return v;
+}
+
 bool k1_gather() {
     static const bool v = [] {
         const char* e = std::getenv("WINO_K1");
@@ -458,6 +466,26 @@ int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, c
     const long long blocks = (long long)n_tb * (tc ? Cp / 8 : Cp) + (long long)n_kb * Cp;
     if (blocks >= (1LL << 31)) return wino::fail(WINO_EUNSUPPORTED, "transforms: grid too large");
     int cfast = k1_cfast(), Wl = 0;
+    if (tc && k1_gather() && Cp / 8 <= 65535 && L.P <= 16 && !k1_no8()) {
+        CUfunction fg;
+        if ((rc = plan->layer.function("wino_transforms_tcg8", &fg))) return rc;
+        float rtw = 1.0f / tw, rth = 1.0f / th;
+        int nt128 = (int)cdiv(Tp, 128), nk16 = (int)cdiv(Kp, 16);
+        void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &nt128, (void*)&w, &U, &K, &Kp,
+                        &rtw, &rth};
+        return wino::launch(fg, dim3((unsigned)(nt128 + nk16), (unsigned)(Cp / 8)), dim3(128), 0, stream, args,
+                            "transforms");
+    }
+    if (tc && k1_gather() && Cp / 8 <= 65535) {
+        CUfunction fg;
+        if ((rc = plan->layer.function("wino_transforms_tcg", &fg))) return rc;
+        float rtw = 1.0f / tw, rth = 1.0f / th;
+        int nt32 = (int)cdiv(Tp, 32), nk32 = (int)cdiv(Kp, 32);
+        void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &nt32, (void*)&w, &U, &K, &Kp,
+                        &rtw, &rth};
+        return wino::launch(fg, dim3((unsigned)(nt32 + nk32), (unsigned)(Cp / 8)), dim3(256), 0, stream, args,
+                            "transforms");
+    }
     if (!tc && k1_gather() && (long long)n_tb + n_kb <= 65535 && Cp <= 65535) {
         CUfunction fg;
         if ((rc = plan->layer.function("wino_transforms_gather", &fg))) return rc;
@@ -488,6 +516,20 @@ int wino_input_transform(wino_plan* plan, const wino_layer_shape* s, const void*
             void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &Wl, &rtw, &rth};
             return wino::launch(f, dim3((unsigned)Cp, (unsigned)n_tb), dim3(tb), 0, stream, args, "input_transform");
         }
+    }
+    if (plan->mode >= WINO_CONTRACT_TC_BF16 && k1_gather() && Cp / 8 <= 65535 && L.P <= 16 && !k1_no8()) {
+        if ((rc = plan->layer.function("wino_input_tcg8", &f))) return rc;
+        float rtw = 1.0f / tw, rth = 1.0f / th;
+        void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &rtw, &rth};
+        return wino::launch(f, dim3((unsigned)cdiv(Tp, 128), (unsigned)(Cp / 8)), dim3(128), 0, stream, args,
+                            "input_transform");
+    }
+    if (plan->mode >= WINO_CONTRACT_TC_BF16 && k1_gather() && Cp / 8 <= 65535) {
+        if ((rc = plan->layer.function("wino_input_tcg", &f))) return rc;
+        float rtw = 1.0f / tw, rth = 1.0f / th;
+        void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &rtw, &rth};
+        return wino::launch(f, dim3((unsigned)cdiv(Tp, 32), (unsigned)(Cp / 8)), dim3(256), 0, stream, args,
+                            "input_transform");
     }
     if ((rc = plan->layer.function("wino_input_xform", &f))) return rc;
     void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp};

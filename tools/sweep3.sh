@@ -1,8 +1,6 @@
-timeout 900 python -m pytest tests/test_gpu_layer.py tests/test_gpu_stack.py tests/test_gpu_tc.py -x -q > gpurun_out/pt.log 2>&1; tail -2 gpurun_out/pt.log
-for k in gather staged; do
-  for cm in exact tc_bf16; do
-  for sh in "32,128,28,128 --m 2" "64,256,28,256 --m 6" "8,64,56,64 --m 4" "32,512,14,512 --m 4" "8,64,224,64 --m 6"; do
-    WINO_K4=$k python tools/xform_bench.py --contraction $cm --shape $sh | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$k $cm', d['shape'], d['m'], 'out %.1f (%.0f GB/s)' % (d['real_output_us'], d['real_output_gbs']))"
-  done
+timeout 900 python -m pytest tests/test_gpu_tc.py -x -q > gpurun_out/pt.log 2>&1; tail -2 gpurun_out/pt.log
+for k in 8 4x8; do
+  for sh in "32,128,28,128 --m 2" "8,224,112,224 --m 2" "64,3,224,64 --m 2"; do
+    WINO_K1TC=$k python tools/xform_bench.py --contraction tc_bf16 --shape $sh | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$k', d['shape'], d['m'], 'tr %.1f in %.1f (%.0f GB/s) triv-tr %.1f' % (d['real_transforms_us'], d['real_input_us'], d['real_input_gbs'], d['trivial_transforms_us']))"
   done
 done
