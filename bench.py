@@ -178,7 +178,8 @@ def config_dict(args, cfg, world=1):
     return {"workload": args.config, "winograd": f"F({m}x{m},{r}x{r})", "points": pts, "N_per_gpu": N,
             "global_batch": N * world, "C": C, "K": K, "H": H, "W": H, "pad": pad, "precision": prec,
             "dot_order": order, "channel_sum": cs, "contraction": args.contraction,
-            "x_dist": xd, "w_init": wi, "l2": "flushed between timed steps (256 MiB write)",
+            "x_dist": xd, "w_init": wi, "l2": "flushed between timed steps: 256 MiB write, then 256 MiB read of a clean buffer "
+                  "(no step data and no dirty lines left in L2)",
             "parallelism": f"dp{world} (independent batches per GPU)"}
 
 
@@ -209,8 +210,17 @@ def run_gpu(args, cfg):
     uvdt = torch.float64 if prec == "fp64" else torch.float32
     U = torch.empty((L.P, L.Cp, L.Kp), dtype=uvdt, device="cuda")
     V = torch.empty((L.P, L.Cp, L.Tp), dtype=uvdt, device="cuda")
-    M = torch.empty((L.P, L.Kp, L.Tp), dtype=uvdt, device="cuda")
+    fused = args.contraction.startswith("tcf_")  # K3t + K4 in one kernel (wino_tcf), no M
+    M = torch.empty((1,) if fused else (L.P, L.Kp, L.Tp), dtype=uvdt, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    clean = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
+
+    def flush_l2():
+        # evict L2: write 256 MiB, then read a clean 256 MiB buffer so the write-back
+        # of those dirty lines happens here, not inside the next timed step
+        flush.zero_()
+        clean.sum()
+
     lib = _native.lib()
     shp = op.shape
     import ctypes
@@ -228,6 +238,13 @@ def run_gpu(args, cfg):
         if ev is not None:
             ev[1].record(stream)
             ev[2].record(stream)
+        if fused:
+            _native.check(lib.wino_contract_output(op.plan.handle, sref, _native.as_ptr(U), _native.as_ptr(V),
+                                                   _native.as_ptr(y), sh))
+            if ev is not None:
+                ev[3].record(stream)
+                ev[4].record(stream)
+            return
         _native.check(lib.wino_contract(op.plan.handle, sref, _native.as_ptr(U), _native.as_ptr(V),
                                         _native.as_ptr(M), sh))
         if ev is not None:
@@ -270,17 +287,17 @@ def run_gpu(args, cfg):
         torch.cuda.synchronize()
         n0 = _native.launch_count()
         for i in range(args.steps):
-            flush.zero_()  # evict L2 (outside the timed interval of the step)
+            flush_l2()  # evict L2 (outside the timed interval of the step)
             e_start[i].record(stream)
             graph.replay()
             e_end[i].record(stream)
         # instrumented steps: the same four kernels launched eagerly with an
         # event between stages -> per-kernel durations for the roofline
         for i in range(args.steps):
-            flush.zero_()
+            flush_l2()
             step(evs[i])
         torch.cuda.synchronize()
-        n_launch = 3 * args.steps + (_native.launch_count() - n0)
+        n_launch = (2 if fused else 3) * args.steps + (_native.launch_count() - n0)
     if world > 1:
         dist.barrier()
     stage = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(4)] for i in range(args.steps)])
@@ -297,7 +314,8 @@ def run_gpu(args, cfg):
     xh = torch.from_numpy(x_np).pin_memory()
     wh = torch.from_numpy(w_np).pin_memory()
     yh = torch.empty(op.out_shape, dtype=y.dtype).pin_memory()
-    pipe = W.HostPipeline(ts, wcfg, N, C, H, H, K, pad, chunks=args.e2e_chunks, contraction=args.contraction)
+    chunks = [int(v) for v in args.e2e_chunks.split(",")] if "," in args.e2e_chunks else int(args.e2e_chunks)
+    pipe = W.HostPipeline(ts, wcfg, N, C, H, H, K, pad, chunks=chunks, contraction=args.contraction)
 
     for _ in range(3):
         pipe(xh, wh, yh)
@@ -305,7 +323,7 @@ def run_gpu(args, cfg):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_ms = []
     for _ in range(args.steps):
-        flush.zero_()
+        flush_l2()
         e0.record(stream)
         pipe(xh, wh, yh)
         e1.record(stream)
@@ -339,7 +357,16 @@ def run_gpu(args, cfg):
     exact = args.contraction == "exact"
     mp = measured_peaks()
     hbm = mp["hbm_gbs"]
-    if args.contraction.startswith("tc_"):
+    if fused:
+        # wino_tcf: V and U read once (16-bit), y written once; tensor work is ~2 us of it
+        fb = 2 * L.P * L.T * C + 2 * L.P * C * K + (4 if prec == "fp32" else 8) * N * K * L.Ho * L.Wo
+        gbs = fb / (ms_stage[2] * 1e-3) / 1e9
+        roof = {"kernel": "wino_tcf (tcgen05 contraction + output transform, one kernel)", "bound": "hbm",
+                "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                "traffic": traffic_of("wino_tcf", args.config, args.contraction),
+                "peak_source": mp["source"] + " hbm copy bandwidth", "bytes_per_launch": fb,
+                "tensor_tflops": ach, "tensor_frac": ach / mp["bf16_tflops"]}
+    elif args.contraction.startswith("tc_"):
         pk = mp["bf16_tflops"]
         roof = {"kernel": "tc_contract_kernel (tcgen05.mma kind::f16)", "bound": "tensor", "achieved": ach,
                 "peak": pk, "unit": "TFLOP/s", "frac": ach / pk, "traffic": None,
@@ -351,7 +378,9 @@ def run_gpu(args, cfg):
                 "peak_source": "measured in this run: libwino wino_peak_probe FFMA (8 chains x 148*8 CTAs); "
                                "MEASURED_PEAKS.json has no FP32 figure",
                 "exact_ceiling_tflops": peak["fmul_fadd_tflops"] if exact else None,
-                "frac_of_exact_ceiling": ach / peak["fmul_fadd_tflops"] if exact else None}
+                "frac_of_exact_ceiling": ach / peak["fmul_fadd_tflops"] if exact else None,
+                "exact_ceiling_reg_tflops": peak["fmul_fadd_reg_tflops"] if exact else None,
+                "frac_of_exact_ceiling_reg": ach / peak["fmul_fadd_reg_tflops"] if exact else None}
     roof.update({"flops_per_launch": flops_c, "share_of_step": float(ms_stage[2] / ms_stage.sum())})
     eb = L.elem_bytes_uv
     stage_bytes = [4 * K * C * r * r + eb * L.P * C * K + 4 * N * C * H * H + eb * L.P * L.T * C,
@@ -359,8 +388,11 @@ def run_gpu(args, cfg):
                    None,
                    eb * L.P * L.T * K + (4 if prec == "fp32" else 8) * N * K * L.Ho * L.Wo]
     stages = {}
-    for j, name in enumerate(["transforms (K1 input + K2 filter, one launch)", None, "contract",
-                              "output_transform"]):
+    if fused:
+        stage_bytes[2] = roof["bytes_per_launch"]
+    for j, name in enumerate(["transforms (K1 input + K2 filter, one launch)", None,
+                              "contract + output transform (wino_tcf)" if fused else "contract",
+                              None if fused else "output_transform"]):
         if name is None:
             continue
         d = {"ms": float(ms_stage[j])}
@@ -380,7 +412,8 @@ def run_gpu(args, cfg):
                 "error_vs_fp64": err,
                 "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": x_np.nbytes + w_np.nbytes,
                         "d2h_bytes_per_step": yh.numel() * yh.element_size(), "ms_per_step": e2e_t,
-                        "api": f"HostPipeline({args.e2e_chunks} chunks: H2D | K1-K3-K4 | D2H overlapped)",
+                        "api": f"HostPipeline(chunks={args.e2e_chunks}: H2D | K1-K3-K4 | D2H overlapped on "
+                               "3 streams, captured once into a CUDA graph and replayed)",
                         "bitwise_equal_to_device_path": e2e_same},
                 "timing": "value/ms_per_step: CUDA-graph replay of the 4-kernel step, events around each "
                           "step, L2 flushed between steps; stages: eager launches with an event between stages",
@@ -546,7 +579,9 @@ def vgg_roof(args, ach, peak, share):
     return {"kernel": "wino_contract (13 layers)", "bound": "fp32", "achieved": ach, "peak": peak["ffma_tflops"],
             "unit": "TFLOP/s", "frac": ach / peak["ffma_tflops"], "traffic": None,
             "exact_ceiling_tflops": peak["fmul_fadd_tflops"],
-            "frac_of_exact_ceiling": ach / peak["fmul_fadd_tflops"], "share_of_step": share}
+            "frac_of_exact_ceiling": ach / peak["fmul_fadd_tflops"],
+            "exact_ceiling_reg_tflops": peak["fmul_fadd_reg_tflops"],
+            "frac_of_exact_ceiling_reg": ach / peak["fmul_fadd_reg_tflops"], "share_of_step": share}
 
 
 def measure_peaks(lib, _native, torch):
@@ -555,8 +590,9 @@ def measure_peaks(lib, _native, torch):
     sm = torch.cuda.get_device_properties(0).multi_processor_count
     blocks, iters = sm * 8, 4096
     res = {}
-    for mode, name in ((0, "ffma_tflops"), (1, "fmul_fadd_tflops"), (2, "dfma_tflops"), (3, "dmul_dadd_tflops")):
-        it = iters if mode < 2 else iters // 8
+    for mode, name in ((0, "ffma_tflops"), (1, "fmul_fadd_tflops"), (2, "dfma_tflops"), (3, "dmul_dadd_tflops"),
+                       (4, "fmul_fadd_reg_tflops")):
+        it = iters if mode in (0, 1, 4) else iters // 8
         for _ in range(2):
             _native.check(lib.wino_peak_probe(mode, blocks, it, ctypes.c_void_p(out.data_ptr()),
                                               torch.cuda.current_stream().cuda_stream))
@@ -582,11 +618,11 @@ def main():
     ap.add_argument("--vgg-batch", type=int, default=256)
     ap.add_argument("--err-images", type=int, default=8)
     ap.add_argument("--no-err", action="store_true")
-    ap.add_argument("--contraction", default="exact", choices=["exact", "ffma", "tc_bf16", "tc_fp16"])
+    ap.add_argument("--contraction", default="exact", choices=["exact", "ffma", "tc_bf16", "tc_fp16", "tcf_bf16", "tcf_fp16"])
     ap.add_argument("--cpu-images", type=int, default=32)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--soak", type=float, default=1.5, help="seconds of untimed load before the timed region")
-    ap.add_argument("--e2e-chunks", type=int, default=4)
+    ap.add_argument("--e2e-chunks", default="4", help="image chunks of the e2e pipeline: a count or sizes a,b,...")
     ap.add_argument("--ncu", action="store_true", help="profiling mode: warm-up + K eager steps only, no output")
     args = ap.parse_args()
     if args.config == "vgg16":

@@ -53,6 +53,12 @@ extern "C" {
  * precision must be fp32 or mixed. */
 #define WINO_CONTRACT_TC_BF16 2
 #define WINO_CONTRACT_TC_FP16 3
+/* fused tensor-core modes: the same BF16 / FP16 products, but the contraction
+ * and the output transform run as one kernel (wino_contract_output): all
+ * alpha^2 accumulators of a (128 tiles x NK filters) block sit in TMEM and the
+ * epilogue writes y directly -- M never exists.  Needs alpha^2 <= 32. */
+#define WINO_CONTRACT_TCF_BF16 4
+#define WINO_CONTRACT_TCF_FP16 5
 
 /* One postfix op of a row program (reference engine.py:153-208 compiled
  * programs, flattened): LEAF pushes coeff * in[col] (one rounded product;
@@ -139,6 +145,10 @@ int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, con
 /* K4: y = A^T M A per (k, tile), crop + NCHW write-back -- engine.py:418-423 */
 int wino_output_transform(wino_plan* plan, const wino_layer_shape* s, const void* M,
                           void* y, void* stream);
+/* K3 + K4 fused (TCF modes only): y = A^T (sum_c U_p[c] V_p[c]) A straight
+ * from the tensor-memory accumulators -- engine.py:415-423 */
+int wino_contract_output(wino_plan* plan, const wino_layer_shape* s, const void* U, const void* V,
+                         void* y, void* stream);
 /* K2 -> K1 -> K3 -> K4 with a caller-provided workspace of
  * layout.workspace_bytes bytes (256-byte aligned). */
 int wino_conv2d(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w,
@@ -202,7 +212,9 @@ int wino_mean_f64(int64_t n, const double* v, double* out, void* stream);
 
 /* Arithmetic-throughput probe for roofline denominators: `blocks` x 256
  * threads, each running 8 independent chains of `iters` steps of
- * mode 0 FFMA | 1 FMUL+FADD | 2 DFMA | 3 DMUL+DADD (flops = 2 per step). */
+ * mode 0 FFMA | 1 FMUL+FADD | 2 DFMA | 3 DMUL+DADD (immediate multiplier
+ * and addend) | 4 FMUL+FADD with register operands (read from out[2], out[3];
+ * the operand form of the exact contraction); flops = 2 per step. */
 int wino_peak_probe(int mode, int blocks, int iters, float* out, void* stream);
 
 /* number of kernels this library has launched in the calling process */

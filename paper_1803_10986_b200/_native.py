@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwino.so"
 WINO_OK, WINO_EINVAL, WINO_EUNSUPPORTED, WINO_ECUDA, WINO_ECOMPILE = 0, -1, -2, -3, -4
 PRECISION_CODE = {"fp32": 0, "fp64": 1, "mixed": 2}
 SUM_CODE = {"linear": 0, "pairwise": 1}
-CONTRACT_CODE = {"exact": 0, "ffma": 1, "tc_bf16": 2, "tc_fp16": 3}
+CONTRACT_CODE = {"exact": 0, "ffma": 1, "tc_bf16": 2, "tc_fp16": 3, "tcf_bf16": 4, "tcf_fp16": 5}
 
 
 class WinoOp(ctypes.Structure):
@@ -56,6 +56,7 @@ SIGNATURES = [
     ("wino_transforms", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("wino_contract", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_void_p]),
     ("wino_output_transform", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p]),
+    ("wino_contract_output", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_void_p]),
     ("wino_conv2d", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                             c_void_p]),
     ("wino_tile_hadamard2d", c_int, [c_void_p, c_int64, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),

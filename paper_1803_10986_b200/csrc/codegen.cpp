@@ -1,6 +1,7 @@
 // Straight-line CUDA generation for the transform stages (see codegen.h).
 #include "codegen.h"
 
+#include <algorithm>
 #include <cstdio>
 #include <map>
 #include <sstream>
@@ -706,8 +707,211 @@ std::string gen_tile_source(int r, int m, const MatProg& G, const MatProg& BT, c
 // (one stage of one tile = 8 KB contiguous = one bulk copy).  The transforms
 // themselves are the same straight-line FP32/FP64 code; only the final store
 // rounds to 16 bits (FP32 first in mixed mode).
+// Fused K3t + K4 for the tensor-core modes (P * NK <= 512): one persistent CTA
+// per SM walks (128-tile, NK-filter) blocks.  All P Winograd-point GEMMs of a
+// block accumulate side by side in TMEM (point p in columns [p NK, p NK + NK),
+// rows = tiles), so the epilogue holds every point of a (tile, filter) pair
+// and applies the output transform right out of TMEM: M never reaches HBM.
+//   warp 0      producer: one cp.async.bulk for the V stage (P x 128 x 16,
+//               contiguous) and one for the U stage (P x NK x 16) per
+//               16-channel step, ST-deep smem ring (mbarrier complete_tx)
+//   warp 1      one thread issues P tcgen05.mma (M=128, N=NK, K=16) per
+//               stage; tcgen05.commit frees the stage / publishes the block
+//   warps 2-5   epilogue: tcgen05.ld (32 lanes = 32 tiles per warp) of every
+//               point for KC filters, (A^T M) A in registers, crop, NCHW store
+static void emit_tcf_kernel(std::ostringstream& os, int r, int m, const MatProg& AT, const GenTypes& ty, bool fp16,
+                            int NK, int& ctr) {
+    const int n = r + m - 1, P = n * n;
+    const int VST = P * 4096, UST = P * NK * 32, STB = VST + UST;
+    const int ST = std::max(1, std::min(4, (232448 - 256) / STB));
+    const int KC = P <= 16 ? 8 : 4;  // filters per tcgen05.ld batch (P x KC registers)
+    const int NB = 2 * P * NK <= 512 ? 2 : 1;  // TMEM accumulator sets (2: epilogue overlaps the next block)
+    const char* PT = ty.y_double ? "double2" : "float2";
+    os << "typedef unsigned long long tcf_u64;\n"
+          "static __device__ __forceinline__ unsigned tcf_s(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }\n"
+          "static __device__ __forceinline__ void tcf_wait(tcf_u64* b, unsigned parity) {\n"
+          "  asm volatile(\"{\\n\\t.reg .pred P1;\\nTCF_WAIT_%=:\\n\\t\"\n"
+          "               \"mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\\n\\t\"\n"
+          "               \"@!P1 bra TCF_WAIT_%=;\\n}\\n\" :: \"r\"(tcf_s(b)), \"r\"(parity) : \"memory\");\n"
+          "}\n"
+          "static __device__ __forceinline__ tcf_u64 tcf_desc(unsigned addr, unsigned lbo, unsigned sbo) {\n"
+          "  return (tcf_u64)((addr >> 4) & 0x3FFF) | ((tcf_u64)((lbo >> 4) & 0x3FFF) << 16) |\n"
+          "         ((tcf_u64)((sbo >> 4) & 0x3FFF) << 32) | ((tcf_u64)1 << 46);\n"
+          "}\n\n";
+    os << "extern \"C\" __global__ void __launch_bounds__(192, 1) wino_tcf(\n"
+          "    const unsigned short* __restrict__ U, const unsigned short* __restrict__ V, y_t* __restrict__ y,\n"
+          "    int K, int Ho, int Wo, int th, int tw, long long T, long long Tp, long long Kp, long long Cp,\n"
+          "    int n_tiles, float rtw, float rth, int dbg) {\n"
+       << "  constexpr int P = " << P << ", NK = " << NK << ", ST = " << ST << ", KC = " << KC << ", NB = " << NB
+       << ";\n"
+       << "  constexpr unsigned VST = " << VST << "u, UST = " << UST << "u, STB = " << STB << "u;\n"
+       << "  extern __shared__ __align__(1024) unsigned char smem[];\n"
+          "  tcf_u64* full = reinterpret_cast<tcf_u64*>(smem + ST * STB);\n"
+          "  tcf_u64* empty = full + ST;\n"
+          "  tcf_u64* acc_full = empty + ST;\n"
+          "  tcf_u64* acc_empty = acc_full + NB;\n"
+          "  unsigned* tmem_slot = reinterpret_cast<unsigned*>(acc_empty + NB);\n"
+          "  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;\n"
+          "  const int nk = (int)(Cp >> 4), n_kb = (int)(Kp / NK);\n"
+          "  if (tid == 0) {\n"
+          "    for (int s = 0; s < ST; ++s) {\n"
+          "      asm volatile(\"mbarrier.init.shared::cta.b64 [%0], 1;\" :: \"r\"(tcf_s(&full[s])) : \"memory\");\n"
+          "      asm volatile(\"mbarrier.init.shared::cta.b64 [%0], 1;\" :: \"r\"(tcf_s(&empty[s])) : \"memory\");\n"
+          "    }\n"
+          "    for (int b = 0; b < NB; ++b) {\n"
+          "      asm volatile(\"mbarrier.init.shared::cta.b64 [%0], 1;\" :: \"r\"(tcf_s(&acc_full[b])) : \"memory\");\n"
+          "      asm volatile(\"mbarrier.init.shared::cta.b64 [%0], 4;\" :: \"r\"(tcf_s(&acc_empty[b])) : \"memory\");\n"
+          "    }\n"
+          "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n"
+          "  }\n"
+          "  if (warp == 1) {  // all 512 TMEM columns: P x NK fp32 accumulators x 128 lanes\n"
+          "    asm volatile(\"tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\" :: \"r\"(tcf_s(tmem_slot)) : \"memory\");\n"
+          "    asm volatile(\"tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\" ::: \"memory\");\n"
+          "  }\n"
+          "  asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n"
+          "  __syncthreads();\n"
+          "  asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n"
+          "  const unsigned tmem = *tmem_slot;\n"
+          "  if (warp == 0) {\n"
+          "    if (lane == 0) {  // producer\n"
+          "      int g = 0;\n"
+          "      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {\n"
+          "        const int kb = tile % n_kb, tb = tile / n_kb;\n"
+          "        const unsigned short* gV = V + (long long)tb * nk * (VST / 2);\n"
+          "        const unsigned short* gU = U + (long long)kb * nk * (UST / 2);\n"
+          "        for (int kt = 0; kt < nk; ++kt, ++g) {\n"
+          "          const int s = g % ST;\n"
+          "          if (g >= ST) tcf_wait(&empty[s], (unsigned)(((g / ST) - 1) & 1));\n"
+          "          unsigned char* dst = smem + s * STB;\n"
+          "          asm volatile(\"mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\" :: \"r\"(tcf_s(&full[s])), \"r\"(STB) : \"memory\");\n"
+          "          asm volatile(\"cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\"\n"
+          "                       :: \"r\"(tcf_s(dst)), \"l\"(gV + (long long)kt * (VST / 2)), \"r\"(VST), \"r\"(tcf_s(&full[s])) : \"memory\");\n"
+          "          asm volatile(\"cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\"\n"
+          "                       :: \"r\"(tcf_s(dst + VST)), \"l\"(gU + (long long)kt * (UST / 2)), \"r\"(UST), \"r\"(tcf_s(&full[s])) : \"memory\");\n"
+          "        }\n"
+          "      }\n"
+          "    }\n"
+          "  } else if (warp == 1) {\n"
+          "    if (lane == 0) {  // MMA issuer: D[t][k] += V_p[t][c] U_p[k][c] for every point p\n"
+       << "      const unsigned idesc = (1u << 4) | (" << (fp16 ? 0 : 1) << "u << 7) | (" << (fp16 ? 0 : 1)
+       << "u << 10) | ((unsigned)(NK >> 3) << 17) | (8u << 24);\n"
+          "      int g = 0, it = 0;\n"
+          "      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {\n"
+          "        const int ab = it % NB;\n"
+          "        if (it >= NB) tcf_wait(&acc_empty[ab], (unsigned)(((it / NB) - 1) & 1));\n"
+          "        asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n"
+          "        for (int kt = 0; kt < nk; ++kt, ++g) {\n"
+          "          const int s = g % ST;\n"
+          "          tcf_wait(&full[s], (unsigned)((g / ST) & 1));\n"
+          "          asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n"
+          "          const unsigned a0 = tcf_s(smem + s * STB), b0 = a0 + VST;\n"
+          "#pragma unroll\n"
+          "          for (int p = 0; p < P; ++p) {\n"
+          "            if (dbg & 1) break;\n"
+          "            const tcf_u64 da = tcf_desc(a0 + p * 4096, 2048, 128);\n"
+          "            const tcf_u64 db = tcf_desc(b0 + p * (NK * 32), NK * 16, 128);\n"
+          "            asm volatile(\"{\\n\\t.reg .pred q;\\n\\tsetp.ne.b32 q, %4, 0;\\n\\t\"\n"
+          "                         \"tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q;\\n\\t}\\n\"\n"
+          "                         :: \"r\"(tmem + (unsigned)(ab * 256 + p * NK)), \"l\"(da), \"l\"(db), \"r\"(idesc), \"r\"((unsigned)kt) : \"memory\");\n"
+          "          }\n"
+          "          asm volatile(\"tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\" :: \"r\"(tcf_s(&empty[s])) : \"memory\");\n"
+          "        }\n"
+          "        asm volatile(\"tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\" :: \"r\"(tcf_s(&acc_full[ab])) : \"memory\");\n"
+          "      }\n"
+          "    }\n"
+          "  } else {\n"
+          "    // epilogue: warp (2..5) % 4 selects TMEM lanes = tiles [32 q4, 32 q4 + 32) of the block\n"
+          "    const int q4 = warp & 3;\n"
+          "    int it = 0;\n"
+          "    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {\n"
+          "      const int kb = tile % n_kb, tb = tile / n_kb;\n"
+          "      const int ab = it % NB;\n"
+          "      tcf_wait(&acc_full[ab], (unsigned)((it / NB) & 1));\n"
+          "      asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n"
+          "      const int t0 = tb * 128;\n"
+          "      const int t = t0 + q4 * 32 + lane;\n"
+          "      const int g0 = t0 / tw, off0 = t0 - g0 * tw;\n"
+          "      const int img0 = g0 / th, ti0 = g0 - img0 * th;\n"
+          "      const int off = off0 + q4 * 32 + lane;\n"
+          "      const int kk = idiv_small(off, tw, rtw), tj = off - kk * tw;\n"
+          "      const int di = idiv_small(ti0 + kk, th, rth);\n"
+          "      const int ti = ti0 + kk - di * th;\n"
+       << "      const int y0 = ti * " << m << ", x0 = tj * " << m << ";\n"
+       << "      const bool live = t < T;\n"
+          "      const bool inner = y0 + " << m << " <= Ho && x0 + " << m << " <= Wo;\n"
+          "      y_t* ybase = y + ((long long)(img0 + di) * K) * Ho * Wo + (long long)y0 * Wo + x0;\n"
+          "      const unsigned trow = tmem + ((unsigned)(q4 * 32) << 16) + (unsigned)(ab * 256);\n"
+          "#pragma unroll 1\n"
+          "      for (int kc = 0; kc < ((dbg & 2) ? 0 : NK); kc += KC) {\n"
+          "        unsigned rr[P][KC];\n"
+          "#pragma unroll\n"
+          "        for (int p = 0; p < P; ++p) {\n";
+    if (KC == 8)
+        os << "          asm volatile(\"tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\"\n"
+              "                       : \"=r\"(rr[p][0]), \"=r\"(rr[p][1]), \"=r\"(rr[p][2]), \"=r\"(rr[p][3]),\n"
+              "                         \"=r\"(rr[p][4]), \"=r\"(rr[p][5]), \"=r\"(rr[p][6]), \"=r\"(rr[p][7])\n"
+              "                       : \"r\"(trow + (unsigned)(p * NK + kc)));\n";
+    else
+        os << "          asm volatile(\"tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\"\n"
+              "                       : \"=r\"(rr[p][0]), \"=r\"(rr[p][1]), \"=r\"(rr[p][2]), \"=r\"(rr[p][3])\n"
+              "                       : \"r\"(trow + (unsigned)(p * NK + kc)));\n";
+    os << "        }\n"
+          "        asm volatile(\"tcgen05.wait::ld.sync.aligned;\" ::: \"memory\");\n"
+          "#pragma unroll\n"
+          "        for (int j = 0; j < KC; ++j) {\n"
+          "          const int k = kb * NK + kc + j;\n"
+          "          if (!live || k >= K || (dbg & 4)) continue;\n";
+    std::vector<std::vector<std::string>> mm(n, std::vector<std::string>(n));
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+            mm[a][b] = "m" + std::to_string(a) + "_" + std::to_string(b);
+            os << "          const ct_t " << mm[a][b] << " = (ct_t)__uint_as_float(rr[" << a * n + b << "][j]);\n";
+        }
+    Emitter em(os, ty.compute_double, ctr);
+    auto yv = em.apply2d(AT, mm);
+    auto val = [&](int a, int b) { return store_cvt(ty.compute_double, ty.y_double, yv[a][b]); };
+    os << "          y_t* dst = ybase + (long long)k * Ho * Wo;\n"
+          "          if (inner) {\n";
+    if (m % 2 == 0) {
+        os << "            if ((Wo & 1) == 0) {\n";
+        for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; b += 2)
+                os << "              *reinterpret_cast<" << PT << "*>(dst + " << a << " * Wo + " << b << ") = make_" << PT
+                   << "(" << val(a, b) << ", " << val(a, b + 1) << ");\n";
+        os << "            } else {\n";
+        for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; ++b) os << "              dst[" << a << " * Wo + " << b << "] = " << val(a, b) << ";\n";
+        os << "            }\n";
+    } else {
+        for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; ++b) os << "            dst[" << a << " * Wo + " << b << "] = " << val(a, b) << ";\n";
+    }
+    os << "          } else {\n";
+    for (int a = 0; a < m; ++a) {
+        os << "            if (y0 + " << a << " < Ho) {\n";
+        for (int b = 0; b < m; ++b)
+            os << "              if (x0 + " << b << " < Wo) dst[" << a << " * Wo + " << b << "] = " << val(a, b) << ";\n";
+        os << "            }\n";
+    }
+    os << "          }\n"
+          "        }\n"
+          "      }\n"
+          "      asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n"
+          "      __syncwarp();\n"
+          "      if (lane == 0) asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(tcf_s(&acc_empty[ab])) : \"memory\");\n"
+          "    }\n"
+          "  }\n"
+          "  asm volatile(\"tcgen05.fence::before_thread_sync;\" ::: \"memory\");\n"
+          "  __syncthreads();\n"
+          "  if (warp == 1) {\n"
+          "    asm volatile(\"tcgen05.fence::after_thread_sync;\" ::: \"memory\");\n"
+          "    asm volatile(\"tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\" :: \"r\"(tmem) : \"memory\");\n"
+          "  }\n"
+          "}\n\n";
+}
+
 std::string gen_layer_source_tc(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
-                                const GenTypes& ty, bool fp16) {
+                                const GenTypes& ty, bool fp16, int fused_nk) {
     const int n = r + m - 1, P = n * n;
     std::ostringstream os;
     os << header(ty)
@@ -718,6 +922,31 @@ std::string gen_layer_source_tc(int r, int m, const MatProg& G, const MatProg& B
        << "static __device__ __forceinline__ long long tc_off(long long row, long long c, long long Cp) {\n"
        << "  return ((row >> 7) * (Cp >> 5) + (c >> 5)) * 4096 + ((c >> 3) & 3) * 1024 + (row & 127) * 8 + (c & 7);\n"
        << "}\n";
+    // Operand layouts written by the gather transforms.  Unfused (K3t kernel,
+    // tc_contract.cu): X16[p][row/128][c/32][(c/8)%4][(row%128)/8][row%8][c%8],
+    // p-stride = rows x Cp.  Fused (wino_tcf below): every pipeline stage of a
+    // (128-tile | NK-filter, 16-channel) block holds all P points contiguously,
+    //   V16[t/128][c/16][p][(c/8)%2][(t%128)/8][t%8][c%8]      (p-stride 2048)
+    //   U16[k/NK][c/16][p][(c/8)%2][(k%NK)/8][k%8][c%8]         (p-stride 16 NK)
+    if (fused_nk) {
+        const int NK = fused_nk;
+        os << "static __device__ __forceinline__ long long tc_voff(long long t, long long c, long long Cp) {\n"
+           << "  return ((t >> 7) * (Cp >> 4) + (c >> 4)) * " << P * 2048
+           << "LL + ((c >> 3) & 1) * 1024 + (t & 127) * 8 + (c & 7);\n}\n"
+           << "static __device__ __forceinline__ long long tc_uoff(long long k, long long c, long long Cp) {\n"
+           << "  return ((k / " << NK << ") * (Cp >> 4) + (c >> 4)) * " << (long long)P * NK * 16 << "LL + ((c >> 3) & 1) * "
+           << NK * 8 << " + (k % " << NK << ") * 8 + (c & 7);\n}\n"
+           << "static __device__ __forceinline__ long long tc_vstride(long long, long long) { return 2048; }\n"
+           << "static __device__ __forceinline__ long long tc_ustride(long long, long long) { return " << NK * 16
+           << "; }\n";
+    } else {
+        os << "static __device__ __forceinline__ long long tc_voff(long long t, long long c, long long Cp) {\n"
+              "  return tc_off(t, c, Cp);\n}\n"
+              "static __device__ __forceinline__ long long tc_uoff(long long k, long long c, long long Cp) {\n"
+              "  return tc_off(k, c, Cp);\n}\n"
+              "static __device__ __forceinline__ long long tc_vstride(long long Cp, long long Tp) { return Cp * Tp; }\n"
+              "static __device__ __forceinline__ long long tc_ustride(long long Cp, long long Kp) { return Cp * Kp; }\n";
+    }
     const std::string cv = ty.compute_double ? "to16(__double2float_rn(" : "to16((";
     int ctr = 0;
     // filter: one thread per (k, c)
@@ -836,8 +1065,8 @@ std::string gen_layer_source_tc(int r, int m, const MatProg& G, const MatProg& B
     {
         os << "static __device__ __forceinline__ void filter_tcg(const in_t* __restrict__ w, unsigned short* __restrict__ U,\n"
               "    int K, int C, long long Kp, long long Cp, int k, int c) {\n"
-              "  const long long plane = Cp * Kp;\n"
-              "  unsigned short* o = U + tc_off(k, c, Cp);\n"
+              "  const long long plane = tc_ustride(Cp, Kp);\n"
+              "  unsigned short* o = U + tc_uoff(k, c, Cp);\n"
               "  if (k >= K || c >= C) {\n"
               "#pragma unroll\n"
            << "    for (int p = 0; p < " << P << "; ++p) o[p * plane] = 0;\n"
@@ -859,10 +1088,10 @@ std::string gen_layer_source_tc(int r, int m, const MatProg& G, const MatProg& B
         os << "static __device__ __forceinline__ void input_tcg(const in_t* __restrict__ x, unsigned short* __restrict__ V,\n"
               "    int C, int H, int W, int pad, int th, int tw, long long T, long long Tp, long long Cp,\n"
               "    float rtw, float rth, int t0, int c) {\n"
-              "  const long long plane = Cp * Tp;\n"
+              "  const long long plane = tc_vstride(Cp, Tp);\n"
               "  const int tl = ((threadIdx.x >> 5) << 2) + ((threadIdx.x >> 3) & 3);\n"
               "  const int t = t0 + tl;\n"
-              "  unsigned short* o = V + tc_off(t, c, Cp);\n"
+              "  unsigned short* o = V + tc_voff(t, c, Cp);\n"
               "  if (c >= C || t >= T) {\n"
               "#pragma unroll\n"
            << "    for (int p = 0; p < " << P << "; ++p) o[p * plane] = 0;\n"
@@ -912,9 +1141,9 @@ std::string gen_layer_source_tc(int r, int m, const MatProg& G, const MatProg& B
         os << "static __device__ __forceinline__ void input_tcg8(const in_t* __restrict__ x, unsigned short* __restrict__ V,\n"
               "    int C, int H, int W, int pad, int th, int tw, long long T, long long Tp, long long Cp,\n"
               "    float rtw, float rth, int t0, int c0) {\n"
-              "  const long long plane = Cp * Tp;\n"
+              "  const long long plane = tc_vstride(Cp, Tp);\n"
               "  const int t = t0 + threadIdx.x;\n"
-              "  uint4* o = reinterpret_cast<uint4*>(V + tc_off(t, c0, Cp));\n"
+              "  uint4* o = reinterpret_cast<uint4*>(V + tc_voff(t, c0, Cp));\n"
            << "  unsigned pk[" << P << "][4];\n"
            << "  if (t >= T) {\n"
               "#pragma unroll\n"
@@ -1001,12 +1230,18 @@ std::string gen_layer_source_tc(int r, int m, const MatProg& G, const MatProg& B
           "    const int k = ((int)blockIdx.x - n_tb) * 32 + ((threadIdx.x >> 5) << 2) + ((threadIdx.x >> 3) & 3);\n"
           "    if (k < Kp) filter_tcg(w, U, K, C, Kp, Cp, k, c);\n"
           "  }\n"
+          "}\n\n"
+          "extern \"C\" __global__ void __launch_bounds__(256) wino_filter_tcg(\n"
+          "    const in_t* __restrict__ w, unsigned short* __restrict__ U, int K, int C, long long Kp, long long Cp) {\n"
+          "  const int k = (int)blockIdx.x * 32 + ((threadIdx.x >> 5) << 2) + ((threadIdx.x >> 3) & 3);\n"
+          "  if (k < Kp) filter_tcg(w, U, K, C, Kp, Cp, k, blockIdx.y * 8 + (threadIdx.x & 7));\n"
           "}\n\n";
     int TB = 128;
     while (TB > 32 && (long long)P * TB * 4 > 64 * 1024) TB /= 2;
     emit_output_kernel(os, r, m, AT, ty, TB, ctr, "float", 4);
     emit_output_flat(os, r, m, AT, ty, TB, ctr, "float", 4);
     emit_output_gather(os, r, m, AT, ty, 128, ctr, "float");
+    if (fused_nk) emit_tcf_kernel(os, r, m, AT, ty, fp16, fused_nk, ctr);
     return os.str();
 }
 

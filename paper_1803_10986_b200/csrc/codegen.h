@@ -41,9 +41,10 @@ std::string validate(const MatProg& m, int expect_rows, int expect_cols, const c
 // so one pipeline stage of a contraction tile is a single contiguous block.
 std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
                              const GenTypes& ty, int bm, int bn);
-// tensor-core variant: 16-bit U/V in the UMMA K-major core-matrix layout (see codegen.cpp)
+// tensor-core variant: 16-bit U/V in the UMMA K-major core-matrix layout (see codegen.cpp);
+// fused_nk > 0: the fused K3t+K4 layouts and kernel (wino_tcf, NK filters per tile)
 std::string gen_layer_source_tc(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
-                                const GenTypes& ty, bool fp16);
+                                const GenTypes& ty, bool fp16, int fused_nk = 0);
 std::string gen_tile_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
                             const GenTypes& ty);
 

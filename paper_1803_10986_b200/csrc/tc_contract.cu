@@ -50,9 +50,9 @@ __device__ __forceinline__ void bar_wait(u64* b, unsigned parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "TC_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
         "@!P1 bra TC_WAIT_%=;\n}\n" ::"r"(su32(b)),
-        "r"(parity), "r"(1000000u)
+        "r"(parity)
         : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, u64* b) {

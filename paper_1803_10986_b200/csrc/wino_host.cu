@@ -197,6 +197,8 @@ struct GemmCfg {
 // ------------------------------------------------------------------ plan
 struct wino_plan {
     int r, m, n, precision, chsum, mode;
+    int nk = 0;  // fused tensor-core modes: filters per TMEM block (P * nk <= 512)
+    bool fused() const { return mode >= WINO_CONTRACT_TCF_BF16; }
     wino::MatProg G, BT, AT;
     wino::GenTypes ty;
     wino::GemmCfg gemm;
@@ -268,12 +270,19 @@ int layout_of(const wino_plan* p, const wino_layer_shape* s, wino_layer_layout* 
     L->Tp = round_up(L->T > 0 ? L->T : 1, p->gemm.bn());
     L->Cp = round_up(s->C, p->gemm.bk);
     L->Kp = round_up(s->K, p->gemm.bm());
+    if (p->fused()) {  // wino_tcf blocking: 128 tiles x nk filters x 16 channels
+        L->bm = p->nk;
+        L->bn = 128;
+        L->Tp = round_up(L->T > 0 ? L->T : 1, 128);
+        L->Cp = round_up(s->C, 16);
+        L->Kp = round_up(s->K, p->nk);
+    }
     const bool tc = p->mode >= WINO_CONTRACT_TC_BF16;
     L->elem_bytes_uv = tc ? 2 : p->ty.uv_double ? 8 : 4;  // tc: 16-bit U/V, fp32 M
     L->elem_bytes_y = p->ty.y_double ? 8 : 4;
     L->u_bytes = (size_t)L->P * L->Cp * L->Kp * L->elem_bytes_uv;
     L->v_bytes = (size_t)L->P * L->Cp * L->Tp * L->elem_bytes_uv;
-    L->m_bytes = (size_t)L->P * L->Kp * L->Tp * (tc ? 4 : L->elem_bytes_uv);
+    L->m_bytes = p->fused() ? 0 : (size_t)L->P * L->Kp * L->Tp * (tc ? 4 : L->elem_bytes_uv);
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     L->workspace_bytes = al(L->u_bytes) + al(L->v_bytes) + al(L->m_bytes);
     return WINO_OK;
@@ -348,8 +357,8 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
     if (r < 1 || m < 1) return wino::fail(WINO_EINVAL, "kernel and output sizes must be >= 1");
     if (precision < 0 || precision > 2) return wino::fail(WINO_EINVAL, "precision must be fp32, fp64 or mixed");
     if (channel_sum < 0 || channel_sum > 1) return wino::fail(WINO_EINVAL, "channel_sum must be linear or pairwise");
-    if (contract_mode < 0 || contract_mode > 3)
-        return wino::fail(WINO_EINVAL, "contract mode must be exact, ffma, tc_bf16 or tc_fp16");
+    if (contract_mode < 0 || contract_mode > 5)
+        return wino::fail(WINO_EINVAL, "contract mode must be exact, ffma, tc_bf16, tc_fp16, tcf_bf16 or tcf_fp16");
     if (contract_mode >= WINO_CONTRACT_TC_BF16 && precision == WINO_FP64)
         return wino::fail(WINO_EINVAL, "tensor-core contraction needs fp32 or mixed precision");
     const int n = r + m - 1;
@@ -361,6 +370,15 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
     p->precision = precision;
     p->chsum = channel_sum;
     p->mode = contract_mode;
+    if (p->fused()) {
+        const int P = n * n;
+        p->nk = std::min(256, (512 / P) / 16 * 16);
+        if (const char* e = getenv("WINO_TCF_NK")) {  // tuning: smaller blocks (16 x P <= 256: double-buffered TMEM)
+            const int v = atoi(e);
+            if (v >= 16 && v % 16 == 0 && v <= p->nk) p->nk = v;
+        }
+        if (p->nk < 16) return wino::fail(WINO_EUNSUPPORTED, "fused tensor-core mode needs alpha^2 <= 32");
+    }
     if (convert_prog(G, &p->G) || convert_prog(BT, &p->BT) || convert_prog(AT, &p->AT))
         return wino::fail(WINO_EINVAL, "malformed program table");
     std::string e = wino::validate(p->G, n, r, "G");
@@ -394,7 +412,9 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
     p->layer.name = "wino_layer_" + tag + ".cu";
     p->layer.source = contract_mode >= WINO_CONTRACT_TC_BF16
                           ? wino::gen_layer_source_tc(r, m, p->G, p->BT, p->AT, p->ty,
-                                                      contract_mode == WINO_CONTRACT_TC_FP16)
+                                                      contract_mode == WINO_CONTRACT_TC_FP16 ||
+                                                          contract_mode == WINO_CONTRACT_TCF_FP16,
+                                                      p->nk)
                           : wino::gen_layer_source(r, m, p->G, p->BT, p->AT, p->ty, p->gemm.bm(), p->gemm.bn());
     p->tile.name = "wino_tile_" + tag + ".cu";
     p->tile.source = wino::gen_tile_source(r, m, p->G, p->BT, p->AT, p->ty);
@@ -439,9 +459,16 @@ int wino_filter_transform(wino_plan* plan, const wino_layer_shape* s, const void
     int rc = layout_of(plan, s, &L);
     if (rc) return rc;
     CUfunction f;
-    if ((rc = plan->layer.function("wino_filter_xform", &f))) return rc;
     int K = s->K, C = s->C;
     long long Kp = L.Kp, Cp = L.Cp;
+    if (plan->mode >= WINO_CONTRACT_TC_BF16 && (k1_gather() || plan->fused()) && Cp / 8 <= 65535) {
+        if ((rc = plan->layer.function("wino_filter_tcg", &f))) return rc;
+        void* args[] = {(void*)&w, &U, &K, &C, &Kp, &Cp};
+        return wino::launch(f, dim3(cdiv(Kp, 32), (unsigned)(Cp / 8), 1), dim3(256), 0, stream, args,
+                            "filter_transform");
+    }
+    if (plan->fused()) return wino::fail(WINO_EUNSUPPORTED, "filter_transform: grid too large for the fused layout");
+    if ((rc = plan->layer.function("wino_filter_xform", &f))) return rc;
     int smem = 0;
     const int tb = plan->mode >= WINO_CONTRACT_TC_BF16 ? 64 : xform_block(plan, &smem);
     void* args[] = {(void*)&w, &U, &K, &C, &Kp, &Cp};
@@ -466,7 +493,7 @@ int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, c
     const long long blocks = (long long)n_tb * (tc ? Cp / 8 : Cp) + (long long)n_kb * Cp;
     if (blocks >= (1LL << 31)) return wino::fail(WINO_EUNSUPPORTED, "transforms: grid too large");
     int cfast = k1_cfast(), Wl = 0;
-    if (tc && k1_gather() && Cp / 8 <= 65535 && L.P <= 16 && !k1_no8()) {
+    if (tc && (k1_gather() || plan->fused()) && Cp / 8 <= 65535 && L.P <= 16 && !k1_no8()) {
         CUfunction fg;
         if ((rc = plan->layer.function("wino_transforms_tcg8", &fg))) return rc;
         float rtw = 1.0f / tw, rth = 1.0f / th;
@@ -476,7 +503,7 @@ int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, c
         return wino::launch(fg, dim3((unsigned)(nt128 + nk16), (unsigned)(Cp / 8)), dim3(128), 0, stream, args,
                             "transforms");
     }
-    if (tc && k1_gather() && Cp / 8 <= 65535) {
+    if (tc && (k1_gather() || plan->fused()) && Cp / 8 <= 65535) {
         CUfunction fg;
         if ((rc = plan->layer.function("wino_transforms_tcg", &fg))) return rc;
         float rtw = 1.0f / tw, rth = 1.0f / th;
@@ -494,6 +521,7 @@ int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, c
                         &Wl, &rtw, &rth};
         return wino::launch(fg, dim3((unsigned)Cp, (unsigned)(n_tb + n_kb)), dim3(tb), 0, stream, args, "transforms");
     }
+    if (plan->fused()) return wino::fail(WINO_EUNSUPPORTED, "transforms: grid too large for the fused layout");
     void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &n_tb, (void*)&w, &U, &K, &Kp, &n_kb, &cfast};
     return wino::launch(f, dim3((unsigned)blocks, 1, 1), dim3(tb), (unsigned)smem, stream, args, "transforms");
 }
@@ -517,20 +545,22 @@ int wino_input_transform(wino_plan* plan, const wino_layer_shape* s, const void*
             return wino::launch(f, dim3((unsigned)Cp, (unsigned)n_tb), dim3(tb), 0, stream, args, "input_transform");
         }
     }
-    if (plan->mode >= WINO_CONTRACT_TC_BF16 && k1_gather() && Cp / 8 <= 65535 && L.P <= 16 && !k1_no8()) {
+    if (plan->mode >= WINO_CONTRACT_TC_BF16 && (k1_gather() || plan->fused()) && Cp / 8 <= 65535 && L.P <= 16 &&
+        !k1_no8()) {
         if ((rc = plan->layer.function("wino_input_tcg8", &f))) return rc;
         float rtw = 1.0f / tw, rth = 1.0f / th;
         void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &rtw, &rth};
         return wino::launch(f, dim3((unsigned)cdiv(Tp, 128), (unsigned)(Cp / 8)), dim3(128), 0, stream, args,
                             "input_transform");
     }
-    if (plan->mode >= WINO_CONTRACT_TC_BF16 && k1_gather() && Cp / 8 <= 65535) {
+    if (plan->mode >= WINO_CONTRACT_TC_BF16 && (k1_gather() || plan->fused()) && Cp / 8 <= 65535) {
         if ((rc = plan->layer.function("wino_input_tcg", &f))) return rc;
         float rtw = 1.0f / tw, rth = 1.0f / th;
         void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &rtw, &rth};
         return wino::launch(f, dim3((unsigned)cdiv(Tp, 32), (unsigned)(Cp / 8)), dim3(256), 0, stream, args,
                             "input_transform");
     }
+    if (plan->fused()) return wino::fail(WINO_EUNSUPPORTED, "input_transform: grid too large for the fused layout");
     if ((rc = plan->layer.function("wino_input_xform", &f))) return rc;
     void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp};
     if (plan->mode >= WINO_CONTRACT_TC_BF16)
@@ -547,6 +577,8 @@ int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, con
     if (rc) return rc;
     if (((uintptr_t)U | (uintptr_t)V | (uintptr_t)M) & 15)
         return wino::fail(WINO_EINVAL, "contract: U, V, M must be 16-byte aligned");
+    if (plan->fused())
+        return wino::fail(WINO_EINVAL, "contract: fused tensor-core plan has no M; use wino_contract_output");
     if (plan->mode >= WINO_CONTRACT_TC_BF16)
         return wino::tc_contract_launch(U, V, M, L.Kp, L.Tp, L.Cp, L.P, plan->mode == WINO_CONTRACT_TC_FP16,
                                         stream);
@@ -580,6 +612,8 @@ int wino_output_transform(wino_plan* plan, const wino_layer_shape* s, const void
     wino_layer_layout L;
     int rc = layout_of(plan, s, &L);
     if (rc) return rc;
+    if (plan->fused())
+        return wino::fail(WINO_EINVAL, "output_transform: fused tensor-core plan has no M; use wino_contract_output");
     CUfunction f;
     int K = s->K, Ho = L.Ho, Wo = L.Wo, th = L.th, tw = L.tw;
     long long T = L.T, Tp = L.Tp, Kp = L.Kp;
@@ -630,8 +664,42 @@ int wino_conv2d(wino_plan* plan, const wino_layer_shape* s, const void* x, const
     char* V = U + al(L.u_bytes);
     char* M = V + al(L.v_bytes);
     if ((rc = wino_transforms(plan, s, x, w, U, V, stream))) return rc;
+    if (plan->fused()) return wino_contract_output(plan, s, U, V, y, stream);
     if ((rc = wino_contract(plan, s, U, V, M, stream))) return rc;
     return wino_output_transform(plan, s, M, y, stream);
+}
+
+int wino_contract_output(wino_plan* plan, const wino_layer_shape* s, const void* U, const void* V, void* y,
+                         void* stream) {
+    wino_layer_layout L;
+    int rc = layout_of(plan, s, &L);
+    if (rc) return rc;
+    if (!plan->fused()) return wino::fail(WINO_EINVAL, "contract_output: needs a fused tensor-core plan (tcf_*)");
+    if (((uintptr_t)U | (uintptr_t)V) & 15) return wino::fail(WINO_EINVAL, "contract_output: U, V must be 16-byte aligned");
+    if (s->N == 0) return WINO_OK;
+    CUfunction f;
+    if ((rc = plan->layer.function("wino_tcf", &f))) return rc;
+    // must match codegen.cpp emit_tcf_kernel
+    const long long P = L.P, NK = plan->nk;
+    const long long stb = P * 4096 + P * NK * 32;
+    const long long st = std::max(1LL, std::min(4LL, (232448 - 256) / stb));
+    const unsigned smem = (unsigned)(st * stb + 256);
+    long long tiles = (L.Tp / 128) * (L.Kp / NK);
+    if (tiles > (1LL << 30)) return wino::fail(WINO_EUNSUPPORTED, "contract_output: too many tiles");
+    int n_tiles = (int)tiles, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int K = s->K, Ho = L.Ho, Wo = L.Wo, th = L.th, tw = L.tw;
+    long long T = L.T, Tp = L.Tp, Kp = L.Kp, Cp = L.Cp;
+    float rtw = 1.0f / tw, rth = 1.0f / th;
+    static const int dbg = [] {  // timing experiments only: 1 = no MMAs, 2 = no epilogue, 4 = no y stores
+        const char* e = std::getenv("WINO_TCF_DBG");
+        return e ? atoi(e) : 0;
+    }();
+    int dbgv = dbg;
+    void* args[] = {(void*)&U, (void*)&V, &y, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp, &Cp, &n_tiles, &rtw, &rth, &dbgv};
+    return wino::launch(f, dim3((unsigned)std::min<long long>(tiles, sms)), dim3(192), smem, stream, args,
+                        "contract_output");
 }
 
 int wino_tile_hadamard2d(wino_plan* plan, int64_t B, int C, const void* h, const void* x, void* z, void* stream) {

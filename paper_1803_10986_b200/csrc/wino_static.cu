@@ -272,7 +272,7 @@ __global__ void mean_kernel(long long n, const double* __restrict__ v, double* _
 // ---------------------------------------------------------------- peak probes
 // Arithmetic-throughput probes for the roofline denominators (mode 0: FFMA,
 // 1: FMUL+FADD pairs, 2: DFMA, 3: DMUL+DADD).  8 independent chains per thread.
-__global__ void peak_probe_kernel(int mode, int iters, float seedf, float* __restrict__ out) {
+__global__ void peak_probe_kernel(int mode, int iters, float seedf, float* out) {
     float a[8];
     double d[8];
     for (int i = 0; i < 8; ++i) {
@@ -288,6 +288,13 @@ __global__ void peak_probe_kernel(int mode, int iters, float seedf, float* __res
         for (int it = 0; it < iters; ++it)
 #pragma unroll
             for (int i = 0; i < 8; ++i) a[i] = __fadd_rn(__fmul_rn(a[i], m), c);
+    } else if (mode == 4) {
+        // FMUL+FADD with register operands (multiplier and addend loaded at run
+        // time): the form the contraction issues, without immediate operands
+        const float mr = out[2] + m, cr = out[3] + c;
+        for (int it = 0; it < iters; ++it)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = __fadd_rn(__fmul_rn(a[i], mr), cr);
     } else if (mode == 2) {
         for (int it = 0; it < iters; ++it)
 #pragma unroll
@@ -389,7 +396,7 @@ int wino_program_eval(int dtype, const void* ops, int nops, int cols, int64_t co
 
 
 int wino_peak_probe(int mode, int blocks, int iters, float* out, void* stream) {
-    if (mode < 0 || mode > 3 || blocks < 1 || iters < 1) return wino::fail(WINO_EINVAL, "peak_probe: bad arguments");
+    if (mode < 0 || mode > 4 || blocks < 1 || iters < 1) return wino::fail(WINO_EINVAL, "peak_probe: bad arguments");
     peak_probe_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(mode, iters, 1.0f, out);
     return wino::after_launch("peak_probe");
 }

@@ -32,7 +32,7 @@ from .transforms import TransformSet
 PRECISION_MODES = ("fp32", "fp64", "mixed")
 DOT_ORDERS = ("linear", "huffman")
 CHANNEL_SUMS = ("linear", "pairwise")
-CONTRACTIONS = ("exact", "ffma", "tc_bf16", "tc_fp16")
+CONTRACTIONS = ("exact", "ffma", "tc_bf16", "tc_fp16", "tcf_bf16", "tcf_fp16")
 
 __all__ = [
     "ConvConfig", "EvalLeaf", "EvalNode", "huffman_order", "linear_order", "row_trees", "tree_depth",

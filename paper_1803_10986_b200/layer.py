@@ -78,12 +78,17 @@ class LayerOp:
     # -- individual stages (tests, profiling) --------------------------------
     @property
     def tensor_core(self) -> bool:
-        return self.contraction.startswith("tc_")
+        return self.contraction.startswith(("tc_", "tcf_"))
+
+    @property
+    def fused(self) -> bool:
+        """tcf_* modes: contraction + output transform in one kernel (no M)."""
+        return self.contraction.startswith("tcf_")
 
     def _uv_dtype(self):
-        if self.contraction == "tc_bf16":
+        if self.contraction in ("tc_bf16", "tcf_bf16"):
             return D.torch.bfloat16
-        if self.contraction == "tc_fp16":
+        if self.contraction in ("tc_fp16", "tcf_fp16"):
             return D.torch.float16
         return D.torch.float64 if self.cfg.precision == "fp64" else D.torch.float32
 
@@ -106,19 +111,26 @@ class LayerOp:
 
     # Tensor-core modes keep U/V as 16-bit UMMA operands:
     #   X16[p][row/128][c/32][(c/8)%4][(row%128)/8][row%8][c%8]
-    def _tc_unpack(self, X, R):
+    # Fused modes (tcf_*): every 16-channel stage of a (row block, all P) is contiguous:
+    #   X16[row/B][c/16][p][(c/8)%2][(row%B)/8][row%8][c%8],  B = 128 (V) or NK (U)
+    def _tc_unpack(self, X, R, B=128):
         L = self.layout
+        if self.fused:
+            return X.reshape(R // B, L.Cp // 16, L.P, 2, B // 8, 8, 8).permute(2, 1, 3, 6, 0, 4, 5).reshape(
+                L.P, L.Cp, R)
         return X.reshape(L.P, R // 128, L.Cp // 32, 4, 16, 8, 8).permute(0, 2, 3, 6, 1, 4, 5).reshape(L.P, L.Cp, R)
 
-    def _tc_pack(self, X, R):
+    def _tc_pack(self, X, R, B=128):
         L = self.layout
+        if self.fused:
+            return X.reshape(L.P, L.Cp // 16, 2, 8, R // B, B // 8, 8).permute(4, 1, 0, 2, 5, 6, 3).contiguous()
         return X.reshape(L.P, L.Cp // 32, 4, 8, R // 128, 16, 8).permute(0, 4, 1, 2, 5, 6, 3).contiguous()
 
     def unblock_u(self, U):
         """device layout of U -> dense U[P][Cp][Kp]"""
         L = self.layout
         if self.tensor_core:
-            return self._tc_unpack(U, L.Kp)
+            return self._tc_unpack(U, L.Kp, L.bm if self.fused else 128)
         return U.reshape(L.P, L.Kp // L.bm, L.Cp, L.bm).permute(0, 2, 1, 3).reshape(L.P, L.Cp, L.Kp)
 
     def unblock_v(self, V):
@@ -132,7 +144,7 @@ class LayerOp:
         """dense U[P][Cp][Kp] -> device layout"""
         L = self.layout
         if self.tensor_core:
-            return self._tc_pack(U.to(self._uv_dtype()), L.Kp)
+            return self._tc_pack(U.to(self._uv_dtype()), L.Kp, L.bm if self.fused else 128)
         return U.reshape(L.P, L.Cp, L.Kp // L.bm, L.bm).permute(0, 2, 1, 3).contiguous()
 
     def block_v(self, V):
@@ -149,6 +161,14 @@ class LayerOp:
                                                   D.ptr(M), D.stream_handle()), "contract")
         return M
 
+    def contract_output(self, U, V, out=None):
+        """fused modes: y = A^T (sum_c U_p V_p) A straight from the TMEM accumulators"""
+        if out is None:
+            out = D.empty(self.out_shape, self.out_dtype)
+        _native.check(_native.lib().wino_contract_output(self.plan.handle, ctypes.byref(self.shape), D.ptr(U),
+                                                         D.ptr(V), D.ptr(out), D.stream_handle()), "contract_output")
+        return out
+
     def output_transform(self, M, out=None):
         if out is None:
             out = D.empty(self.out_shape, self.out_dtype)
@@ -163,12 +183,28 @@ class HostPipeline:
     D2H run concurrently on three streams (PCIe is full duplex).  The filter
     transform K2 runs once per call (U does not depend on the images).
 
-    x_host / y_host must be pinned CPU tensors (N, C, H, W) / (N, K, Ho, Wo)."""
+    x_host / y_host must be pinned CPU tensors (N, C, H, W) / (N, K, Ho, Wo).
 
-    def __init__(self, ts: TransformSet, cfg: ConvConfig, N, C, H, W, K, pad, chunks=4, contraction="exact"):
+    `chunks` is a count (equal chunks) or a list of image counts (e.g. decreasing
+    sizes shorten the compute + D2H tail after the last H2D).  With `graph=True`
+    the second call with the same host buffers captures the whole multi-stream
+    pipeline (copies, kernels, cross-stream events) into a CUDA graph and later
+    calls replay it -- one launch instead of ~5 per chunk from Python."""
+
+    def __init__(self, ts: TransformSet, cfg: ConvConfig, N, C, H, W, K, pad, chunks=4, contraction="exact",
+                 graph=True):
         self.full = layer_op(ts, cfg, N, C, H, W, K, pad, contraction)
-        chunks = max(1, min(chunks, N))
-        self.bounds = [(i * N // chunks, (i + 1) * N // chunks) for i in range(chunks)]
+        if isinstance(chunks, int):
+            chunks = max(1, min(chunks, N))
+            self.bounds = [(i * N // chunks, (i + 1) * N // chunks) for i in range(chunks)]
+        else:
+            sizes = [int(c) for c in chunks]
+            if sum(sizes) != N or min(sizes) < 1:
+                raise ValueError("chunk sizes must be >= 1 and sum to N")
+            edges = np.cumsum([0] + sizes)
+            self.bounds = [(int(a), int(b)) for a, b in zip(edges[:-1], edges[1:])]
+        self.graph = graph
+        self._graphs, self._seen = {}, set()
         self.ops = [layer_op(ts, cfg, b - a, C, H, W, K, pad, contraction) for a, b in self.bounds]
         L = self.full.layout
         self.U = D.torch.empty((L.P, L.Cp, L.Kp), dtype=self.full._uv_dtype(), device="cuda")
@@ -181,6 +217,23 @@ class HostPipeline:
         self.ev = [(D.torch.cuda.Event(), D.torch.cuda.Event()) for _ in self.bounds]
 
     def __call__(self, x_host, w_host, y_host):
+        if not self.graph:
+            return self._run(x_host, w_host, y_host)
+        torch = D.torch
+        key = (x_host.data_ptr(), w_host.data_ptr(), y_host.data_ptr())
+        g = self._graphs.get(key)
+        if g is None and key in self._seen:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._run(x_host, w_host, y_host)
+            self._graphs[key] = g
+        if g is None:
+            self._seen.add(key)
+            return self._run(x_host, w_host, y_host)
+        g.replay()
+        return y_host
+
+    def _run(self, x_host, w_host, y_host):
         torch = D.torch
         lib = _native.lib()
         cur = torch.cuda.current_stream()
@@ -203,9 +256,14 @@ class HostPipeline:
                 xs, ys = self.x_dev[a:b], self.y_dev[a:b]
                 sh = ctypes.byref(op.shape)
                 _native.check(lib.wino_input_transform(op.plan.handle, sh, D.ptr(xs), D.ptr(V), sc), "input")
-                _native.check(lib.wino_contract(op.plan.handle, sh, D.ptr(self.U), D.ptr(V), D.ptr(M), sc),
-                              "contract")
-                _native.check(lib.wino_output_transform(op.plan.handle, sh, D.ptr(M), D.ptr(ys), sc), "output")
+                if op.fused:
+                    _native.check(lib.wino_contract_output(op.plan.handle, sh, D.ptr(self.U), D.ptr(V), D.ptr(ys),
+                                                           sc), "contract_output")
+                else:
+                    _native.check(lib.wino_contract(op.plan.handle, sh, D.ptr(self.U), D.ptr(V), D.ptr(M), sc),
+                                  "contract")
+                    _native.check(lib.wino_output_transform(op.plan.handle, sh, D.ptr(M), D.ptr(ys), sc),
+                                  "output")
                 e_out.record(self.s_cmp)
         with torch.cuda.stream(self.s_d2h):
             for (a, b), (_, e_out) in zip(self.bounds, self.ev):

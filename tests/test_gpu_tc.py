@@ -62,3 +62,41 @@ def test_tc_layer_error_vs_fp64(mode):
     yx = W.conv2d_layer(ts, x, w, W.ConvConfig(), pad=1)
     rel_exact = np.abs(yx.astype(np.float64) - y64).sum() / np.abs(y64).sum()
     assert rel_exact < rel
+
+
+@pytest.mark.parametrize("mode,dt", [("tcf_bf16", torch.bfloat16), ("tcf_fp16", torch.float16)])
+@pytest.mark.parametrize("geom", [(3, 70, 20, 20, 150, 1), (2, 16, 9, 11, 16, 0), (1, 33, 28, 28, 40, 1)],
+                         ids=lambda g: "N{}C{}H{}W{}K{}".format(*g[:5]))
+def test_tcf_fused_matches_rounded_gemm_then_output(mode, dt, geom):
+    """Fused K3t+K4 (all alpha^2 accumulators in TMEM, output transform in the
+    epilogue) == fp64 GEMM of the 16-bit operands followed by the fp64 output
+    transform, to fp32 accumulation accuracy; and == the unfused tc mode's result
+    within the same bound."""
+    N, C, H, Wd, K, pad = geom
+    pts = "0,1,-1,inf"
+    ts = W.build_transforms(3, 2, W.parse_points(pts))
+    op = W.layer_op(ts, W.ConvConfig(), N, C, H, Wd, K, pad, contraction=mode)
+    L = op.layout
+    x = torch.from_numpy(O.synthetic((N, C, H, Wd), 5, 0)).cuda()
+    w = torch.from_numpy(O.synthetic((K, C, 3, 3), 5, 1)).cuda()
+    U, V = op.filter_transform(w), op.input_transform(x)
+    y = op.contract_output(U, V)
+    torch.cuda.synchronize()
+    Uu = op.unblock_u(U).double()
+    Vu = op.unblock_v(V).double()
+    M = torch.einsum("pck,pct->pkt", Uu, Vu)[:, :K, :L.T]  # [P][K][T]
+    n = 4
+    AT = torch.tensor(np.array(ts.matrix_fp("A_T", "fp64"), dtype=np.float64)).cuda()
+    Mt = M.reshape(n, n, K, L.T).permute(2, 3, 0, 1)  # [K][T][n][n]
+    Yt = AT @ Mt @ AT.T  # [K][T][2][2]
+    Yt = Yt.reshape(K, N, L.th, L.tw, 2, 2).permute(1, 0, 2, 4, 3, 5).reshape(N, K, L.th * 2, L.tw * 2)
+    ref = Yt[:, :, :L.Ho, :L.Wo]
+    scale = torch.einsum("pck,pct->pkt", Uu.abs(), Vu.abs()).max().item() * 4
+    err = (y.double() - ref).abs().max().item()
+    assert err <= 2e-5 * scale, (err, scale)
+    # whole-layer API (wino_conv2d) gives the same bits as the stage calls
+    y2 = W.conv2d_layer(ts, x, w, W.ConvConfig(), pad=pad, contraction=mode)
+    assert torch.equal(y2, y)
+    # and agrees with the unfused tensor-core mode to accumulation accuracy
+    y3 = W.conv2d_layer(ts, x, w, W.ConvConfig(), pad=pad, contraction=mode.replace("tcf", "tc"))
+    assert (y3.double() - y.double()).abs().max().item() <= 2e-5 * scale

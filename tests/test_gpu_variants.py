@@ -1,0 +1,72 @@
+"""The alternative transform kernels (selected by environment variables, read
+once per process) must produce the same bits as the default kernels:
+
+  WINO_K1=tile     K1 parks V in smem and writes 16-byte rows (input_body) --
+                   also the fallback for grids beyond 65535 tile chunks
+  WINO_K4=staged   K4 stages M in smem (flat for m <= 2, banded otherwise)
+  WINO_K1TC=4x8    TC K1 with 4 tiles x 8 channels per warp also for P <= 16
+
+Each variant runs in a subprocess; its outputs are compared bitwise with the
+default kernels' outputs computed here (exact mode also with the oracle)."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import paper_1803_10986_b200 as W
+from oracle import wino_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # r, m, points, N, C, K, H, W, pad
+    (3, 2, "0,1,-1,inf", 3, 33, 70, 15, 17, 1),
+    (3, 4, "0,1,-1,1/2,-1/2,inf", 2, 20, 24, 20, 20, 1),
+    (3, 6, "0,-1,1,1/2,-1/2,2,-2,inf", 1, 17, 19, 29, 23, 1),
+]
+MODES = ["exact", "tc_bf16"]
+
+_CHILD = r"""
+import json, sys
+import numpy as np
+import paper_1803_10986_b200 as W
+from oracle import wino_oracle as O
+cases, modes, out = json.loads(sys.argv[1]), json.loads(sys.argv[2]), sys.argv[3]
+res = {}
+for i, (r, m, pts, N, C, K, H, Wd, pad) in enumerate(cases):
+    ts = W.build_transforms(r, m, W.parse_points(pts))
+    x = O.synthetic((N, C, H, Wd), 7, 0)
+    w = O.synthetic((K, C, r, r), 7, 99)
+    for mode in modes:
+        res[f"{i}/{mode}"] = W.conv2d_layer(ts, x, w, W.ConvConfig(), pad=pad, contraction=mode)
+np.savez(out, **res)
+"""
+
+
+def _run_variant(env_extra, tmp_path):
+    out = str(tmp_path / "variant.npz")
+    env = dict(os.environ, **env_extra)
+    here = os.path.dirname(os.path.abspath(__file__))
+    env["PYTHONPATH"] = os.pathsep.join([os.path.dirname(here), env.get("PYTHONPATH", "")])
+    subprocess.run([sys.executable, "-c", _CHILD, json.dumps(CASES), json.dumps(MODES), out], check=True, env=env,
+                   timeout=600)
+    return np.load(out)
+
+
+@pytest.mark.parametrize("env", [{"WINO_K1": "tile"}, {"WINO_K4": "staged"}, {"WINO_K1TC": "4x8"}],
+                         ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_variant_bits(env, tmp_path):
+    got = _run_variant(env, tmp_path)
+    for i, (r, m, pts, N, C, K, H, Wd, pad) in enumerate(CASES):
+        ts = W.build_transforms(r, m, W.parse_points(pts))
+        x = O.synthetic((N, C, H, Wd), 7, 0)
+        w = O.synthetic((K, C, r, r), 7, 99)
+        for mode in MODES:
+            want = W.conv2d_layer(ts, x, w, W.ConvConfig(), pad=pad, contraction=mode)
+            assert np.array_equal(got[f"{i}/{mode}"].view(np.uint32), want.view(np.uint32)), (env, i, mode)
+        trip = O.Triple.from_points(r, m, pts)
+        oracle = O.layer_conv2d(trip, x, w, pad, "fp32", "huffman", "linear")
+        assert np.array_equal(got[f"{i}/exact"].view(np.uint32), oracle.view(np.uint32)), (env, i)

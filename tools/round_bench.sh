@@ -18,6 +18,6 @@ python bench.py --ncu --steps 5 --warmup 3 > gpurun_out/b_small.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --ncu --steps 5 --warmup 3 > gpurun_out/ncu1.log 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"wino_contract|wino_transforms|wino_output_xform" -s 3 -c 3 \
+    -k regex:"wino_contract|wino_transforms|wino_output" -s 3 -c 3 \
     -o gpurun_out/prof_bench python bench.py --ncu --steps 2 --warmup 3 > gpurun_out/ncu2.log 2>&1
 echo all done
