@@ -17,6 +17,8 @@
 //   WINO_SUM      0 exact-linear, 1 exact-pairwise, 2 ffma-linear, 3 ffma-pairwise
 //   WINO_LEVELS   pairwise: slots of the chunk-level binary counter
 //   WINO_MAXREG   register cap (0 = __launch_bounds__ only)
+//   WINO_PACK     1: float only -- packed f32x2 arithmetic (two adjacent t columns per
+//                 instruction: FFMA2/FADD2 issue once for 64 lanes of work)
 //
 // Summation order (exact modes, bitwise equal to the reference):
 //   linear   : acc = -0; acc = acc + fl(u*v) for c = 0, 1, ...  (-0 + z = z exactly)
@@ -43,6 +45,9 @@
 #ifndef WINO_NOPROD
 #define WINO_NOPROD 0  // 1: no producer warp; the last consumer warp to release a stage refills it
 #endif
+#ifndef WINO_PACK
+#define WINO_PACK 0
+#endif
 #ifndef WINO_DBUF
 #define WINO_DBUF (WINO_SUM == 1 || WINO_SUM == 3)  // explicit fragment double buffer (pairwise)
 #endif
@@ -67,6 +72,51 @@ typedef double2 vec_t;
 #define XADD(a, b) __fadd_rn((a), (b))
 #define XFMA(a, b, c) __fmaf_rn((a), (b), (c))
 typedef float4 vec_t;
+#endif
+
+// Arithmetic on the accumulator unit.  Scalar: one DT per value.  Packed
+// (WINO_PACK): one u64 = f32x2 pair of adjacent t columns; the k-side operand
+// is broadcast into both halves.  The exact product is fma.rn.f32x2(a, b, -0):
+// fl(a*b + (-0)) == fl(a*b) for every a, b (including the sign of exact zeros:
+// +0 + -0 = +0, -0 + -0 = -0 under round-to-nearest).  The -0 pair arrives as a
+// kernel parameter so ptxas cannot fold it into an FMUL2 that it would then fuse
+// with the following FADD2 into an FFMA2 (verified on nvcc 12.9:
+// mul.rn.f32x2 + add.rn.f32x2 -> FFMA2 even with -fmad=false).  The SASS gate
+// (tests/test_abi.py) accepts FFMA2 in exact kernels only with a uniform addend.
+#if WINO_PACK
+#if WINO_DT_IS_DOUBLE
+#error "WINO_PACK needs float"
+#endif
+typedef u64 acc_t;
+#define NJ (WINO_TN / 2)
+#define ACC_NEG0 0x8000000080000000ull
+#define ACC_POS0 0ull
+static __device__ __forceinline__ u64 p_fma(u64 a, u64 b, u64 c) {
+    u64 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+static __device__ __forceinline__ u64 p_add(u64 a, u64 b) {
+    u64 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+static __device__ __forceinline__ u64 p_bcast(float a) {
+    u64 r;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(a));
+    return r;
+}
+#define AMUL(a, b) p_fma((a), (b), nz2)
+#define AADD(a, b) p_add((a), (b))
+#define AFMA(a, b, c) p_fma((a), (b), (c))
+#else
+typedef DT acc_t;
+#define NJ WINO_TN
+#define ACC_NEG0 ((DT)(-0.0))
+#define ACC_POS0 ((DT)0)
+#define AMUL(a, b) XMUL((a), (b))
+#define AADD(a, b) XADD((a), (b))
+#define AFMA(a, b, c) XFMA((a), (b), (c))
 #endif
 
 static __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -120,7 +170,7 @@ static __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsi
 
 extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, const DT* __restrict__ V,
                                                   DT* __restrict__ M, long long Kp, long long Tp, long long Cp,
-                                                  int n_tiles) {
+                                                  int n_tiles, u64 nz2) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     DT* sU = reinterpret_cast<DT*>(smem_raw);      // [STAGES][BK][BM]
     DT* sV = sU + WINO_STAGES * WINO_BK * BM;      // [STAGES][BK][BN]
@@ -208,27 +258,27 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
         const long long p = rest / n_kb;
 
 #if WINO_SUM == 0
-        DT acc[WINO_TM][WINO_TN];
+        acc_t acc[WINO_TM][NJ];
 #pragma unroll
         for (int i = 0; i < WINO_TM; ++i)
 #pragma unroll
-            for (int j = 0; j < WINO_TN; ++j) acc[i][j] = (DT)(-0.0);
+            for (int j = 0; j < NJ; ++j) acc[i][j] = ACC_NEG0;
 #elif WINO_SUM == 2
-        DT acc[WINO_TM][WINO_TN];
+        acc_t acc[WINO_TM][NJ];
 #pragma unroll
         for (int i = 0; i < WINO_TM; ++i)
 #pragma unroll
-            for (int j = 0; j < WINO_TN; ++j) acc[i][j] = (DT)0;
+            for (int j = 0; j < NJ; ++j) acc[i][j] = ACC_POS0;
 #else
-        DT pa[WINO_TM][WINO_TN];
+        acc_t pa[WINO_TM][NJ];
 #if WINO_SUM == 1
-        DT pb[WINO_TM][WINO_TN], pd[WINO_TM][WINO_TN];
+        acc_t pb[WINO_TM][NJ], pd[WINO_TM][NJ];
 #endif
         // Z: static counter inside a stage (a stage = WINO_BK/8 chunks of 8 channels);
         // slot: dynamic counter over stages (slot j holds 2^j stages)
 #define ZL (WINO_BK == 8 ? 1 : WINO_BK == 16 ? 1 : WINO_BK == 32 ? 2 : 3)
-        DT zs[ZL][WINO_TM][WINO_TN];
-        DT slot[WINO_LEVELS][WINO_TM][WINO_TN];
+        acc_t zs[ZL][WINO_TM][NJ];
+        acc_t slot[WINO_LEVELS][WINO_TM][NJ];
 #endif
 
 #pragma unroll 1
@@ -245,6 +295,26 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
             for (int kk0 = 0; kk0 < WINO_BK; kk0 += WINO_KU) {
                 // register double buffer: fragments of k-step kk+1 are loaded
                 // while k-step kk is multiplied
+#if WINO_PACK
+                u64 fa[2][WINO_TM], fb[2][NJ];
+                auto load_frag = [&](int buf, int kk) {
+#pragma unroll
+                    for (int q = 0; q < GM; ++q) {
+                        const float4 w4 = *reinterpret_cast<const float4*>(cu + kk * BM + q * (WINO_THM * VW) + tm * VW);
+                        fa[buf][q * VW + 0] = p_bcast(w4.x);
+                        fa[buf][q * VW + 1] = p_bcast(w4.y);
+                        fa[buf][q * VW + 2] = p_bcast(w4.z);
+                        fa[buf][q * VW + 3] = p_bcast(w4.w);
+                    }
+#pragma unroll
+                    for (int q = 0; q < GN; ++q) {
+                        const ulonglong2 w2 =
+                            *reinterpret_cast<const ulonglong2*>(cv + kk * BN + q * (WINO_THN * VW) + tn * VW);
+                        fb[buf][q * 2 + 0] = w2.x;
+                        fb[buf][q * 2 + 1] = w2.y;
+                    }
+                };
+#else
                 DT fa[2][WINO_TM], fb[2][WINO_TN];
                 auto load_frag = [&](int buf, int kk) {
 #pragma unroll
@@ -262,6 +332,7 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
                         for (int v = 0; v < VW; ++v) fb[buf][q * VW + v] = ww[v];
                     }
                 };
+#endif
 #if WINO_DBUF
                 load_frag(0, kk0);
 #endif
@@ -270,42 +341,42 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
                     const int kk = kk0 + kk1;
 #if WINO_DBUF
                     if (kk1 + 1 < WINO_KU) load_frag((kk1 + 1) & 1, kk + 1);
-                    const DT* a = fa[kk1 & 1];
-                    const DT* b = fb[kk1 & 1];
+                    const auto* a = fa[kk1 & 1];
+                    const auto* b = fb[kk1 & 1];
 #else
                     load_frag(0, kk);
-                    const DT* a = fa[0];
-                    const DT* b = fb[0];
+                    const auto* a = fa[0];
+                    const auto* b = fb[0];
 #endif
 #if WINO_SUM == 0
 #pragma unroll
                     for (int i = 0; i < WINO_TM; ++i)
 #pragma unroll
-                        for (int j = 0; j < WINO_TN; ++j) acc[i][j] = XADD(acc[i][j], XMUL(a[i], b[j]));
+                        for (int j = 0; j < NJ; ++j) acc[i][j] = AADD(acc[i][j], AMUL(a[i], b[j]));
 #elif WINO_SUM == 2
 #pragma unroll
                     for (int i = 0; i < WINO_TM; ++i)
 #pragma unroll
-                        for (int j = 0; j < WINO_TN; ++j) acc[i][j] = XFMA(a[i], b[j], acc[i][j]);
+                        for (int j = 0; j < NJ; ++j) acc[i][j] = AFMA(a[i], b[j], acc[i][j]);
 #else
                     const int pos = kk1 & 7;  // compile-time after unrolling (WINO_KU % 8 == 0)
 #pragma unroll
                     for (int i = 0; i < WINO_TM; ++i)
 #pragma unroll
-                        for (int j = 0; j < WINO_TN; ++j) {
+                        for (int j = 0; j < NJ; ++j) {
 #if WINO_SUM == 1
-                            const DT z = XMUL(a[i], b[j]);
+                            const acc_t z = AMUL(a[i], b[j]);
                             if (pos == 0) pa[i][j] = z;
-                            else if (pos == 1) pa[i][j] = XADD(pa[i][j], z);
+                            else if (pos == 1) pa[i][j] = AADD(pa[i][j], z);
                             else if (pos == 2) pb[i][j] = z;
-                            else if (pos == 3) { pb[i][j] = XADD(pb[i][j], z); pa[i][j] = XADD(pa[i][j], pb[i][j]); }
+                            else if (pos == 3) { pb[i][j] = AADD(pb[i][j], z); pa[i][j] = AADD(pa[i][j], pb[i][j]); }
                             else if (pos == 4) pb[i][j] = z;
-                            else if (pos == 5) pb[i][j] = XADD(pb[i][j], z);
+                            else if (pos == 5) pb[i][j] = AADD(pb[i][j], z);
                             else if (pos == 6) pd[i][j] = z;
-                            else { pd[i][j] = XADD(pd[i][j], z); pb[i][j] = XADD(pb[i][j], pd[i][j]); pa[i][j] = XADD(pa[i][j], pb[i][j]); }
+                            else { pd[i][j] = AADD(pd[i][j], z); pb[i][j] = AADD(pb[i][j], pd[i][j]); pa[i][j] = AADD(pa[i][j], pb[i][j]); }
 #else
-                            if (pos == 0) pa[i][j] = XMUL(a[i], b[j]);
-                            else pa[i][j] = XFMA(a[i], b[j], pa[i][j]);
+                            if (pos == 0) pa[i][j] = AMUL(a[i], b[j]);
+                            else pa[i][j] = AFMA(a[i], b[j], pa[i][j]);
 #endif
                         }
                     if (pos == 7) {
@@ -317,11 +388,11 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
 #pragma unroll
                         for (int i = 0; i < WINO_TM; ++i)
 #pragma unroll
-                            for (int j = 0; j < WINO_TN; ++j) {
-                                DT cy = pa[i][j];
+                            for (int j = 0; j < NJ; ++j) {
+                                acc_t cy = pa[i][j];
 #pragma unroll
                                 for (int e = 0; e < ZL; ++e)
-                                    if (e < dc) cy = XADD(zs[e][i][j], cy);
+                                    if (e < dc) cy = AADD(zs[e][i][j], cy);
                                 if (c != NCH - 1) {
 #pragma unroll
                                     for (int e = 0; e < ZL; ++e)
@@ -338,10 +409,10 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
 #pragma unroll
                                     for (int i = 0; i < WINO_TM; ++i)
 #pragma unroll
-                                        for (int j = 0; j < WINO_TN; ++j) {
-                                            DT cy = pa[i][j];
+                                        for (int j = 0; j < NJ; ++j) {
+                                            acc_t cy = pa[i][j];
 #pragma unroll
-                                            for (int e = 0; e < L; ++e) cy = XADD(slot[e][i][j], cy);
+                                            for (int e = 0; e < L; ++e) cy = AADD(slot[e][i][j], cy);
                                             slot[L][i][j] = cy;
                                         }
                                 }
@@ -367,7 +438,7 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
 
 #if WINO_SUM == 1 || WINO_SUM == 3
         // fold the occupied slots (set bits of the chunk count), smallest block first
-        DT acc[WINO_TM][WINO_TN];
+        acc_t acc[WINO_TM][NJ];
         {
             const long long Q = Cp / WINO_BK;  // number of stages = counter pushes
             bool have = false;
@@ -377,8 +448,8 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
 #pragma unroll
                     for (int i = 0; i < WINO_TM; ++i)
 #pragma unroll
-                        for (int j = 0; j < WINO_TN; ++j)
-                            acc[i][j] = have ? XADD(slot[L][i][j], acc[i][j]) : slot[L][i][j];
+                        for (int j = 0; j < NJ; ++j)
+                            acc[i][j] = have ? AADD(slot[L][i][j], acc[i][j]) : slot[L][i][j];
                     have = true;
                 }
             }
@@ -396,8 +467,18 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
                 for (int h = 0; h < GN; ++h) {
                     vec_t w4;
                     DT* ww = reinterpret_cast<DT*>(&w4);
+#if WINO_PACK
+#pragma unroll
+                    for (int u = 0; u < VW / 2; ++u) {
+                        float lo, hi;
+                        asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc[i][h * 2 + u]));
+                        ww[2 * u] = lo;
+                        ww[2 * u + 1] = hi;
+                    }
+#else
 #pragma unroll
                     for (int u = 0; u < VW; ++u) ww[u] = acc[i][h * VW + u];
+#endif
                     *reinterpret_cast<vec_t*>(gM + row * Tp + h * (WINO_THN * VW) + tn * VW) = w4;
                 }
             }

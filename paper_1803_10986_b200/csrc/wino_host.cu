@@ -186,6 +186,7 @@ static const char* kContractTemplate =
 struct GemmCfg {
     int tm, tn, thm, thn, bk, stages, maxreg, ku = 0;  // ku: k-steps unrolled per inner loop (0 = bk)
     int noprod = 0;  // 1: no producer warp (last consumer warp to release a stage refills it)
+    int pack = 0;    // 1: packed f32x2 arithmetic (float U/V only)
     int bm() const { return thm * tm; }
     int bn() const { return thn * tn; }
     int threads() const { return thm * thn; }
@@ -223,7 +224,8 @@ struct wino_plan {
            << "\n#define WINO_TM " << gemm.tm << "\n#define WINO_TN " << gemm.tn << "\n#define WINO_THM " << gemm.thm
            << "\n#define WINO_THN " << gemm.thn << "\n#define WINO_BK " << gemm.bk << "\n#define WINO_STAGES "
            << gemm.stages << "\n#define WINO_SUM " << sum_mode() << "\n#define WINO_LEVELS "
-           << (levels > 0 ? levels : 1) << "\n#define WINO_MAXREG " << gemm.maxreg << "\n#define WINO_KU " << (gemm.ku > 0 ? gemm.ku : gemm.bk) << "\n#define WINO_NOPROD " << gemm.noprod << "\n"
+           << (levels > 0 ? levels : 1) << "\n#define WINO_MAXREG " << gemm.maxreg << "\n#define WINO_KU " << (gemm.ku > 0 ? gemm.ku : gemm.bk) << "\n#define WINO_NOPROD " << gemm.noprod
+           << "\n#define WINO_PACK " << (gemm.pack && !dbl ? 1 : 0) << "\n"
            << wino::kContractTemplate;
         mod->source = os.str();
         mod->name = "wino_contract_s" + std::to_string(sum_mode()) + "_L" + std::to_string(levels) + ".cu";
@@ -390,21 +392,23 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
     p->ty.in_double = dbl64;
     p->ty.uv_double = dbl64;
     p->ty.y_double = precision != WINO_FP32;
-    // Tile configs {tm, tn, thm, thn, bk, stages, maxreg} picked by tools/contract_bench.py
-    // sweeps on B200 (profiles/): 4 consumer warps + 1 producer warp per CTA,
-    // so three CTAs (15 warps) fit per SM within the per-SMSP register file.
+    // Tile configs {tm, tn, thm, thn, bk, stages, maxreg, ku, noprod, pack} picked by
+    // tools/contract_bench.py sweeps on B200 (profiles/): 4 consumer warps + 1 producer
+    // warp per CTA, so three CTAs (15 warps) fit per SM within the per-SMSP register
+    // file; float U/V use packed f32x2 arithmetic (FFMA2(a, b, -0) + FADD2 in exact
+    // modes: cfg2 27.4 -> 31.1 TFLOP/s, cfg3 m=6 29.1 -> 33.6, pairwise 25.6 -> 27.7).
     if (contract_mode >= WINO_CONTRACT_TC_BF16)
         p->gemm = {8, 8, 16, 16, 32, 3, 0};  // only the 128/128/32 blocking matters (tc_contract.cu)
     else if (dbl64)
         p->gemm = {4, 4, 8, 16, 16, 4, 0};
     else if (channel_sum == WINO_SUM_PAIRWISE)
-        p->gemm = {4, 4, 8, 16, 32, 4, 168, 8};
+        p->gemm = {4, 4, 8, 16, 32, 4, 168, 8, 0, 1};
     else
-        p->gemm = {8, 8, 16, 8, 16, 4, 0, 8};
+        p->gemm = {8, 8, 16, 8, 16, 4, 0, 16, 0, 1};
     if (const char* env = getenv("WINO_GEMM")) {  // tuning override: tm,tn,thm,thn,bk,stages,maxreg
         wino::GemmCfg g{};
-        const int got = sscanf(env, "%d,%d,%d,%d,%d,%d,%d,%d,%d", &g.tm, &g.tn, &g.thm, &g.thn, &g.bk, &g.stages,
-                               &g.maxreg, &g.ku, &g.noprod);
+        const int got = sscanf(env, "%d,%d,%d,%d,%d,%d,%d,%d,%d,%d", &g.tm, &g.tn, &g.thm, &g.thn, &g.bk,
+                               &g.stages, &g.maxreg, &g.ku, &g.noprod, &g.pack);
         if (got >= 7 && g.bk % 8 == 0 && g.tm % 4 == 0 && g.tn % 4 == 0 && (g.ku == 0 || g.bk % g.ku == 0))
             p->gemm = g;
     }
@@ -604,7 +608,8 @@ int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, con
         per_sm < 1)
         per_sm = 1;
     const long long grid = std::min<long long>(tiles, (long long)per_sm * (sms > 0 ? sms : 148));
-    void* args[] = {(void*)&U, (void*)&V, &M, &Kp, &Tp, &Cp, &n_tiles};
+    unsigned long long nz2 = 0x8000000080000000ull;  // (-0, -0): exact packed products (contract_template.cuh)
+    void* args[] = {(void*)&U, (void*)&V, &M, &Kp, &Tp, &Cp, &n_tiles, &nz2};
     return wino::launch(f, dim3((unsigned)grid, 1, 1), dim3(threads), smem, stream, args, "contract");
 }
 

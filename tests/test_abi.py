@@ -64,20 +64,56 @@ def _sass(cubin: bytes) -> str:
 
 
 FMA = re.compile(r"\b(FFMA2?|DFMA)\b")  # (HFMA2 RZ,RZ is the zeroing idiom)
+FFMA2_LINE = re.compile(r"\bFFMA2\s+([^;]*);")
+
+
+def _fused_ops(sass: str) -> list:
+    """Instructions that would fuse a multiply into a per-thread sum.  FFMA/DFMA
+    always do.  FFMA2 is allowed only with a uniform-register or constant-bank
+    addend: that is the packed exact product fma.rn.f32x2(a, b, -0) ==
+    fl(a*b) of contract_template.cuh (accumulators are per-thread registers,
+    never uniform)."""
+    bad = [m.group(0) for m in re.finditer(r"\b(FFMA|DFMA)\b(?!2)[^;]*;", sass)]
+    for m in FFMA2_LINE.finditer(sass):
+        ops = [o.strip() for o in m.group(1).split(",")]
+        if len(ops) != 4 or not re.match(r"^(UR\d+|c\[0x[0-9a-f]+\]\[0x[0-9a-f]+\])", ops[3]):
+            bad.append(m.group(0))
+    return bad
+
+
+def _pack_tag(pack):
+    return {"tile": None, "pack": "8,8,16,8,16,4,0,8,0,1", "scalar": "8,8,16,8,16,4,0,8,0,0"}[pack]
 
 
 @pytest.mark.parametrize("prec", ["fp32", "mixed", "fp64"])
 @pytest.mark.parametrize("cs", ["linear", "pairwise"])
-def test_sass_gate_exact_kernels_have_no_fma(built, prec, cs):
+@pytest.mark.parametrize("pack", ["tile", "pack", "scalar"])
+def test_sass_gate_exact_kernels_have_no_fma(built, prec, cs, pack, monkeypatch):
     """Exactness needs every product and sum rounded separately: FMUL/FADD
-    (DMUL/DADD), never FFMA/FFMA2/DFMA."""
+    (DMUL/DADD) or the packed exact product FFMA2(a, b, uniform -0), never a
+    multiply fused into a running sum."""
+    if _pack_tag(pack):
+        monkeypatch.setenv("WINO_GEMM", _pack_tag(pack))
     plan = _plan(3, 4, "0,1,-1,1/2,-1/2,inf", prec, cs)
     for which in (0, 1, 2):
         sass = _sass(plan.cubin(which, 128))
-        assert not FMA.search(sass), (which, FMA.search(sass).group(0))
+        bad = _fused_ops(sass)
+        assert not bad, (which, bad[:3])
     contract = _sass(plan.cubin(2, 128))
     assert "UBLKCP" in contract          # cp.async.bulk global->shared (TMA bulk copy)
     assert re.search(r"\bSYNCS\.", contract)  # mbarrier pipeline
+    if pack == "pack" and prec != "fp64":
+        assert "FADD2" in contract and "FFMA2" in contract
+    if pack == "scalar" or prec == "fp64":
+        assert "FFMA2" not in contract
+
+
+def test_sass_gate_rejects_fused_sums():
+    assert _fused_ops("FFMA R1, R2, R3, R4 ;")
+    assert _fused_ops("FFMA2 R16, R25.F32, R32.F32x2.HI_LO, R8.F32x2.HI_LO ;")
+    assert _fused_ops("DFMA R2, R4, R6, R8 ;")
+    assert not _fused_ops("FFMA2 R16, R25.F32, R32.F32x2.HI_LO, UR8.F32x2.HI_LO ;")
+    assert not _fused_ops("FMUL R1, R2, R3 ; FADD2 R4, R6.F32x2.HI_LO, R8.F32x2.HI_LO ; HFMA2 R5, -RZ, RZ, 0, 0 ;")
 
 
 def test_ffma_mode_uses_fma(built):

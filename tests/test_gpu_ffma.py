@@ -1,0 +1,66 @@
+"""FFMA contraction mode (products fused into the running sum, same channel order):
+not bitwise by design.  BASELINE.json's parity bar for it: elementwise within an
+ulp-scaled tolerance of the exact (reference-equal) result, and the same error
+statistics against the fp64 direct convolution to 2 significant digits.
+
+Tolerance metric (written here, reported by bench.py as well):
+    d = |y_ffma - y_exact| / ulp32(s),   s = max(|y_exact|, rms(y_exact of the layer))
+ulp32(s) = 2^(floor(log2 s) - 23).  The rms floor keeps outputs that cancel to
+~0 from turning a sub-ulp absolute difference into an unbounded relative one.
+"""
+import numpy as np
+import pytest
+
+from oracle import wino_oracle as O
+
+pytestmark = pytest.mark.gpu
+W = pytest.importorskip("paper_1803_10986_b200")
+torch = pytest.importorskip("torch")
+
+
+def ulp_scaled(y, ref):
+    ref64 = ref.astype(np.float64)
+    s = np.maximum(np.abs(ref64), np.sqrt(np.mean(ref64 ** 2)))
+    ulp = np.exp2(np.floor(np.log2(s)) - 23)
+    return np.abs(y.astype(np.float64) - ref64) / ulp
+
+
+def rel_l1(y, y64):
+    return float(np.abs(y.astype(np.float64) - y64).sum() / np.abs(y64).sum())
+
+
+CASES = [
+    # r, m, points, N, C, K, H, pad, channel_sum, x_dist
+    (3, 2, "0,1,-1,inf", 4, 128, 64, 28, 1, "linear", "uniform"),
+    (3, 4, "0,1,-1,1/2,-1/2,inf", 2, 64, 64, 56, 1, "linear", "uniform"),
+    (3, 6, "0,-1,1,1/2,-1/2,2,-2,inf", 2, 256, 64, 28, 1, "pairwise", "uniform"),
+    (5, 4, "0,-1,1,1/2,-1/2,2,-2,inf", 2, 512, 32, 14, 2, "pairwise", "uniform01"),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"r{c[0]}m{c[1]}C{c[4]}-{c[8]}")
+def test_ffma_within_ulp_tolerance_and_same_error_stats(case):
+    r, m, pts, N, C, K, H, pad, cs, dist = case
+    ts = W.build_transforms(r, m, W.parse_points(pts))
+    x = O.synthetic((N, C, H, H), 11, 0)
+    if dist == "uniform01":
+        x = (x + np.float32(1)) * np.float32(0.5)
+    w = O.synthetic((K, C, r, r), 11, 1) * np.float32(np.sqrt(2.0 / (r * r * C)))
+    cfg = W.ConvConfig("fp32", "huffman", cs)
+    y_exact = W.conv2d_layer(ts, x, w, cfg, pad=pad)
+    y_ffma = W.conv2d_layer(ts, x, w, cfg, pad=pad, contraction="ffma")
+    d = ulp_scaled(y_ffma, y_exact)
+    y64 = O.layer_direct_fp64(x, w, pad)
+    e_exact, e_ffma = rel_l1(y_exact, y64), rel_l1(y_ffma, y64)
+    own = np.abs(y_exact.astype(np.float64) - y64)          # the reference path's own error
+    dev = np.abs(y_ffma.astype(np.float64) - y_exact)       # FFMA deviation from it
+    print(case[:2], cs, "ulp p50/p99/max", np.percentile(d, 50), np.percentile(d, 99), d.max(),
+          "dev/own p99", np.percentile(dev, 99) / np.percentile(own, 99), "rel", e_exact, e_ffma)
+    # (1) same error statistics vs fp64 to 2 significant digits (5% band)
+    assert f"{e_exact:.1e}" == f"{e_ffma:.1e}" or abs(e_ffma / e_exact - 1) < 0.05, (e_exact, e_ffma)
+    # (2) the FFMA deviation is within the reference's own rounding error
+    assert np.percentile(dev, 99) <= np.percentile(own, 99), (np.percentile(dev, 99), np.percentile(own, 99))
+    assert dev.max() <= 2 * own.max(), (dev.max(), own.max())
+    # (3) ulp-scaled bound: one rounding saved per channel -> random walk ~ sqrt(C) ulps
+    bound = 4.0 * np.sqrt(C / 16.0)
+    assert np.percentile(d, 99) <= bound, (np.percentile(d, 99), bound)

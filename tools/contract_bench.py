@@ -59,7 +59,8 @@ def run(shape, m, r, prec, cs, contraction, variant, reps):
     key = (shape, m, r, prec, cs, contraction)
     same = None
     if key in _REF:
-        same = bool(torch.equal(_REF[key], M))
+        # compare the valid region only (Kp/Tp padding depends on the tile config)
+        same = bool(torch.equal(_REF[key][:, :K, :L.T], M[:, :K, :L.T]))
     else:
         _REF[key] = M.clone()
     return {"same_as_default": same, "variant": variant or "default", "shape": shape, "m": m, "prec": prec, "cs": cs,
