@@ -214,7 +214,8 @@ int wino_mean_f64(int64_t n, const double* v, double* out, void* stream);
  * threads, each running 8 independent chains of `iters` steps of
  * mode 0 FFMA | 1 FMUL+FADD | 2 DFMA | 3 DMUL+DADD (immediate multiplier
  * and addend) | 4 FMUL+FADD with register operands (read from out[2], out[3];
- * the operand form of the exact contraction); flops = 2 per step. */
+ * the operand form of the exact contraction) | 5 packed exact FFMA2(a, m, -0) +
+ * FADD2 | 6 packed FFMA2; flops = 2 per lane step (packed steps carry 2 lanes). */
 int wino_peak_probe(int mode, int blocks, int iters, float* out, void* stream);
 
 /* number of kernels this library has launched in the calling process */

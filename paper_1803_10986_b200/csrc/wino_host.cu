@@ -202,20 +202,65 @@ struct wino_plan {
     bool fused() const { return mode >= WINO_CONTRACT_TCF_BF16; }
     wino::MatProg G, BT, AT;
     wino::GenTypes ty;
-    wino::GemmCfg gemm;
-    wino::Module layer, tile;
+    wino::GemmCfg gemm;                 // cands[0]
+    std::vector<wino::GemmCfg> cands;   // contraction tile configs a layer shape picks from
+    wino::Module layer, tile;           // layer: transforms blocked for cands[0]
     std::mutex mu;
-    std::map<int, std::unique_ptr<wino::Module>> contract;  // key: counter levels
+    std::map<int, std::unique_ptr<wino::Module>> contract;  // key: counter levels * 16 + candidate
+    std::map<int, std::unique_ptr<wino::Module>> layer_x;   // transforms for other (bm, bn) blockings
+
+    // Tile config for a layer shape: the candidate with the least padded work per
+    // persistent wave.  cost = ceil(tiles / slots) * bm * bn * Cp / eff, slots = 148 SMs x 3
+    // co-resident CTAs (a fixed B200 constant, so the layout never depends on which
+    // device answers); ties keep the earlier candidate.
+    static long long rup(long long v, long long q) { return (v + q - 1) / q * q; }
+    int pick(const wino_layer_shape* s) const {
+        if (cands.size() < 2) return 0;
+        const int Ho = s->H + 2 * s->pad - r + 1, Wo = s->W + 2 * s->pad - r + 1;
+        const long long T = (long long)s->N * ((Ho + m - 1) / m) * ((Wo + m - 1) / m);
+        const long long slots = 148 * 3;
+        int best = 0;
+        double best_cost = 0;
+        for (size_t i = 0; i < cands.size(); ++i) {
+            const long long bm = cands[i].bm(), bn = cands[i].bn();
+            const long long tiles = (long long)n * n * ((s->K + bm - 1) / bm) * ((T > 0 ? T : 1) + bn - 1) / bn;
+            // measured per-flop speed of the 4x8 microtile vs 8x8: 0.91 (cfg2 28.3 vs 31.0 TFLOP/s)
+            const double eff = cands[i].tm * cands[i].tn < 64 ? 0.91 : 1.0;
+            const double cost = (double)((tiles + slots - 1) / slots) * bm * bn * rup(s->C, cands[i].bk) / eff;
+            if (i == 0 || cost < best_cost * 0.97) {
+                best = (int)i;
+                best_cost = cost;
+            }
+        }
+        return best;
+    }
+
+    wino::Module* layer_mod(int ci) {
+        if (ci <= 0 || (cands[ci].bm() == gemm.bm() && cands[ci].bn() == gemm.bn())) return &layer;
+        const int key = cands[ci].bm() * 4096 + cands[ci].bn();
+        std::lock_guard<std::mutex> g(mu);
+        auto it = layer_x.find(key);
+        if (it != layer_x.end()) return it->second.get();
+        auto mod = std::make_unique<wino::Module>();
+        mod->name = layer.name.substr(0, layer.name.size() - 3) + "_b" + std::to_string(cands[ci].bm()) + "x" +
+                    std::to_string(cands[ci].bn()) + ".cu";
+        mod->source = wino::gen_layer_source(r, m, G, BT, AT, ty, cands[ci].bm(), cands[ci].bn());
+        wino::Module* raw = mod.get();
+        layer_x[key] = std::move(mod);
+        return raw;
+    }
 
     int sum_mode() const { return (mode == WINO_CONTRACT_FFMA ? 2 : 0) + (chsum == WINO_SUM_PAIRWISE ? 1 : 0); }
 
-    wino::Module* contract_module(long long Cp) {
+    wino::Module* contract_module(long long Cp, int ci = 0) {
+        const wino::GemmCfg& gemm = cands.empty() ? this->gemm : cands[ci];
         int levels = 1;
         const long long Q = Cp / gemm.bk;  // pairwise: the dynamic counter runs over stages
         while ((1LL << levels) <= Q) ++levels;  // bit_length(Q)
         if (chsum != WINO_SUM_PAIRWISE) levels = 0;
         std::lock_guard<std::mutex> g(mu);
-        auto it = contract.find(levels);
+        const int key = levels * 16 + ci;
+        auto it = contract.find(key);
         if (it != contract.end()) return it->second.get();
         auto mod = std::make_unique<wino::Module>();
         std::ostringstream os;
@@ -228,9 +273,10 @@ struct wino_plan {
            << "\n#define WINO_PACK " << (gemm.pack && !dbl ? 1 : 0) << "\n"
            << wino::kContractTemplate;
         mod->source = os.str();
-        mod->name = "wino_contract_s" + std::to_string(sum_mode()) + "_L" + std::to_string(levels) + ".cu";
+        mod->name = "wino_contract_s" + std::to_string(sum_mode()) + "_L" + std::to_string(levels) + "_c" +
+                    std::to_string(ci) + ".cu";
         wino::Module* raw = mod.get();
-        contract[levels] = std::move(mod);
+        contract[key] = std::move(mod);
         return raw;
     }
 };
@@ -260,8 +306,9 @@ int layout_of(const wino_plan* p, const wino_layer_shape* s, wino_layer_layout* 
     if (Ho < 1 || Wo < 1) return wino::fail(WINO_EINVAL, "input smaller than kernel");
     std::memset(L, 0, sizeof *L);
     L->P = p->n * p->n;
-    L->bm = p->gemm.bm();
-    L->bn = p->gemm.bn();
+    const wino::GemmCfg& g = p->cands.empty() ? p->gemm : p->cands[p->pick(s)];
+    L->bm = g.bm();
+    L->bn = g.bn();
     L->Ho = Ho;
     L->Wo = Wo;
     L->th = (Ho + p->m - 1) / p->m;
@@ -269,9 +316,9 @@ int layout_of(const wino_plan* p, const wino_layer_shape* s, wino_layer_layout* 
     L->T = (long long)s->N * L->th * L->tw;
     if (L->T > (1LL << 30) || (long long)s->H * s->W > (1LL << 30) || s->K > (1 << 30))
         return wino::fail(WINO_EUNSUPPORTED, "layer too large for 32-bit tile indexing; split the batch");
-    L->Tp = round_up(L->T > 0 ? L->T : 1, p->gemm.bn());
-    L->Cp = round_up(s->C, p->gemm.bk);
-    L->Kp = round_up(s->K, p->gemm.bm());
+    L->Tp = round_up(L->T > 0 ? L->T : 1, g.bn());
+    L->Cp = round_up(s->C, g.bk);
+    L->Kp = round_up(s->K, g.bm());
     if (p->fused()) {  // wino_tcf blocking: 128 tiles x nk filters x 16 channels
         L->bm = p->nk;
         L->bn = 128;
@@ -405,12 +452,25 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
         p->gemm = {4, 4, 8, 16, 32, 4, 168, 8, 0, 1};
     else
         p->gemm = {8, 8, 16, 8, 16, 4, 0, 16, 0, 1};
+    bool env_gemm = false;
     if (const char* env = getenv("WINO_GEMM")) {  // tuning override: tm,tn,thm,thn,bk,stages,maxreg
         wino::GemmCfg g{};
         const int got = sscanf(env, "%d,%d,%d,%d,%d,%d,%d,%d,%d,%d", &g.tm, &g.tn, &g.thm, &g.thn, &g.bk,
                                &g.stages, &g.maxreg, &g.ku, &g.noprod, &g.pack);
-        if (got >= 7 && g.bk % 8 == 0 && g.tm % 4 == 0 && g.tn % 4 == 0 && (g.ku == 0 || g.bk % g.ku == 0))
+        if (got >= 7 && g.bk % 8 == 0 && g.tm % 4 == 0 && g.tn % 4 == 0 && (g.ku == 0 || g.bk % g.ku == 0)) {
             p->gemm = g;
+            env_gemm = true;
+        }
+    }
+    p->cands = {p->gemm};
+    if (!env_gemm && contract_mode < WINO_CONTRACT_TC_BF16 && !dbl64 && channel_sum != WINO_SUM_PAIRWISE) {
+        // same 8x8 microtile transposed (64 filters x 128 tiles) and a 4x8 microtile
+        // (64 x 64): small K or T layers pad less and fill the persistent wave better
+        p->cands.push_back({8, 8, 8, 16, 16, 4, 0, 16, 0, 1});
+        p->cands.push_back({4, 8, 16, 8, 16, 4, 0, 16, 0, 1});
+        p->cands.push_back({8, 8, 16, 8, 8, 4, 0, 8, 0, 1});  // C <= 8 (first layers): 8-channel stages
+    } else if (!env_gemm && contract_mode < WINO_CONTRACT_TC_BF16 && !dbl64) {
+        p->cands.push_back({4, 4, 8, 16, 8, 4, 168, 8, 0, 1});  // pairwise, C <= 8
     }
     const std::string tag = "r" + std::to_string(r) + "m" + std::to_string(m) + "p" + std::to_string(precision);
     p->layer.name = "wino_layer_" + tag + ".cu";
@@ -466,13 +526,13 @@ int wino_filter_transform(wino_plan* plan, const wino_layer_shape* s, const void
     int K = s->K, C = s->C;
     long long Kp = L.Kp, Cp = L.Cp;
     if (plan->mode >= WINO_CONTRACT_TC_BF16 && (k1_gather() || plan->fused()) && Cp / 8 <= 65535) {
-        if ((rc = plan->layer.function("wino_filter_tcg", &f))) return rc;
+        if ((rc = plan->layer_mod(plan->pick(s))->function("wino_filter_tcg", &f))) return rc;
         void* args[] = {(void*)&w, &U, &K, &C, &Kp, &Cp};
         return wino::launch(f, dim3(cdiv(Kp, 32), (unsigned)(Cp / 8), 1), dim3(256), 0, stream, args,
                             "filter_transform");
     }
     if (plan->fused()) return wino::fail(WINO_EUNSUPPORTED, "filter_transform: grid too large for the fused layout");
-    if ((rc = plan->layer.function("wino_filter_xform", &f))) return rc;
+    if ((rc = plan->layer_mod(plan->pick(s))->function("wino_filter_xform", &f))) return rc;
     int smem = 0;
     const int tb = plan->mode >= WINO_CONTRACT_TC_BF16 ? 64 : xform_block(plan, &smem);
     void* args[] = {(void*)&w, &U, &K, &C, &Kp, &Cp};
@@ -490,7 +550,7 @@ int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, c
     long long T = L.T, Tp = L.Tp, Cp = L.Cp, Kp = L.Kp;
     int smem = 0;
     const bool tc = plan->mode >= WINO_CONTRACT_TC_BF16;
-    if ((rc = plan->layer.function("wino_transforms", &f))) return rc;
+    if ((rc = plan->layer_mod(plan->pick(s))->function("wino_transforms", &f))) return rc;
     const int tb = tc ? 64 : xform_block(plan, &smem);
     if (tc) smem = L.P * 64 * 8 * 2;
     int n_tb = (int)cdiv(Tp, tb), n_kb = (int)cdiv(Kp, tb);
@@ -499,7 +559,7 @@ int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, c
     int cfast = k1_cfast(), Wl = 0;
     if (tc && (k1_gather() || plan->fused()) && Cp / 8 <= 65535 && L.P <= 16 && !k1_no8()) {
         CUfunction fg;
-        if ((rc = plan->layer.function("wino_transforms_tcg8", &fg))) return rc;
+        if ((rc = plan->layer_mod(plan->pick(s))->function("wino_transforms_tcg8", &fg))) return rc;
         float rtw = 1.0f / tw, rth = 1.0f / th;
         int nt128 = (int)cdiv(Tp, 128), nk16 = (int)cdiv(Kp, 16);
         void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &nt128, (void*)&w, &U, &K, &Kp,
@@ -509,7 +569,7 @@ int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, c
     }
     if (tc && (k1_gather() || plan->fused()) && Cp / 8 <= 65535) {
         CUfunction fg;
-        if ((rc = plan->layer.function("wino_transforms_tcg", &fg))) return rc;
+        if ((rc = plan->layer_mod(plan->pick(s))->function("wino_transforms_tcg", &fg))) return rc;
         float rtw = 1.0f / tw, rth = 1.0f / th;
         int nt32 = (int)cdiv(Tp, 32), nk32 = (int)cdiv(Kp, 32);
         void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &nt32, (void*)&w, &U, &K, &Kp,
@@ -519,7 +579,7 @@ int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, c
     }
     if (!tc && k1_gather() && (long long)n_tb + n_kb <= 65535 && Cp <= 65535) {
         CUfunction fg;
-        if ((rc = plan->layer.function("wino_transforms_gather", &fg))) return rc;
+        if ((rc = plan->layer_mod(plan->pick(s))->function("wino_transforms_gather", &fg))) return rc;
         float rtw = 1.0f / tw, rth = 1.0f / th;
         void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &n_tb, (void*)&w, &U, &K, &Kp,
                         &Wl, &rtw, &rth};
@@ -543,7 +603,7 @@ int wino_input_transform(wino_plan* plan, const wino_layer_shape* s, const void*
         const int tb = xform_block(plan, &smem);
         int Wl = 0, n_tb = (int)cdiv(Tp, tb);
         if (n_tb <= 65535 && Cp <= 65535) {
-            if ((rc = plan->layer.function("wino_input_gather", &f))) return rc;
+            if ((rc = plan->layer_mod(plan->pick(s))->function("wino_input_gather", &f))) return rc;
             float rtw = 1.0f / tw, rth = 1.0f / th;
             void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &Wl, &rtw, &rth};
             return wino::launch(f, dim3((unsigned)Cp, (unsigned)n_tb), dim3(tb), 0, stream, args, "input_transform");
@@ -551,21 +611,21 @@ int wino_input_transform(wino_plan* plan, const wino_layer_shape* s, const void*
     }
     if (plan->mode >= WINO_CONTRACT_TC_BF16 && (k1_gather() || plan->fused()) && Cp / 8 <= 65535 && L.P <= 16 &&
         !k1_no8()) {
-        if ((rc = plan->layer.function("wino_input_tcg8", &f))) return rc;
+        if ((rc = plan->layer_mod(plan->pick(s))->function("wino_input_tcg8", &f))) return rc;
         float rtw = 1.0f / tw, rth = 1.0f / th;
         void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &rtw, &rth};
         return wino::launch(f, dim3((unsigned)cdiv(Tp, 128), (unsigned)(Cp / 8)), dim3(128), 0, stream, args,
                             "input_transform");
     }
     if (plan->mode >= WINO_CONTRACT_TC_BF16 && (k1_gather() || plan->fused()) && Cp / 8 <= 65535) {
-        if ((rc = plan->layer.function("wino_input_tcg", &f))) return rc;
+        if ((rc = plan->layer_mod(plan->pick(s))->function("wino_input_tcg", &f))) return rc;
         float rtw = 1.0f / tw, rth = 1.0f / th;
         void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &rtw, &rth};
         return wino::launch(f, dim3((unsigned)cdiv(Tp, 32), (unsigned)(Cp / 8)), dim3(256), 0, stream, args,
                             "input_transform");
     }
     if (plan->fused()) return wino::fail(WINO_EUNSUPPORTED, "input_transform: grid too large for the fused layout");
-    if ((rc = plan->layer.function("wino_input_xform", &f))) return rc;
+    if ((rc = plan->layer_mod(plan->pick(s))->function("wino_input_xform", &f))) return rc;
     void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp};
     if (plan->mode >= WINO_CONTRACT_TC_BF16)
         return wino::launch(f, dim3(cdiv(Tp, 64), (unsigned)(Cp / 8), 1), dim3(64), (unsigned)(L.P * 64 * 16),
@@ -586,10 +646,11 @@ int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, con
     if (plan->mode >= WINO_CONTRACT_TC_BF16)
         return wino::tc_contract_launch(U, V, M, L.Kp, L.Tp, L.Cp, L.P, plan->mode == WINO_CONTRACT_TC_FP16,
                                         stream);
-    wino::Module* mod = plan->contract_module(L.Cp);
+    const int ci = plan->pick(s);
+    wino::Module* mod = plan->contract_module(L.Cp, ci);
     CUfunction f;
     if ((rc = mod->function("wino_contract", &f))) return rc;
-    const wino::GemmCfg& g = plan->gemm;
+    const wino::GemmCfg& g = plan->cands.empty() ? plan->gemm : plan->cands[ci];
     long long Kp = L.Kp, Tp = L.Tp, Cp = L.Cp;
     const long long tiles = (long long)L.P * (Kp / g.bm()) * (Tp / g.bn());
     if (tiles > (1LL << 30)) return wino::fail(WINO_EUNSUPPORTED, "contract: too many tiles");
@@ -623,7 +684,7 @@ int wino_output_transform(wino_plan* plan, const wino_layer_shape* s, const void
     int K = s->K, Ho = L.Ho, Wo = L.Wo, th = L.th, tw = L.tw;
     long long T = L.T, Tp = L.Tp, Kp = L.Kp;
     if (k4_gather() && K <= 65535) {
-        if ((rc = plan->layer.function("wino_output_gather", &f))) return rc;
+        if ((rc = plan->layer_mod(plan->pick(s))->function("wino_output_gather", &f))) return rc;
         float rtw = 1.0f / tw, rth = 1.0f / th;
         void* gargs[] = {(void*)&M, &y, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp, &rtw, &rth};
         return wino::launch(f, dim3(cdiv(T, 128), (unsigned)K, 1), dim3(128), 0, stream, gargs, "output_transform");
@@ -631,14 +692,14 @@ int wino_output_transform(wino_plan* plan, const wino_layer_shape* s, const void
     if (plan->m <= 2) {
         // small output blocks: one thread per (k, tile), M staged per 128 tiles,
         // per-thread m x m stores (rows of m <= 2 values)
-        if ((rc = plan->layer.function("wino_output_flat", &f))) return rc;
+        if ((rc = plan->layer_mod(plan->pick(s))->function("wino_output_flat", &f))) return rc;
         int smem = 0;
         const int tb = xform_block(plan, &smem);
         void* fargs[] = {(void*)&M, &y, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp};
         return wino::launch(f, dim3(cdiv(T, tb), (unsigned)K, 1), dim3(tb), (unsigned)smem, stream, fargs,
                             "output_transform");
     }
-    if ((rc = plan->layer.function("wino_output_xform", &f))) return rc;
+    if ((rc = plan->layer_mod(plan->pick(s))->function("wino_output_xform", &f))) return rc;
     // block = R tile rows of one image x KB output channels (~256 tiles), output
     // band staged in smem (<= 96 KB)
     const int es = L.elem_bytes_y, m = plan->m;
@@ -683,7 +744,7 @@ int wino_contract_output(wino_plan* plan, const wino_layer_shape* s, const void*
     if (((uintptr_t)U | (uintptr_t)V) & 15) return wino::fail(WINO_EINVAL, "contract_output: U, V must be 16-byte aligned");
     if (s->N == 0) return WINO_OK;
     CUfunction f;
-    if ((rc = plan->layer.function("wino_tcf", &f))) return rc;
+    if ((rc = plan->layer_mod(plan->pick(s))->function("wino_tcf", &f))) return rc;
     // must match codegen.cpp emit_tcf_kernel
     const long long P = L.P, NK = plan->nk;
     const long long stb = P * 4096 + P * NK * 32;

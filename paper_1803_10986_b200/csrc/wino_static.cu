@@ -271,7 +271,20 @@ __global__ void mean_kernel(long long n, const double* __restrict__ v, double* _
 
 // ---------------------------------------------------------------- peak probes
 // Arithmetic-throughput probes for the roofline denominators (mode 0: FFMA,
-// 1: FMUL+FADD pairs, 2: DFMA, 3: DMUL+DADD).  8 independent chains per thread.
+// 1: FMUL+FADD pairs, 2: DFMA, 3: DMUL+DADD, 4: FMUL+FADD with register operands,
+// 5: packed exact FFMA2(a, m, -0) + FADD2 -- the contraction's exact form,
+// 6: packed FFMA2).  8 independent chains per thread (packed: 8 f32x2 pairs).
+__device__ __forceinline__ unsigned long long pk_fma(unsigned long long a, unsigned long long b,
+                                                     unsigned long long c) {
+    unsigned long long r;
+    asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ unsigned long long pk_add(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm volatile("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
 __global__ void peak_probe_kernel(int mode, int iters, float seedf, float* out) {
     float a[8];
     double d[8];
@@ -295,6 +308,24 @@ __global__ void peak_probe_kernel(int mode, int iters, float seedf, float* out) 
         for (int it = 0; it < iters; ++it)
 #pragma unroll
             for (int i = 0; i < 8; ++i) a[i] = __fadd_rn(__fmul_rn(a[i], mr), cr);
+    } else if (mode == 5 || mode == 6) {
+        unsigned long long q[8];
+        const unsigned long long m2 = 0x3f7ff9723f7ff972ull;                      // (0.9999f, 0.9999f)
+        const unsigned long long c2 = ((unsigned long long)__float_as_uint(out[3] + c) << 32) |
+                                      __float_as_uint(out[3] + c);
+        const unsigned long long nz = 0x8000000080000000ull | (unsigned long long)__float_as_uint(out[2]);
+        for (int i = 0; i < 8; ++i)
+            q[i] = ((unsigned long long)__float_as_uint(a[i]) << 32) | __float_as_uint(a[i] + 0.5f);
+        if (mode == 5) {
+            for (int it = 0; it < iters; ++it)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) q[i] = pk_add(pk_fma(q[i], m2, nz), c2);
+        } else {
+            for (int it = 0; it < iters; ++it)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) q[i] = pk_fma(q[i], m2, c2);
+        }
+        for (int i = 0; i < 8; ++i) a[i] = __uint_as_float((unsigned)q[i]) + __uint_as_float((unsigned)(q[i] >> 32));
     } else if (mode == 2) {
         for (int it = 0; it < iters; ++it)
 #pragma unroll
@@ -396,7 +427,7 @@ int wino_program_eval(int dtype, const void* ops, int nops, int cols, int64_t co
 
 
 int wino_peak_probe(int mode, int blocks, int iters, float* out, void* stream) {
-    if (mode < 0 || mode > 4 || blocks < 1 || iters < 1) return wino::fail(WINO_EINVAL, "peak_probe: bad arguments");
+    if (mode < 0 || mode > 6 || blocks < 1 || iters < 1) return wino::fail(WINO_EINVAL, "peak_probe: bad arguments");
     peak_probe_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(mode, iters, 1.0f, out);
     return wino::after_launch("peak_probe");
 }
