@@ -307,25 +307,30 @@ static void emit_output_kernel(std::ostringstream& os, int r, int m, const MatPr
           "  }\n}\n";
 }
 
-// K1, gather form with direct stores: thread = one (tile, channel); the
-// alpha x alpha window is gathered from global memory (zero padding fused,
-// unpredicated interior path) and the P values are stored straight from
-// registers -- a warp's store of one p covers 32 consecutive t of the blocked
-// V, one aligned 128-byte line.  Grid (Cp, n_tb [+ n_kb filter rows]).
+// K1, gather form with direct stores: thread = one tile x CPT consecutive
+// channels (the tile index math -- two divisions, padding predicates -- is done
+// once per thread, then a channel loop); the alpha x alpha window is gathered
+// from global memory (zero padding fused, unpredicated interior path) and the P
+// values are stored straight from registers -- a warp's store of one p covers
+// 32 consecutive t of the blocked V, one aligned 128-byte line.
+// Grid (Cp / CPT, n_tb [+ n_kb filter rows]).
 static void emit_input_gather(std::ostringstream& os, int r, int m, const MatProg& BT, const GenTypes& ty, int bn,
                               int TB, int& ctr) {
     const int n = r + m - 1, P = n * n;
     os << "static __device__ __forceinline__ void input_gather_body(const in_t* __restrict__ x, uv_t* __restrict__ V,\n"
           "    int C, int H, int W, int pad, int th, int tw, long long T, long long Tp, long long Cp,\n"
-          "    float rtw, float rth, int t0, int c) {\n"
+          "    float rtw, float rth, int t0, int cb) {\n"
           "  const long long plane = Cp * Tp;\n"
           "  const long long tt = (long long)t0 + threadIdx.x;\n"
        << "  if (tt >= Tp) return;\n"
-       << "  uv_t* op = V + ((tt / " << bn << ") * Cp + c) * " << bn << " + (tt % " << bn << ");\n"
-       << "  if (c >= C || tt >= T) {\n"
-          "    const uv_t z = (c >= C) ? (uv_t)(-0.0) : (uv_t)0;\n"
+       << "  const int c0 = cb * " << gather_cpt() << ";\n"
+       << "  uv_t* op = V + ((tt / " << bn << ") * Cp + c0) * " << bn << " + (tt % " << bn << ");\n"
+       << "  if (tt >= T || c0 >= C) {\n"
+       << "    for (int cc = 0; cc < " << gather_cpt() << "; ++cc, op += " << bn << ") {\n"
+          "      const uv_t z = (c0 + cc >= C) ? (uv_t)(-0.0) : (uv_t)0;\n"
           "#pragma unroll\n"
-       << "    for (int p = 0; p < " << P << "; ++p) op[p * plane] = z;\n"
+       << "      for (int p = 0; p < " << P << "; ++p) op[p * plane] = z;\n"
+          "    }\n"
           "    return;\n"
           "  }\n"
           "  const int g0 = t0 / tw, off0 = t0 - g0 * tw;\n"
@@ -335,14 +340,23 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
           "  const int di = idiv_small(ti0 + k, th, rth);\n"
           "  const int ti = ti0 + k - di * th;\n"
        << "  const int h0 = ti * " << m << " - pad, w0 = tj * " << m << " - pad;\n"
-       << "  const in_t* src = x + ((long long)(img0 + di) * C + c) * ((long long)H * W);\n";
+       << "  const long long HW = (long long)H * W;\n"
+       << "  const in_t* src = x + ((long long)(img0 + di) * C + c0) * HW;\n"
+       << "  const bool interior = h0 >= 0 && w0 >= 0 && h0 + " << n << " <= H && w0 + " << n << " <= W;\n"
+       << "#pragma unroll 1\n"
+       << "  for (int cc = 0; cc < " << gather_cpt() << "; ++cc, src += HW, op += " << bn << ") {\n"
+       << "  if (c0 + cc >= C) {\n"
+          "#pragma unroll\n"
+       << "    for (int p = 0; p < " << P << "; ++p) op[p * plane] = (uv_t)(-0.0);\n"
+          "    continue;\n"
+          "  }\n";
     std::vector<std::vector<std::string>> d(n, std::vector<std::string>(n));
     for (int a = 0; a < n; ++a)
         for (int b = 0; b < n; ++b) {
             d[a][b] = "x" + std::to_string(a) + "_" + std::to_string(b);
             os << "  ct_t " << d[a][b] << ";\n";
         }
-    os << "  if (h0 >= 0 && w0 >= 0 && h0 + " << n << " <= H && w0 + " << n << " <= W) {\n"
+    os << "  if (interior) {\n"
        << "    const in_t* rp = src + h0 * W + w0;\n";
     for (int a = 0; a < n; ++a)
         for (int b = 0; b < n; ++b)
@@ -363,7 +377,7 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
         for (int j = 0; j < n; ++j)
             os << "  op[" << (i * n + j) << " * plane] = " << store_cvt(ty.compute_double, ty.uv_double, v[i][j])
                << ";\n";
-    os << "}\n\n";
+    os << "  }\n}\n\n";
     os << "extern \"C\" __global__ void __launch_bounds__(" << TB << ") wino_input_gather(\n"
           "    const in_t* __restrict__ x, uv_t* __restrict__ V, int C, int H, int W, int pad, int th,\n"
           "    int tw, long long T, long long Tp, long long Cp, int Wl, float rtw, float rth) {\n"
@@ -378,7 +392,9 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
        << "    input_gather_body(x, V, C, H, W, pad, th, tw, T, Tp, Cp, rtw, rth, blockIdx.y * " << TB
        << ", blockIdx.x);\n"
        << "  } else {\n"
-       << "    filter_body(w, U, K, C, Kp, Cp, (blockIdx.y - n_tb) * " << TB << " + threadIdx.x, blockIdx.x);\n"
+       << "    for (int cc = 0; cc < " << gather_cpt() << "; ++cc)\n"
+       << "      filter_body(w, U, K, C, Kp, Cp, (blockIdx.y - n_tb) * " << TB << " + threadIdx.x, blockIdx.x * "
+       << gather_cpt() << " + cc);\n"
           "  }\n"
           "}\n\n";
 }
@@ -388,7 +404,8 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
 // 32 consecutive t: one coalesced 128-byte line), transformed in registers and
 // the m x m block is stored to NCHW y -- as 8/16-byte pairs when m and Wo are
 // even, so a warp's row store covers a contiguous stretch of the output row.
-// Grid (ceil(T / TB), K).
+// Each thread loops over KPT output channels (tile index math done once).
+// Grid (ceil(T / TB), ceil(K / KPT)).
 static void emit_output_gather(std::ostringstream& os, int r, int m, const MatProg& AT, const GenTypes& ty, int TB,
                                int& ctr, const char* mt = "uv_t") {
     const int n = r + m - 1;
@@ -399,27 +416,31 @@ static void emit_output_gather(std::ostringstream& os, int r, int m, const MatPr
        << "  const int t0 = blockIdx.x * " << TB << ";\n"
           "  const int t = t0 + threadIdx.x;\n"
           "  if (t >= T) return;\n"
-          "  const int k = blockIdx.y;\n"
           "  const long long plane = Kp * Tp;\n"
-          "  const " << mt << "* src = Mm + (long long)k * Tp + t;\n";
+          "  const int g0 = t0 / tw, off0 = t0 - g0 * tw;\n"
+          "  const int img0 = g0 / th, ti0 = g0 - img0 * th;\n"
+          "  const int off = off0 + threadIdx.x;\n"
+          "  const int kk = idiv_small(off, tw, rtw), tj = off - kk * tw;\n"
+          "  const int di = idiv_small(ti0 + kk, th, rth);\n"
+          "  const int ti = ti0 + kk - di * th;\n"
+       << "  const int y0 = ti * " << m << ", x0 = tj * " << m << ";\n"
+       << "  const int k0 = blockIdx.y * " << gather_kpt() << ";\n"
+       << "  const long long HoWo = (long long)Ho * Wo;\n"
+       << "  const " << mt << "* src = Mm + (long long)k0 * Tp + t;\n"
+       << "  y_t* dst = y + (((long long)(img0 + di) * K + k0) * Ho + y0) * Wo + x0;\n"
+       << "  const bool full = y0 + " << m << " <= Ho && x0 + " << m << " <= Wo;\n"
+       << "#pragma unroll 1\n"
+       << "  for (int k = k0; k < k0 + " << gather_kpt() << " && k < K; ++k, src += Tp, dst += HoWo) {\n";
     std::vector<std::vector<std::string>> mm(n, std::vector<std::string>(n));
     for (int a = 0; a < n; ++a)
         for (int b = 0; b < n; ++b) {
             mm[a][b] = "m" + std::to_string(a) + "_" + std::to_string(b);
             os << "  const ct_t " << mm[a][b] << " = (ct_t)__ldg(src + " << (a * n + b) << " * plane);\n";
         }
-    os << "  const int g0 = t0 / tw, off0 = t0 - g0 * tw;\n"
-          "  const int img0 = g0 / th, ti0 = g0 - img0 * th;\n"
-          "  const int off = off0 + threadIdx.x;\n"
-          "  const int kk = idiv_small(off, tw, rtw), tj = off - kk * tw;\n"
-          "  const int di = idiv_small(ti0 + kk, th, rth);\n"
-          "  const int ti = ti0 + kk - di * th;\n";
     Emitter em(os, ty.compute_double, ctr);
     auto yv = em.apply2d(AT, mm);
     auto val = [&](int a, int b) { return store_cvt(ty.compute_double, ty.y_double, yv[a][b]); };
-    os << "  const int y0 = ti * " << m << ", x0 = tj * " << m << ";\n"
-       << "  y_t* dst = y + (((long long)(img0 + di) * K + k) * Ho + y0) * Wo + x0;\n"
-       << "  if (y0 + " << m << " <= Ho && x0 + " << m << " <= Wo) {\n";
+    os << "  if (full) {\n";
     if (m % 2 == 0) {
         os << "    if ((Wo & 1) == 0) {\n";
         for (int a = 0; a < m; ++a)
@@ -441,7 +462,7 @@ static void emit_output_gather(std::ostringstream& os, int r, int m, const MatPr
             os << "      if (x0 + " << b << " < Wo) dst[" << a << " * Wo + " << b << "] = " << val(a, b) << ";\n";
         os << "    }\n";
     }
-    os << "  }\n}\n\n";
+    os << "  }\n  }\n}\n\n";
 }
 
 std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,

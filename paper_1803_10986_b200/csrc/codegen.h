@@ -10,6 +10,7 @@
 //     subtraction (a + (-1*x) == a - x bit for bit; (-x) + (-y) == (-x) - y);
 //   * a row with no nonzero coefficient yields +0 (np.zeros_like).
 #pragma once
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -47,5 +48,25 @@ std::string gen_layer_source_tc(int r, int m, const MatProg& G, const MatProg& B
                                 const GenTypes& ty, bool fp16, int fused_nk = 0);
 std::string gen_tile_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
                             const GenTypes& ty);
+
+// Gather transforms: channels per K1 thread / output channels per K4 thread (the
+// tile index math is amortised over them).  Must divide every channel padding
+// (Cp is a multiple of 8).  WINO_CPT / WINO_KPT override (1, 2, 4 or 8).  Default 1:
+// measured on B200 (tools/sweep_xpt.sh) the kernels are bound by loads in flight,
+// not by index math -- cfg2 K1 14.2 / 14.7 / 16.2 us and cfg3 m=6 K4 38.9 / 65.8 /
+// 77.1 us at 1 / 4 / 8 channels per thread.
+inline int env_pow2(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    const int v = e ? std::atoi(e) : dflt;
+    return (v == 1 || v == 2 || v == 4 || v == 8) ? v : dflt;
+}
+inline int gather_cpt() {
+    static const int v = env_pow2("WINO_CPT", 1);
+    return v;
+}
+inline int gather_kpt() {
+    static const int v = env_pow2("WINO_KPT", 1);
+    return v;
+}
 
 }  // namespace wino

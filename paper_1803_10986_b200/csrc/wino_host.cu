@@ -583,7 +583,8 @@ int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, c
         float rtw = 1.0f / tw, rth = 1.0f / th;
         void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &n_tb, (void*)&w, &U, &K, &Kp,
                         &Wl, &rtw, &rth};
-        return wino::launch(fg, dim3((unsigned)Cp, (unsigned)(n_tb + n_kb)), dim3(tb), 0, stream, args, "transforms");
+        return wino::launch(fg, dim3((unsigned)(Cp / wino::gather_cpt()), (unsigned)(n_tb + n_kb)), dim3(tb), 0,
+                            stream, args, "transforms");
     }
     if (plan->fused()) return wino::fail(WINO_EUNSUPPORTED, "transforms: grid too large for the fused layout");
     void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &n_tb, (void*)&w, &U, &K, &Kp, &n_kb, &cfast};
@@ -606,7 +607,8 @@ int wino_input_transform(wino_plan* plan, const wino_layer_shape* s, const void*
             if ((rc = plan->layer_mod(plan->pick(s))->function("wino_input_gather", &f))) return rc;
             float rtw = 1.0f / tw, rth = 1.0f / th;
             void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &Wl, &rtw, &rth};
-            return wino::launch(f, dim3((unsigned)Cp, (unsigned)n_tb), dim3(tb), 0, stream, args, "input_transform");
+            return wino::launch(f, dim3((unsigned)(Cp / wino::gather_cpt()), (unsigned)n_tb), dim3(tb), 0, stream,
+                                args, "input_transform");
         }
     }
     if (plan->mode >= WINO_CONTRACT_TC_BF16 && (k1_gather() || plan->fused()) && Cp / 8 <= 65535 && L.P <= 16 &&
@@ -687,7 +689,8 @@ int wino_output_transform(wino_plan* plan, const wino_layer_shape* s, const void
         if ((rc = plan->layer_mod(plan->pick(s))->function("wino_output_gather", &f))) return rc;
         float rtw = 1.0f / tw, rth = 1.0f / th;
         void* gargs[] = {(void*)&M, &y, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp, &rtw, &rth};
-        return wino::launch(f, dim3(cdiv(T, 128), (unsigned)K, 1), dim3(128), 0, stream, gargs, "output_transform");
+        return wino::launch(f, dim3(cdiv(T, 128), cdiv(K, wino::gather_kpt()), 1), dim3(128), 0, stream, gargs,
+                            "output_transform");
     }
     if (plan->m <= 2) {
         // small output blocks: one thread per (k, tile), M staged per 128 tiles,

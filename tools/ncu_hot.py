@@ -11,7 +11,8 @@ if k:
 out = subprocess.run(cmd, capture_output=True, text=True).stdout
 lines = out.splitlines()
 start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
-rows = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
+end = next((i for i in range(start + 1, len(lines)) if lines[i].startswith('"Kernel Name"')), len(lines))
+rows = list(csv.DictReader(io.StringIO("\n".join(lines[start:end]))))  # first kernel instance
 tot = sum(float(r["Instructions Executed"] or 0) for r in rows)
 samp = sum(float(r["Warp Stall Sampling (All Samples)"] or 0) for r in rows)
 print(f"total inst {tot:.0f}  samples {samp:.0f}  sass lines {len(rows)}")

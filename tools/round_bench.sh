@@ -11,6 +11,9 @@ for m in ffma tc_bf16 tc_fp16; do
   python bench.py --contraction $m --steps 20 --warmup 5 --no-cpu --soak 0.5 > gpurun_out/bench_cfg2_$m.log 2>&1
   python bench.py --config cfg3_m6 --contraction $m --steps 20 --warmup 5 --no-cpu --soak 0.5 > gpurun_out/bench_cfg3_m6_$m.log 2>&1
 done
+for m in tcf_bf16 tcf_fp16; do  # fused K3t+K4 needs alpha^2 <= 32 (cfg2, cfg1)
+  python bench.py --contraction $m --steps 20 --warmup 5 --no-cpu --soak 0.5 > gpurun_out/bench_cfg2_$m.log 2>&1
+done
 python bench.py --config vgg16 --steps 5 --warmup 2 > gpurun_out/bench_vgg16.log 2>&1
 python bench.py --config vgg16 --steps 5 --warmup 2 --contraction tc_bf16 --no-err > gpurun_out/bench_vgg16_tc_bf16.log 2>&1
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.log 2>&1
