@@ -152,3 +152,14 @@ def test_layout_padding_rules(built):
     assert L.u_bytes == 16 * L.Cp * L.Kp * 4 and L.v_bytes == 16 * L.Cp * L.Tp * 4
     with pytest.raises(ValueError):
         plan.layout(1, 1, 2, 2, 1, 0)  # smaller than the kernel
+
+
+def test_layout_picks_per_shape(built):
+    """The picked blocking follows the padded-work model (wino_host.cu pick())."""
+    plan = _plan(3, 6, "0,-1,1,1/2,-1/2,2,-2,inf", "fp32", "linear")
+    L = plan.layout(256, 64, 224, 224, 64, 1)     # VGG-16 layer 2: K = 64 -> 64-row blocks
+    assert (L.bm, L.Kp) == (64, 64)
+    L = plan.layout(256, 3, 224, 224, 64, 1)      # layer 1: C = 3
+    assert L.Cp <= 16
+    L = plan.layout(64, 256, 28, 28, 256, 1)      # cfg3: 128 x 64 tiles
+    assert (L.bm, L.bn) == (128, 64)

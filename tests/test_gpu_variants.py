@@ -5,6 +5,7 @@ once per process) must produce the same bits as the default kernels:
                    also the fallback for grids beyond 65535 tile chunks
   WINO_K4=staged   K4 stages M in smem (flat for m <= 2, banded otherwise)
   WINO_K1TC=4x8    TC K1 with 4 tiles x 8 channels per warp also for P <= 16
+  WINO_CPT/KPT     gather K1 / K4 threads looping over several channels / filters
 
 Each variant runs in a subprocess; its outputs are compared bitwise with the
 default kernels' outputs computed here (exact mode also with the oracle)."""
@@ -56,7 +57,8 @@ def _run_variant(env_extra, tmp_path):
     return np.load(out)
 
 
-@pytest.mark.parametrize("env", [{"WINO_K1": "tile"}, {"WINO_K4": "staged"}, {"WINO_K1TC": "4x8"}],
+@pytest.mark.parametrize("env", [{"WINO_K1": "tile"}, {"WINO_K4": "staged"}, {"WINO_K1TC": "4x8"},
+                                 {"WINO_CPT": "4", "WINO_KPT": "8"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_variant_bits(env, tmp_path):
     got = _run_variant(env, tmp_path)
