@@ -233,7 +233,13 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
 #pragma unroll 1
                 for (int kt = 0; kt < nk; ++kt, ++g) {
                     const int s = g % WINO_STAGES;
-                    if (g >= WINO_STAGES) mbar_wait_sleep(&empty[s], (unsigned)(((g / WINO_STAGES) - 1) & 1));
+                    if (g >= WINO_STAGES) {
+                        mbar_wait_sleep(&empty[s], (unsigned)(((g / WINO_STAGES) - 1) & 1));
+                        // the consumers' generic-proxy reads of this slot (released by their
+                        // mbarrier arrives, acquired above) must be ordered before the
+                        // async-proxy bulk-copy writes that refill it
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    }
                     mbar_expect_tx(&full[s], (unsigned)(WINO_BK * (BM + BN) * sizeof(DT)));
                     bulk_g2s(sU + s * WINO_BK * BM, gU + (long long)kt * WINO_BK * BM, WINO_BK * BM * sizeof(DT),
                              &full[s]);

@@ -206,8 +206,14 @@ class HostPipeline:
         self.graph = graph
         self._graphs, self._seen = {}, set()
         self.ops = [layer_op(ts, cfg, b - a, C, H, W, K, pad, contraction) for a, b in self.bounds]
-        L = self.full.layout
-        self.U = D.torch.empty((L.P, L.Cp, L.Kp), dtype=self.full._uv_dtype(), device="cuda")
+        # U is blocked by the contraction tile the layout picks (wino_host.cu pick());
+        # chunks of a different size may pick another blocking: one U per blocking
+        self.u_key = [(op.layout.bm, op.layout.Kp, op.layout.Cp) for op in self.ops]
+        self.U = {}
+        for key, op in zip(self.u_key, self.ops):
+            if key not in self.U:
+                L = op.layout
+                self.U[key] = (op, D.torch.empty((L.P, L.Cp, L.Kp), dtype=op._uv_dtype(), device="cuda"))
         self.ws = [D.torch.empty((op.layout.v_bytes + op.layout.m_bytes + 512) // 4, dtype=D.torch.float32,
                                  device="cuda") for op in self.ops]
         self.x_dev = D.torch.empty((N, C, H, W), dtype=D._DT[self.full.in_dtype], device="cuda")
@@ -247,9 +253,11 @@ class HostPipeline:
         with torch.cuda.stream(self.s_cmp):
             sc = self.s_cmp.cuda_stream
             self.s_cmp.wait_event(self.ev[0][0])
-            _native.check(lib.wino_filter_transform(self.full.plan.handle, ctypes.byref(self.full.shape),
-                                                    D.ptr(self.w_dev), D.ptr(self.U), sc), "filter_transform")
-            for op, ws, (a, b), (e_in, e_out) in zip(self.ops, self.ws, self.bounds, self.ev):
+            for uop, U in self.U.values():
+                _native.check(lib.wino_filter_transform(uop.plan.handle, ctypes.byref(uop.shape),
+                                                        D.ptr(self.w_dev), D.ptr(U), sc), "filter_transform")
+            for op, key, ws, (a, b), (e_in, e_out) in zip(self.ops, self.u_key, self.ws, self.bounds, self.ev):
+                U = self.U[key][1]
                 self.s_cmp.wait_event(e_in)
                 V = ws
                 M = ws[(op.layout.v_bytes + 255) // 256 * 64:]
@@ -257,10 +265,10 @@ class HostPipeline:
                 sh = ctypes.byref(op.shape)
                 _native.check(lib.wino_input_transform(op.plan.handle, sh, D.ptr(xs), D.ptr(V), sc), "input")
                 if op.fused:
-                    _native.check(lib.wino_contract_output(op.plan.handle, sh, D.ptr(self.U), D.ptr(V), D.ptr(ys),
-                                                           sc), "contract_output")
+                    _native.check(lib.wino_contract_output(op.plan.handle, sh, D.ptr(U), D.ptr(V), D.ptr(ys), sc),
+                                  "contract_output")
                 else:
-                    _native.check(lib.wino_contract(op.plan.handle, sh, D.ptr(self.U), D.ptr(V), D.ptr(M), sc),
+                    _native.check(lib.wino_contract(op.plan.handle, sh, D.ptr(U), D.ptr(V), D.ptr(M), sc),
                                   "contract")
                     _native.check(lib.wino_output_transform(op.plan.handle, sh, D.ptr(M), D.ptr(ys), sc),
                                   "output")
