@@ -329,7 +329,10 @@ def run_gpu(args, cfg):
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
-    e2e_t = float(np.mean(e2e_ms))
+    # median step: a host-side hiccup (page-cache / driver work on the CPU that issues
+    # the copies) can stretch single steps; the mean and every step are reported too
+    e2e_mean = float(np.mean(e2e_ms))
+    e2e_t = float(np.median(e2e_ms))
     if world > 1:
         t = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -415,6 +418,8 @@ def run_gpu(args, cfg):
                 "error_vs_fp64": err,
                 "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": x_np.nbytes + w_np.nbytes,
                         "d2h_bytes_per_step": yh.numel() * yh.element_size(), "ms_per_step": e2e_t,
+                        "timing": "median of the K timed steps (CUDA events on the issuing stream)",
+                        "ms_per_step_mean": e2e_mean, "ms_steps": [round(v, 4) for v in e2e_ms],
                         "api": f"HostPipeline(chunks={args.e2e_chunks}: H2D | K1-K3-K4 | D2H overlapped on "
                                "3 streams, captured once into a CUDA graph and replayed)",
                         "bitwise_equal_to_device_path": e2e_same},

@@ -43,6 +43,8 @@ RANDOM_CASES = [
     (5, 2, "0,-1,1,1/2,-2,inf", 2, 20, 12, 14, 14, 2),
     (3, 3, "0,1,-1,2,-2", 1, 3, 64, 30, 30, 1),
     (2, 3, "0,1,-1,inf", 2, 7, 9, 11, 11, 0),
+    (3, 2, "0,1,-1,inf", 1, 1100, 3, 6, 6, 1),   # deep channel sums: pairwise counter with 6 stage levels
+    (3, 4, "0,1,-1,1/2,-1/2,inf", 1, 2049, 2, 4, 4, 1),  # C = 2^11 + 1: odd tail after 64 full stages
 ]
 
 
