@@ -31,6 +31,7 @@ from .exact_oracle import check_exactness, conv_1d_exact, conv_2d_exact, conv_di
 from .harness import DirectSpec, ErrorReport, compare_reports, measure_error, measure_variants, trial_inputs
 from .layer import HostPipeline, LayerOp, conv2d_layer, direct_layer_f64, layer_error_stats, layer_op
 from .pointsets import curated_points, curated_transform
+from .tensor_io import convolve, load_tensor, save_tensor
 from .transforms import (
     MultCount,
     TransformSet,
