@@ -145,6 +145,12 @@ int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, con
 /* K4: y = A^T M A per (k, tile), crop + NCHW write-back -- engine.py:418-423 */
 int wino_output_transform(wino_plan* plan, const wino_layer_shape* s, const void* M,
                           void* y, void* stream);
+/* K4 with the activation fused (conv stacks, BASELINE config 5; fp32 plans with
+ * an FP32 contraction): act = relu(y) (pool = 0, act [N][K][Ho][Wo]) or the 2x2
+ * max-pool of relu(y) (pool = 1, even m only, act [N][K][Ho/2][Wo/2]); the same
+ * values as wino_output_transform followed by wino_relu_pool, y never stored. */
+int wino_output_transform_act(wino_plan* plan, const wino_layer_shape* s, const void* M,
+                              void* act, int pool, void* stream);
 /* K3 + K4 fused (TCF modes only): y = A^T (sum_c U_p[c] V_p[c]) A straight
  * from the tensor-memory accumulators -- engine.py:415-423 */
 int wino_contract_output(wino_plan* plan, const wino_layer_shape* s, const void* U, const void* V,

@@ -465,6 +465,66 @@ static void emit_output_gather(std::ostringstream& os, int r, int m, const MatPr
     os << "  }\n  }\n}\n\n";
 }
 
+// K4 with the activation fused (conv stacks, BASELINE config 5): the same
+// gather output transform, then ReLU -- and with pool = 1 the 2x2 max-pool, which
+// is local to a tile when m is even (tile origins are even) -- written straight
+// to the activation tensor: the pre-activation y never goes to HBM.  Same
+// expressions as wino_relu_pool (wino_static.cu): v = max(max(q00, q01),
+// max(q10, q11)); out = v > 0 ? v : 0.  fp32 y only.
+static void emit_output_gather_act(std::ostringstream& os, int r, int m, const MatProg& AT, const GenTypes& ty,
+                                   int TB, int& ctr) {
+    const int n = r + m - 1;
+    os << "static __device__ __forceinline__ float wino_relu(float v) { return v > 0.f ? v : 0.f; }\n"
+          "extern \"C\" __global__ void __launch_bounds__(" << TB << ") wino_output_gather_act(\n"
+          "    const uv_t* __restrict__ Mm, float* __restrict__ act, int K, int Ho, int Wo, int th, int tw,\n"
+          "    long long T, long long Tp, long long Kp, float rtw, float rth, int pool) {\n"
+       << "  const int t0 = blockIdx.x * " << TB << ";\n"
+          "  const int t = t0 + threadIdx.x;\n"
+          "  if (t >= T) return;\n"
+          "  const int k = blockIdx.y;\n"
+          "  const long long plane = Kp * Tp;\n"
+          "  const uv_t* src = Mm + (long long)k * Tp + t;\n";
+    std::vector<std::vector<std::string>> mm(n, std::vector<std::string>(n));
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+            mm[a][b] = "m" + std::to_string(a) + "_" + std::to_string(b);
+            os << "  const ct_t " << mm[a][b] << " = (ct_t)__ldg(src + " << (a * n + b) << " * plane);\n";
+        }
+    os << "  const int g0 = t0 / tw, off0 = t0 - g0 * tw;\n"
+          "  const int img0 = g0 / th, ti0 = g0 - img0 * th;\n"
+          "  const int off = off0 + threadIdx.x;\n"
+          "  const int kk = idiv_small(off, tw, rtw), tj = off - kk * tw;\n"
+          "  const int di = idiv_small(ti0 + kk, th, rth);\n"
+          "  const int ti = ti0 + kk - di * th;\n";
+    Emitter em(os, ty.compute_double, ctr);
+    auto yv = em.apply2d(AT, mm);
+    auto val = [&](int a, int b) { return store_cvt(ty.compute_double, false, yv[a][b]); };
+    os << "  const int y0 = ti * " << m << ", x0 = tj * " << m << ";\n"
+          "  if (!pool) {\n"
+          "    float* dst = act + (((long long)(img0 + di) * K + k) * Ho + y0) * Wo + x0;\n";
+    for (int a = 0; a < m; ++a) {
+        os << "    if (y0 + " << a << " < Ho) {\n";
+        for (int b = 0; b < m; ++b)
+            os << "      if (x0 + " << b << " < Wo) dst[" << a << " * Wo + " << b << "] = wino_relu(" << val(a, b)
+               << ");\n";
+        os << "    }\n";
+    }
+    os << "    return;\n  }\n";
+    if (m % 2 == 0) {
+        os << "  const int Hp = Ho >> 1, Wp = Wo >> 1, py0 = y0 >> 1, px0 = x0 >> 1;\n"
+              "  float* dst = act + (((long long)(img0 + di) * K + k) * Hp + py0) * Wp + px0;\n";
+        for (int a = 0; a < m / 2; ++a) {
+            os << "  if (py0 + " << a << " < Hp) {\n";
+            for (int b = 0; b < m / 2; ++b)
+                os << "    if (px0 + " << b << " < Wp) dst[" << a << " * Wp + " << b << "] = wino_relu(fmaxf(fmaxf("
+                   << val(2 * a, 2 * b) << ", " << val(2 * a, 2 * b + 1) << "), fmaxf(" << val(2 * a + 1, 2 * b)
+                   << ", " << val(2 * a + 1, 2 * b + 1) << ")));\n";
+            os << "  }\n";
+        }
+    }
+    os << "}\n\n";
+}
+
 std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
                              const GenTypes& ty, int bm, int bn) {
     const int n = r + m - 1, P = n * n;
@@ -610,6 +670,7 @@ std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, 
         while (tbf > 32 && (long long)P * tbf * es4 > 64 * 1024) tbf /= 2;
         emit_output_flat(os, r, m, AT, ty, tbf, ctr);
         emit_output_gather(os, r, m, AT, ty, 128, ctr);
+        if (!ty.y_double) emit_output_gather_act(os, r, m, AT, ty, 128, ctr);
     }
     return os.str();
 }

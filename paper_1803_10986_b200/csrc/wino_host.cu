@@ -678,6 +678,25 @@ int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, con
     return wino::launch(f, dim3((unsigned)grid, 1, 1), dim3(threads), smem, stream, args, "contract");
 }
 
+int wino_output_transform_act(wino_plan* plan, const wino_layer_shape* s, const void* M, void* act, int pool,
+                              void* stream) {
+    wino_layer_layout L;
+    int rc = layout_of(plan, s, &L);
+    if (rc) return rc;
+    if (plan->mode >= WINO_CONTRACT_TC_BF16 || plan->ty.y_double)
+        return wino::fail(WINO_EUNSUPPORTED, "output_transform_act: fp32 plans with an FP32 contraction only");
+    if (pool != 0 && pool != 1) return wino::fail(WINO_EINVAL, "output_transform_act: pool must be 0 or 1");
+    if (pool && (plan->m & 1)) return wino::fail(WINO_EUNSUPPORTED, "output_transform_act: pooling needs an even m");
+    if (s->K > 65535) return wino::fail(WINO_EUNSUPPORTED, "output_transform_act: K > 65535");
+    CUfunction f;
+    if ((rc = plan->layer_mod(plan->pick(s))->function("wino_output_gather_act", &f))) return rc;
+    int K = s->K, Ho = L.Ho, Wo = L.Wo, th = L.th, tw = L.tw;
+    long long T = L.T, Tp = L.Tp, Kp = L.Kp;
+    float rtw = 1.0f / tw, rth = 1.0f / th;
+    void* args[] = {(void*)&M, &act, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp, &rtw, &rth, &pool};
+    return wino::launch(f, dim3(cdiv(T, 128), (unsigned)K, 1), dim3(128), 0, stream, args, "output_transform_act");
+}
+
 int wino_output_transform(wino_plan* plan, const wino_layer_shape* s, const void* M, void* y, void* stream) {
     wino_layer_layout L;
     int rc = layout_of(plan, s, &L);

@@ -69,30 +69,56 @@ class ConvStack:
         return sum(op.direct_flops for op in self.ops)
 
     @property
-    def kernels_per_forward(self) -> int:
-        return 5 * len(self.ops)
+    def fused_act(self) -> bool:
+        """K4 writes the activation directly (ReLU / 2x2 max-pool fused, y not stored)."""
+        pools = any(pool for _, _, pool in self.layers)
+        return not self.ops[0].tensor_core and (self.ts.n_o % 2 == 0 or not pools)
 
-    def forward(self, x):
-        """x: CUDA f32 tensor (N, C0, H, W) -> activation after the last layer."""
+    @property
+    def kernels_per_forward(self) -> int:
+        return (3 if self.fused_act else 4) * len(self.ops)
+
+    def forward(self, x, keep_conv_out=False):
+        """x: CUDA f32 tensor (N, C0, H, W) -> activation after the last layer.
+
+        Per layer: K2+K1 (one launch), K3, then K4 with ReLU (+ max-pool) fused
+        (wino_output_transform_act) -- bitwise the same activations as K4 followed
+        by wino_relu_pool.  keep_conv_out=True takes the unfused path and keeps
+        every layer's pre-activation output in self.conv_out (layer_errors)."""
         lib = _native.lib()
         s = D.stream_handle()
         cur = x
+        al = lambda v: (v + 255) // 256 * 256
         for i, op in enumerate(self.ops):
-            y = self.conv_out[i]
-            _native.check(lib.wino_conv2d(op.plan.handle, ctypes.byref(op.shape), D.ptr(cur),
-                                          D.ptr(self.weights[i]), D.ptr(y), D.ptr(self.workspace),
-                                          self.workspace.numel(), s), f"layer {i + 1}")
             C, K, h, w, pool = self.shapes[i]
-            _native.check(lib.wino_relu_pool(0, op.N * K, op.layout.Ho, op.layout.Wo, 1 if pool else 0, D.ptr(y),
-                                             D.ptr(self.act[i]), s), "relu_pool")
+            sh = ctypes.byref(op.shape)
+            if keep_conv_out or not self.fused_act:
+                y = self.conv_out[i]
+                _native.check(lib.wino_conv2d(op.plan.handle, sh, D.ptr(cur), D.ptr(self.weights[i]), D.ptr(y),
+                                              D.ptr(self.workspace), self.workspace.numel(), s), f"layer {i + 1}")
+                _native.check(lib.wino_relu_pool(0, op.N * K, op.layout.Ho, op.layout.Wo, 1 if pool else 0,
+                                                 D.ptr(y), D.ptr(self.act[i]), s), "relu_pool")
+            else:
+                L = op.layout
+                U = self.workspace.data_ptr()
+                V = U + al(L.u_bytes)
+                M = V + al(L.v_bytes)
+                _native.check(lib.wino_transforms(op.plan.handle, sh, D.ptr(cur), D.ptr(self.weights[i]),
+                                                  ctypes.c_void_p(U), ctypes.c_void_p(V), s), f"layer {i + 1} K1/K2")
+                _native.check(lib.wino_contract(op.plan.handle, sh, ctypes.c_void_p(U), ctypes.c_void_p(V),
+                                                ctypes.c_void_p(M), s), f"layer {i + 1} K3")
+                _native.check(lib.wino_output_transform_act(op.plan.handle, sh, ctypes.c_void_p(M),
+                                                            D.ptr(self.act[i]), 1 if pool else 0, s),
+                              f"layer {i + 1} K4+act")
             cur = self.act[i]
         return cur
 
     def layer_errors(self, x, images=None):
-        """Per-layer isolated error of the last forward over the first `images`
-        images: (layer, rel_l1, per_point_l1, max_abs) vs fp64 direct conv of the
-        same fp32 input activation."""
+        """Per-layer isolated error over the first `images` images: (layer, rel_l1,
+        per_point_l1, max_abs) vs fp64 direct conv of the same fp32 input
+        activation (runs one unfused forward to keep the pre-activation outputs)."""
         from .layer import direct_layer_f64, layer_error_stats
+        self.forward(x, keep_conv_out=True)
         n = self.N if images is None else min(images, self.N)
         res = []
         inp = x

@@ -23,13 +23,44 @@ def test_small_vgg_like_stack_bitwise():
     st = ConvStack(ts, W.ConvConfig("fp32", "huffman", "pairwise"), layers, N, H)
     st.set_weights(ws)
     xt = torch.from_numpy(x).cuda()
-    out = st.forward(xt).cpu().numpy()
+    assert st.fused_act
+    out = st.forward(xt).cpu().numpy()                       # K4 + ReLU / max-pool fused
     ref_outs, ref = O.stack_forward(trip, x, ws, layers)
+    assert G.same_bits(out, ref)
+    out2 = st.forward(xt, keep_conv_out=True).cpu().numpy()  # unfused: y stored, wino_relu_pool
     for i, y in enumerate(ref_outs):
         assert G.same_bits(st.conv_out[i].cpu().numpy(), y), i
-    assert G.same_bits(out, ref)
+    assert G.same_bits(out2, ref)
     errs = st.layer_errors(xt)
     assert len(errs) == len(layers) and all(e["rel_l1"] < 1e-4 for e in errs)
+
+
+@pytest.mark.parametrize("m,pts", [(4, "0,1,-1,1/2,-1/2,inf"), (3, "0,1,-1,2,-2")])
+def test_fused_activation_matches_relu_pool(m, pts):
+    """wino_output_transform_act == wino_output_transform + wino_relu_pool, bitwise,
+    including partial edge tiles (odd output sizes) and ReLU-only for odd m."""
+    import ctypes
+    from paper_1803_10986_b200 import _native
+    ts = W.build_transforms(3, m, W.parse_points(pts))
+    lib = _native.lib()
+    for (N, C, K, H, Wd) in [(2, 5, 7, 17, 23), (1, 16, 33, 30, 30)]:
+        op = W.layer_op(ts, W.ConvConfig(), N, C, H, Wd, K, 1)
+        x = torch.from_numpy(O.synthetic((N, C, H, Wd), 9, 0)).cuda()
+        w = torch.from_numpy(O.synthetic((K, C, 3, 3), 9, 1)).cuda()
+        U, V = op.filter_transform(w), op.input_transform(x)
+        M = op.contract(U, V)
+        y = op.output_transform(M)
+        s = torch.cuda.current_stream().cuda_stream
+        Ho, Wo = op.layout.Ho, op.layout.Wo
+        for pool in ((0, 1) if m % 2 == 0 else (0,)):
+            shp = (N, K, Ho // 2, Wo // 2) if pool else (N, K, Ho, Wo)
+            want = torch.empty(shp, device="cuda")
+            _native.check(lib.wino_relu_pool(0, N * K, Ho, Wo, pool, _native.as_ptr(y), _native.as_ptr(want), s))
+            got = torch.full(shp, 7.0, device="cuda")
+            _native.check(lib.wino_output_transform_act(op.plan.handle, ctypes.byref(op.shape), _native.as_ptr(M),
+                                                        _native.as_ptr(got), pool, s))
+            torch.cuda.synchronize()
+            assert torch.equal(got.view(torch.int32), want.view(torch.int32)), (N, C, K, H, Wd, pool)
 
 
 def test_vgg16_geometry():
