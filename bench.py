@@ -379,7 +379,7 @@ def run_gpu(args, cfg):
         # exact modes: every MAC is a separately rounded multiply and add (scalar
         # FMUL+FADD or packed FFMA2(a, b, -0)+FADD2): the better of the two probes
         xceil = max(peak["fmul_fadd_tflops"], peak.get("fmul_fadd_packed_tflops", 0.0))
-        roof = {"kernel": "wino_contract", "bound": "fp32", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+        roof = {"kernel": "wino_contract", "bound": "fp32", "bound_note": "FP32 CUDA-core pipe (neither HBM nor tensor cores): the reference rounds every product and sum separately, which tensor-core accumulation cannot reproduce", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
                 "frac": ach / pk, "traffic": traffic_of("wino_contract", args.config, args.contraction),
                 "peak_source": "measured in this run: libwino wino_peak_probe, max of FFMA and packed FFMA2 (8 chains x 148*8 CTAs); "
                                "MEASURED_PEAKS.json has no FP32 figure",
@@ -597,7 +597,7 @@ def vgg_roof(args, ach, peak, share):
                 "peak_source": mp["source"] + " bf16 dense (burst)", "share_of_step": share}
     pk = max(peak["ffma_tflops"], peak.get("ffma2_tflops", 0.0))
     xceil = max(peak["fmul_fadd_tflops"], peak.get("fmul_fadd_packed_tflops", 0.0))
-    return {"kernel": "wino_contract (13 layers)", "bound": "fp32", "achieved": ach, "peak": pk,
+    return {"kernel": "wino_contract (13 layers)", "bound": "fp32", "bound_note": "FP32 CUDA-core pipe (neither HBM nor tensor cores): the reference rounds every product and sum separately, which tensor-core accumulation cannot reproduce", "achieved": ach, "peak": pk,
             "unit": "TFLOP/s", "frac": ach / pk, "traffic": None,
             "peak_source": "measured in this run: libwino wino_peak_probe, max of FFMA and packed FFMA2",
             "exact_ceiling_tflops": xceil, "frac_of_exact_ceiling": ach / xceil, "share_of_step": share}

@@ -356,8 +356,32 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
             d[a][b] = "x" + std::to_string(a) + "_" + std::to_string(b);
             os << "  ct_t " << d[a][b] << ";\n";
         }
-    os << "  if (interior) {\n"
-       << "    const in_t* rp = src + h0 * W + w0;\n";
+    if (m % 2 == 0 && !ty.in_double) {
+        // even m: every window starts at the same parity (w0 = m*tj - pad), so with an
+        // even row length each row of the window is read with 8-byte loads from the
+        // even column at or below w0 -- fewer, fuller load wavefronts than scalar
+        // gathers; the parity branch is warp-uniform.
+        for (int sh = 0; sh < 2; ++sh) {
+            const int nl = (n + sh + 1) / 2;
+            os << "  " << (sh == 0 ? "if" : "else if") << " (interior && (W & 1) == 0 && (pad & 1) == " << sh
+               << " && (reinterpret_cast<size_t>(src) & 7) == 0) {\n"
+               << "    const float2* rp = reinterpret_cast<const float2*>(src + h0 * W + w0 - " << sh << ");\n"
+               << "    const int W2 = W >> 1;\n";
+            for (int a = 0; a < n; ++a) {
+                for (int q = 0; q < nl; ++q)
+                    os << "    const float2 f" << a << "_" << q << " = __ldg(rp + " << a << " * W2 + " << q << ");\n";
+                for (int b = 0; b < n; ++b) {
+                    const int e = b + sh;
+                    os << "    " << d[a][b] << " = (ct_t)f" << a << "_" << e / 2 << (e % 2 ? ".y" : ".x") << ";\n";
+                }
+            }
+            os << "  }\n";
+        }
+        os << "  else if (interior) {\n";
+    } else {
+        os << "  if (interior) {\n";
+    }
+    os << "    const in_t* rp = src + h0 * W + w0;\n";
     for (int a = 0; a < n; ++a)
         for (int b = 0; b < n; ++b)
             os << "    " << d[a][b] << " = (ct_t)__ldg(rp + " << a << " * W + " << b << ");\n";
