@@ -208,6 +208,48 @@ struct wino_plan {
     std::mutex mu;
     std::map<int, std::unique_ptr<wino::Module>> contract;  // key: counter levels * 16 + candidate
     std::map<int, std::unique_ptr<wino::Module>> layer_x;   // transforms for other (bm, bn) blockings
+    std::map<int, wino::DevProgs> dprogs;                     // per device: programs for the tile interpreter
+
+    // Device copies of G / B^T / A^T (postfix ops + row starts), uploaded once per
+    // device on first use by the interpreted tile transforms.
+    int dev_progs(wino::DevProgs* out) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return wino::fail(WINO_ECUDA, "dev_progs: no CUDA device");
+        std::lock_guard<std::mutex> g(mu);
+        auto it = dprogs.find(dev);
+        if (it != dprogs.end()) {
+            *out = it->second;
+            return WINO_OK;
+        }
+        std::vector<wino_op> ops;
+        std::vector<int> rs;
+        size_t off_op[3], off_rs[3];
+        const wino::MatProg* mats[3] = {&G, &BT, &AT};
+        for (int q = 0; q < 3; ++q) {
+            off_op[q] = ops.size();
+            off_rs[q] = rs.size();
+            int pos = 0;
+            for (const auto& row : mats[q]->row) {
+                rs.push_back(pos);
+                ops.insert(ops.end(), row.ops.begin(), row.ops.end());
+                pos += (int)row.ops.size();
+            }
+            rs.push_back(pos);
+        }
+        const size_t ob = ops.size() * sizeof(wino_op), rb = rs.size() * sizeof(int);
+        char* d = nullptr;
+        if (cudaMalloc(&d, ob + rb + 16) != cudaSuccess) return wino::fail(WINO_ECUDA, "dev_progs: cudaMalloc");
+        if (cudaMemcpy(d, ops.data(), ob, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(d + ob, rs.data(), rb, cudaMemcpyHostToDevice) != cudaSuccess)
+            return wino::fail(WINO_ECUDA, "dev_progs: upload");
+        const wino_op* dops = reinterpret_cast<const wino_op*>(d);
+        const int* drs = reinterpret_cast<const int*>(d + ob);
+        wino::DevProgs pg{dops + off_op[0], dops + off_op[1], dops + off_op[2],
+                          drs + off_rs[0], drs + off_rs[1], drs + off_rs[2]};
+        dprogs[dev] = pg;
+        *out = pg;
+        return WINO_OK;
+    }
 
     // Tile config for a layer shape: the candidate with the least padded work per
     // persistent wave.  cost = ceil(tiles / slots) * bm * bn * Cp / eff, slots = 148 SMs x 3
@@ -306,6 +348,7 @@ int layout_of(const wino_plan* p, const wino_layer_shape* s, wino_layer_layout* 
         return wino::fail(WINO_EINVAL, "layer shape: N >= 0, C, K, H, W >= 1, pad >= 0 required");
     const int Ho = s->H + 2 * s->pad - p->r + 1, Wo = s->W + 2 * s->pad - p->r + 1;
     if (Ho < 1 || Wo < 1) return wino::fail(WINO_EINVAL, "input smaller than kernel");
+    if (p->n > 16) return wino::fail(WINO_EUNSUPPORTED, "layer path: alpha = r + m - 1 > 16 is not generated");
     std::memset(L, 0, sizeof *L);
     L->P = p->n * p->n;
     const wino::GemmCfg& g = p->cands.empty() ? p->gemm : p->cands[p->pick(s)];
@@ -384,6 +427,18 @@ bool k1_no8() {  // WINO_K1TC=4x8: use the 4-tiles x 8-channels TC kernel also f
     return v;
 }
 
+// Tile-level API: generated straight-line kernels up to alpha = 10 (NVRTC compile
+// time grows steeply: ~4 s at alpha 10, ~40 s at 14), the program interpreter
+// above that (alpha <= 24) or everywhere with WINO_TILE_INTERP=1.
+bool tile_interp(const wino_plan* p) {
+    static const int force = [] {
+        const char* e = std::getenv("WINO_TILE_INTERP");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (force >= 0) return force > 0 || p->n > 16;
+    return p->n > 10;
+}
+
 bool k1_gather() {
     static const bool v = [] {
         const char* e = std::getenv("WINO_K1");
@@ -413,7 +468,7 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
     if (contract_mode >= WINO_CONTRACT_TC_BF16 && precision == WINO_FP64)
         return wino::fail(WINO_EINVAL, "tensor-core contraction needs fp32 or mixed precision");
     const int n = r + m - 1;
-    if (n > 16) return wino::fail(WINO_EUNSUPPORTED, "alpha = r + m - 1 > 16 is not generated");
+    if (n > 24) return wino::fail(WINO_EUNSUPPORTED, "alpha = r + m - 1 > 24 is not supported");
     auto p = std::make_unique<wino_plan>();
     p->r = r;
     p->m = m;
@@ -484,8 +539,9 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
                           : wino::gen_layer_source(r, m, p->G, p->BT, p->AT, p->ty, p->gemm.bm(), p->gemm.bn());
     p->tile.name = "wino_tile_" + tag + ".cu";
     p->tile.source = wino::gen_tile_source(r, m, p->G, p->BT, p->AT, p->ty);
-    int rc = p->layer.ensure_compiled();
-    if (rc) return rc;
+    // modules are compiled on first use: the tile-level path (measure_error) never
+    // needs the layer kernels, whose straight-line code for large alpha takes
+    // NVRTC minutes
     *out = p.release();
     return WINO_OK;
 }
@@ -794,6 +850,12 @@ int wino_contract_output(wino_plan* plan, const wino_layer_shape* s, const void*
 
 int wino_tile_hadamard2d(wino_plan* plan, int64_t B, int C, const void* h, const void* x, void* z, void* stream) {
     if (!plan || B < 0 || C < 1) return wino::fail(WINO_EINVAL, "tile_hadamard2d: bad arguments");
+    if (tile_interp(plan)) {
+        wino::DevProgs pg;
+        int rc = plan->dev_progs(&pg);
+        return rc ? rc : wino::tile_hadamard_interp_launch(plan->precision, 2, pg, plan->r, plan->n, B * (long long)C,
+                                                           h, x, z, stream);
+    }
     CUfunction f;
     int rc = plan->tile.function("wino_tile_h2d", &f);
     if (rc) return rc;
@@ -804,6 +866,11 @@ int wino_tile_hadamard2d(wino_plan* plan, int64_t B, int C, const void* h, const
 
 int wino_tile_output2d(wino_plan* plan, int64_t B, const void* y, void* out, void* stream) {
     if (!plan || B < 0) return wino::fail(WINO_EINVAL, "tile_output2d: bad arguments");
+    if (tile_interp(plan)) {
+        wino::DevProgs pg;
+        int rc = plan->dev_progs(&pg);
+        return rc ? rc : wino::tile_output_interp_launch(plan->precision, 2, pg, plan->n, plan->m, B, y, out, stream);
+    }
     CUfunction f;
     int rc = plan->tile.function("wino_tile_o2d", &f);
     if (rc) return rc;
@@ -814,6 +881,12 @@ int wino_tile_output2d(wino_plan* plan, int64_t B, const void* y, void* out, voi
 
 int wino_tile_hadamard1d(wino_plan* plan, int64_t B, int C, const void* h, const void* x, void* z, void* stream) {
     if (!plan || B < 0 || C < 1) return wino::fail(WINO_EINVAL, "tile_hadamard1d: bad arguments");
+    if (tile_interp(plan)) {
+        wino::DevProgs pg;
+        int rc = plan->dev_progs(&pg);
+        return rc ? rc : wino::tile_hadamard_interp_launch(plan->precision, 1, pg, plan->r, plan->n, B * (long long)C,
+                                                           h, x, z, stream);
+    }
     CUfunction f;
     int rc = plan->tile.function("wino_tile_h1d", &f);
     if (rc) return rc;
@@ -824,6 +897,11 @@ int wino_tile_hadamard1d(wino_plan* plan, int64_t B, int C, const void* h, const
 
 int wino_tile_output1d(wino_plan* plan, int64_t B, const void* y, void* out, void* stream) {
     if (!plan || B < 0) return wino::fail(WINO_EINVAL, "tile_output1d: bad arguments");
+    if (tile_interp(plan)) {
+        wino::DevProgs pg;
+        int rc = plan->dev_progs(&pg);
+        return rc ? rc : wino::tile_output_interp_launch(plan->precision, 1, pg, plan->n, plan->m, B, y, out, stream);
+    }
     CUfunction f;
     int rc = plan->tile.function("wino_tile_o1d", &f);
     if (rc) return rc;

@@ -13,4 +13,14 @@ void count_launch();
 // K3t: tcgen05 tensor-core contraction (tc_contract.cu)
 int tc_contract_launch(const void* U, const void* V, void* M, long long Kp, long long Tp, long long Cp, int P,
                        int fp16, void* stream);
+// device copies of a plan's row programs (postfix ops + row starts) for the
+// interpreted tile transforms (wino_static.cu)
+struct DevProgs {
+    const wino_op *G, *BT, *AT;
+    const int *Grs, *BTrs, *ATrs;
+};
+int tile_hadamard_interp_launch(int precision, int dims, const DevProgs& pg, int r, int n, long long BC,
+                                const void* h, const void* x, void* z, void* stream);
+int tile_output_interp_launch(int precision, int dims, const DevProgs& pg, int n, int m, long long B, const void* y,
+                              void* out, void* stream);
 }  // namespace wino

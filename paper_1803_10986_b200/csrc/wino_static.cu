@@ -180,6 +180,101 @@ __global__ void program_eval_kernel(const wino_op* __restrict__ ops, int nops, i
     out[i] = nops ? st[0] : (T)0;
 }
 
+// ---------------------------------------------------------------- interpreted tile transforms
+// The tile-level drop-in API (hadamard_1d/2d, output_1d/2d) for any alpha
+// without generated code: each row program (postfix LEAF/ADD ops, the plan's
+// rounded coefficients) is interpreted.  LEAF = fl(c * x), ADD = fl(a + b) --
+// literally the reference's per-ufunc rounding (engine.py:191-232); the
+// generated kernels apply the exact rewrites c = +-1 -> +-x, which give the
+// same bits.  2D = left pass (rows of M against columns of X) then right pass
+// (rows of the result against rows of M), as the generated code.
+constexpr int kInterpMaxN = 24;
+constexpr int kInterpStack = 32;
+
+template <typename CT>
+__device__ CT eval_row(const wino_op* __restrict__ ops, int b, int e, const CT* v, int stride) {
+    CT st[kInterpStack];
+    int sp = 0;
+    for (int k = b; k < e; ++k) {
+        const wino_op op = ops[k];
+        if (op.kind == WINO_OP_LEAF) {
+            st[sp++] = rmul((CT)op.coeff, v[op.col * stride]);
+        } else {
+            const CT y = st[--sp];
+            const CT x0 = st[--sp];
+            st[sp++] = radd(x0, y);
+        }
+    }
+    return e > b ? st[0] : (CT)0;
+}
+
+template <typename T> __device__ __forceinline__ float narrow_f(T v);
+template <> __device__ __forceinline__ float narrow_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ float narrow_f<double>(double v) { return __double2float_rn(v); }
+
+// z[i][p] = (G h G^T)[p] * (B^T x B)[p] (dims 2) or (G h)[p] * (B^T x)[p] (dims 1);
+// IT inputs, CT transform arithmetic, UT product type (float: narrowed, rounded fp32 product)
+template <typename IT, typename CT, typename UT>
+__global__ void tile_hadamard_interp(int dims, wino::DevProgs pg, int r, int n, const IT* __restrict__ h,
+                                     const IT* __restrict__ x, UT* __restrict__ z, long long BC) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= BC) return;
+    CT a[kInterpMaxN * kInterpMaxN], t[kInterpMaxN * kInterpMaxN], u[kInterpMaxN * kInterpMaxN];
+    if (dims == 1) {
+        const IT* hs = h + i * r;
+        const IT* xs = x + i * n;
+        for (int c = 0; c < r; ++c) a[c] = (CT)hs[c];
+        for (int c = 0; c < n; ++c) t[c] = (CT)xs[c];
+        for (int p = 0; p < n; ++p) {
+            const CT uu = eval_row(pg.G, pg.Grs[p], pg.Grs[p + 1], a, 1);
+            const CT vv = eval_row(pg.BT, pg.BTrs[p], pg.BTrs[p + 1], t, 1);
+            if (sizeof(UT) == 4)
+                z[i * n + p] = (UT)__fmul_rn(narrow_f(uu), narrow_f(vv));
+            else
+                z[i * n + p] = (UT)rmul((double)uu, (double)vv);
+        }
+        return;
+    }
+    const IT* hs = h + i * r * r;
+    const IT* xs = x + i * n * n;
+    for (int c = 0; c < r * r; ++c) a[c] = (CT)hs[c];
+    for (int q = 0; q < n; ++q)          // G h: n x r
+        for (int j = 0; j < r; ++j) t[q * r + j] = eval_row(pg.G, pg.Grs[q], pg.Grs[q + 1], a + j, r);
+    for (int q = 0; q < n; ++q)          // (G h) G^T: n x n
+        for (int k = 0; k < n; ++k) u[q * n + k] = eval_row(pg.G, pg.Grs[k], pg.Grs[k + 1], t + q * r, 1);
+    for (int c = 0; c < n * n; ++c) a[c] = (CT)xs[c];
+    for (int q = 0; q < n; ++q)          // B^T x
+        for (int j = 0; j < n; ++j) t[q * n + j] = eval_row(pg.BT, pg.BTrs[q], pg.BTrs[q + 1], a + j, n);
+    for (int q = 0; q < n; ++q)          // (B^T x) B, times U
+        for (int k = 0; k < n; ++k) {
+            const CT vv = eval_row(pg.BT, pg.BTrs[k], pg.BTrs[k + 1], t + q * n, 1);
+            const CT uu = u[q * n + k];
+            if (sizeof(UT) == 4)
+                z[i * n * n + q * n + k] = (UT)__fmul_rn(narrow_f(uu), narrow_f(vv));
+            else
+                z[i * n * n + q * n + k] = (UT)rmul((double)uu, (double)vv);
+        }
+}
+
+// out[i] = A^T y A (dims 2) or A^T y (dims 1); UT inputs widened to CT, YT outputs
+template <typename UT, typename CT, typename YT>
+__global__ void tile_output_interp(int dims, wino::DevProgs pg, int n, int m, const UT* __restrict__ y,
+                                   YT* __restrict__ out, long long B) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B) return;
+    CT a[kInterpMaxN * kInterpMaxN], t[kInterpMaxN * kInterpMaxN];
+    if (dims == 1) {
+        for (int c = 0; c < n; ++c) a[c] = (CT)y[i * n + c];
+        for (int q = 0; q < m; ++q) out[i * m + q] = (YT)eval_row(pg.AT, pg.ATrs[q], pg.ATrs[q + 1], a, 1);
+        return;
+    }
+    for (int c = 0; c < n * n; ++c) a[c] = (CT)y[i * n * n + c];
+    for (int q = 0; q < m; ++q)
+        for (int j = 0; j < n; ++j) t[q * n + j] = eval_row(pg.AT, pg.ATrs[q], pg.ATrs[q + 1], a + j, n);
+    for (int q = 0; q < m; ++q)
+        for (int k = 0; k < m; ++k) out[i * m * m + q * m + k] = (YT)eval_row(pg.AT, pg.ATrs[k], pg.ATrs[k + 1], t + q * n, 1);
+}
+
 // ---------------------------------------------------------------- Philox trial inputs
 // one thread per (trial, 8-float block of the trial's stream)
 __global__ void trial_inputs_kernel(uint64_t seed, long long t0, long long B, long long fh, long long fx,
@@ -367,6 +462,42 @@ __global__ void relu_pool_kernel(long long planes, int H, int W, int pool, const
 inline unsigned blocks_for(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
+
+namespace wino {
+// precision: 0 fp32, 1 fp64, 2 mixed (WINO_FP32 / WINO_FP64 / WINO_MIXED)
+int tile_hadamard_interp_launch(int precision, int dims, const DevProgs& pg, int r, int n, long long BC,
+                                const void* h, const void* x, void* z, void* stream) {
+    if (n > kInterpMaxN || r > n) return fail(WINO_EUNSUPPORTED, "interpreted tile transforms: alpha > 24");
+    if (BC == 0) return WINO_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const unsigned g = blocks_for(BC, 64);
+    if (precision == WINO_FP64)
+        tile_hadamard_interp<double, double, double><<<g, 64, 0, s>>>(dims, pg, r, n, (const double*)h,
+                                                                     (const double*)x, (double*)z, BC);
+    else if (precision == WINO_MIXED)
+        tile_hadamard_interp<float, double, float><<<g, 64, 0, s>>>(dims, pg, r, n, (const float*)h,
+                                                                   (const float*)x, (float*)z, BC);
+    else
+        tile_hadamard_interp<float, float, float><<<g, 64, 0, s>>>(dims, pg, r, n, (const float*)h, (const float*)x,
+                                                                  (float*)z, BC);
+    return after_launch("tile_hadamard_interp");
+}
+
+int tile_output_interp_launch(int precision, int dims, const DevProgs& pg, int n, int m, long long B, const void* y,
+                              void* out, void* stream) {
+    if (n > kInterpMaxN) return fail(WINO_EUNSUPPORTED, "interpreted tile transforms: alpha > 24");
+    if (B == 0) return WINO_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const unsigned g = blocks_for(B, 64);
+    if (precision == WINO_FP64)
+        tile_output_interp<double, double, double><<<g, 64, 0, s>>>(dims, pg, n, m, (const double*)y, (double*)out, B);
+    else if (precision == WINO_MIXED)
+        tile_output_interp<float, double, double><<<g, 64, 0, s>>>(dims, pg, n, m, (const float*)y, (double*)out, B);
+    else
+        tile_output_interp<float, float, float><<<g, 64, 0, s>>>(dims, pg, n, m, (const float*)y, (float*)out, B);
+    return after_launch("tile_output_interp");
+}
+}  // namespace wino
 
 // ============================================================== C-ABI launchers
 extern "C" {

@@ -72,3 +72,17 @@ def test_variant_bits(env, tmp_path):
         trip = O.Triple.from_points(r, m, pts)
         oracle = O.layer_conv2d(trip, x, w, pad, "fp32", "huffman", "linear")
         assert np.array_equal(got[f"{i}/exact"].view(np.uint32), oracle.view(np.uint32)), (env, i)
+
+
+def test_interpreted_tile_transforms_pass_the_tile_goldens():
+    """WINO_TILE_INTERP=1: the tile-level API through the program interpreter
+    (used for alpha > 10) reproduces every tile golden of test_gpu_tile.py --
+    z and y bits of hadamard_2d / output_2d / conv_2d / conv_1d, and the
+    reference's measure_error values repr for repr."""
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, WINO_TILE_INTERP="1")
+    env["PYTHONPATH"] = os.pathsep.join([os.path.dirname(here), env.get("PYTHONPATH", "")])
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_tile.py"), "-m", "gpu", "-q",
+                        "-x", "-k", "golden"], env=env, cwd=os.path.dirname(here), capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:]
