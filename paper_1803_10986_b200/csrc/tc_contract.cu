@@ -19,6 +19,7 @@
 //               the smem stage / publishes the finished accumulator
 //   warps 2-5   epilogue: tcgen05.ld TMEM -> registers -> M (fp32) while the
 //               next tile accumulates into the other TMEM buffer
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -108,11 +109,18 @@ __device__ __forceinline__ uint32_t pack2(float a, float b, int fp16) {
 // so a (tile, 32-channel stage) operand is one contiguous 8 KB block.
 constexpr int kOpStage = TBK * TBM * 2;  // bytes of one operand stage (A or B)
 constexpr int OSTAGES = 6;
+// epilogue staging: per epilogue warp, 2 buffers of 32 rows x 32 fp32 columns with a
+// 144-byte row pitch (16-byte aligned rows for the bulk copies; STS.128 at 4
+// wavefronts per warp instead of 32-way bank conflicts at a 128-byte pitch)
+constexpr int kStagePitch = 36;                                  // floats per staged row
+constexpr int kStageBytes = 32 * kStagePitch * 4;                // one 32x32 block
+constexpr int kEpiBytes = 4 * 2 * kStageBytes;                   // 4 warps x 2 buffers
+constexpr int kEpiOffset = OSTAGES * 2 * kOpStage + 256;         // after operands + barriers
 
 __global__ void __launch_bounds__(192, 1) tc_contract_kernel(const unsigned short* __restrict__ U,
                                                              const unsigned short* __restrict__ V,
                                                              float* __restrict__ M, long long Kp, long long Tp,
-                                                             long long Cp, int n_tiles, int fp16) {
+                                                             long long Cp, int n_tiles, int fp16, int tc_epi_mode) {
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned char* ops = smem;                                   // [OSTAGES][A | B]
     u64* bars = reinterpret_cast<u64*>(ops + OSTAGES * 2 * kOpStage);
@@ -199,6 +207,8 @@ __global__ void __launch_bounds__(192, 1) tc_contract_kernel(const unsigned shor
         // TMEM lane quarter (warp % 4) = rows k of this warp
         const int q4 = warp & 3;
         int it = 0;
+        unsigned eb = 0;  // staged blocks issued by this lane (buffer = eb & 1)
+        const int epi = tc_epi_mode;
         for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
             const int tb = tile % n_tb, rest = tile / n_tb, kb = rest % n_kb;
             const long long p = rest / n_kb;
@@ -207,6 +217,11 @@ __global__ void __launch_bounds__(192, 1) tc_contract_kernel(const unsigned shor
             tc_fence_after();
             const long long krow = (long long)kb * TBM + q4 * 32 + lane;
             float* dst = M + (p * Kp + krow) * Tp + (long long)tb * TBN;
+            // Each lane owns one row k: the 32 values of a tcgen05.ld go to its staged row
+            // in smem, then one 128-byte cp.async.bulk per row writes a full line of M
+            // (TMA engine) -- per-lane 16-byte global stores scattered over 32 rows
+            // throttled the LSU (ncu: lg_throttle the top stall).
+            float* stage = reinterpret_cast<float*>(smem + kEpiOffset) + (size_t)q4 * 2 * 32 * kStagePitch;
 #pragma unroll 1
             for (int j = 0; j < TBN / 32; ++j) {
                 uint32_t r[32];
@@ -222,15 +237,46 @@ __global__ void __launch_bounds__(192, 1) tc_contract_kernel(const unsigned shor
                       "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
                     : "r"(taddr));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (epi == 0) {  // direct: lane-per-row 16-byte stores
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    *reinterpret_cast<uint4*>(dst + j * 32 + q * 4) =
-                        make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+                    for (int q = 0; q < 8; ++q)
+                        *reinterpret_cast<uint4*>(dst + j * 32 + q * 4) =
+                            make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+                } else if (epi == 1) {  // staged row + one 128-byte bulk copy per lane
+                    float* row = stage + ((eb & 1) * 32 + lane) * kStagePitch;
+                    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        *reinterpret_cast<uint4*>(row + q * 4) =
+                            make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 128;" ::"l"(dst + j * 32),
+                                 "r"((uint32_t)__cvta_generic_to_shared(row))
+                                 : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                } else {  // staged, read back 4 rows x 128 B per instruction: full-line stores
+                    float* blk = stage + (eb & 1) * 32 * kStagePitch;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        *reinterpret_cast<uint4*>(blk + lane * kStagePitch + q * 4) =
+                            make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+                    __syncwarp();
+                    const int rsub = lane >> 3, c4 = (lane & 7) * 4;
+                    float* gbase = M + (p * Kp + (long long)kb * TBM + q4 * 32) * Tp + (long long)tb * TBN + j * 32 + c4;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int rr = i * 4 + rsub;
+                        *reinterpret_cast<uint4*>(gbase + (long long)rr * Tp) =
+                            *reinterpret_cast<const uint4*>(blk + rr * kStagePitch + c4);
+                    }
+                }
+                ++eb;
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) bar_arrive(&acc_empty[ab]);
         }
+        if (epi == 1) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // M written before exit
     }
     tc_fence_before();
     __syncthreads();
@@ -244,12 +290,23 @@ __global__ void __launch_bounds__(192, 1) tc_contract_kernel(const unsigned shor
 
 namespace wino {
 
+// epilogue store form (WINO_TC_EPI): 0 direct per-lane stores, 1 per-row bulk copies,
+// 2 (default) staged in smem and stored as full 128-byte lines
+static int epi_mode() {
+    static const int v = [] {
+        const char* e = std::getenv("WINO_TC_EPI");
+        const int x = e ? std::atoi(e) : 2;
+        return (x >= 0 && x <= 2) ? x : 2;
+    }();
+    return v;
+}
+
 int tc_contract_launch(const void* U, const void* V, void* M, long long Kp, long long Tp, long long Cp, int P,
                        int fp16, void* stream) {
     if (Kp % TBM || Tp % TBN || Cp % TBK) return fail(WINO_EINVAL, "tc_contract: layout not padded to 128/128/32");
     const long long tiles = (long long)P * (Kp / TBM) * (Tp / TBN);
     if (tiles > (1LL << 30)) return fail(WINO_EUNSUPPORTED, "tc_contract: too many tiles");
-    const size_t smem = (size_t)OSTAGES * 2 * kOpStage + 256;
+    const size_t smem = (size_t)kEpiOffset + kEpiBytes;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(tc_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -261,7 +318,7 @@ int tc_contract_launch(const void* U, const void* V, void* M, long long Kp, long
     const int grid = (int)(tiles < sms ? tiles : sms);
     tc_contract_kernel<<<grid, 192, smem, (cudaStream_t)stream>>>((const unsigned short*)U,
                                                                  (const unsigned short*)V, (float*)M, Kp, Tp, Cp,
-                                                                 (int)tiles, fp16);
+                                                                 (int)tiles, fp16, epi_mode());
     return after_launch("tc_contract");
 }
 
