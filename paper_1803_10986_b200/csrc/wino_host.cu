@@ -210,6 +210,16 @@ struct wino_plan {
     std::map<int, std::unique_ptr<wino::Module>> layer_x;   // transforms for other (bm, bn) blockings
     std::map<int, wino::DevProgs> dprogs;                     // per device: programs for the tile interpreter
 
+    ~wino_plan() {  // device program copies (errors ignored: the context may already be gone at exit)
+        int cur = 0;
+        if (dprogs.empty() || cudaGetDevice(&cur) != cudaSuccess) return;
+        for (auto& kv : dprogs) {
+            if (cudaSetDevice(kv.first) == cudaSuccess) cudaFree(const_cast<wino_op*>(kv.second.G));
+        }
+        cudaSetDevice(cur);
+        cudaGetLastError();
+    }
+
     // Device copies of G / B^T / A^T (postfix ops + row starts), uploaded once per
     // device on first use by the interpreted tile transforms.
     int dev_progs(wino::DevProgs* out) {
