@@ -275,8 +275,8 @@ struct wino_plan {
         double best_cost = 0;
         for (size_t i = 0; i < cands.size(); ++i) {
             const long long bm = cands[i].bm(), bn = cands[i].bn();
-            const long long tiles = (long long)n * n * ((s->K + bm - 1) / bm) * ((T > 0 ? T : 1) + bn - 1) / bn;
-            // measured per-flop speed of the 4x8 microtile vs 8x8: 0.91 (cfg2 28.3 vs 31.0 TFLOP/s)
+            const long long tiles = (long long)n * n * ((s->K + bm - 1) / bm) * (((T > 0 ? T : 1) + bn - 1) / bn);
+            // measured per-flop speed of the 4x8 / 4x4 microtiles vs 8x8: 0.91 / 0.92 (cfg2, cfg3)
             const double eff = cands[i].tm * cands[i].tn < 64 ? 0.91 : 1.0;
             const double cost = (double)((tiles + slots - 1) / slots) * bm * bn * rup(s->C, cands[i].bk) / eff;
             if (i == 0 || cost < best_cost * 0.97) {
@@ -535,6 +535,7 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
         // (64 x 64): small K or T layers pad less and fill the persistent wave better
         p->cands.push_back({8, 8, 8, 16, 16, 4, 0, 16, 0, 1});
         p->cands.push_back({4, 8, 16, 8, 16, 4, 0, 16, 0, 1});
+        p->cands.push_back({4, 4, 16, 8, 16, 4, 0, 16, 0, 1});  // 64 x 32 (4x4): small layers (cfg1 20.4 -> 22.3)
         p->cands.push_back({8, 8, 16, 8, 8, 4, 0, 8, 0, 1});  // C <= 8 (first layers): 8-channel stages
     } else if (!env_gemm && contract_mode < WINO_CONTRACT_TC_BF16 && !dbl64) {
         p->cands.push_back({4, 4, 16, 16, 8, 4, 168, 8, 0, 1});  // pairwise, C <= 8

@@ -15,6 +15,7 @@ W = pytest.importorskip("paper_1803_10986_b200")
 LINEAR = ["8,8,16,8,16,4,0,16,0,1",    # 128 x 64 (default)
           "8,8,8,16,16,4,0,16,0,1",    # 64 x 128
           "4,8,16,8,16,4,0,16,0,1",    # 64 x 64
+          "4,4,16,8,16,4,0,16,0,1",    # 64 x 32
           "8,8,16,8,8,4,0,8,0,1",      # 8-channel stages (C <= 8)
           "8,8,16,8,16,4,0,8,0,0"]     # scalar FMUL + FADD
 PAIRWISE = ["4,4,16,16,32,3,168,8,0,1",  # default: 8 consumer warps, 64 x 64
