@@ -295,12 +295,24 @@ def layer_op(ts, cfg, N, C, H, W, K, pad, contraction="exact") -> LayerOp:
 
 
 def conv2d_layer(ts: TransformSet, x, w, cfg: ConvConfig = ConvConfig(), pad: int = 0,
-                 contraction: str = "exact"):
+                 contraction: str = "exact", layout: str = "NCHW"):
     """Winograd F(m x m, r x r) convolution layer (stride 1, zero padding `pad`).
 
     x (N, C, H, W), w (K, C, r, r) -> y (N, K, Ho, Wo): numpy in -> numpy out
     (host<->device copies included), CUDA tensors in -> CUDA tensor out.
-    Output dtype f32 in fp32 mode, f64 in mixed / fp64 mode (reference engine.py:378-387)."""
+    Output dtype f32 in fp32 mode, f64 in mixed / fp64 mode (reference engine.py:378-387).
+    layout="NHWC": x (N, H, W, C) -> y (N, Ho, Wo, K); the layer kernels run on NCHW,
+    so the activations are permuted on the device (same values, bit for bit)."""
+    if layout not in ("NCHW", "NHWC"):
+        raise ValueError("layout must be 'NCHW' or 'NHWC'")
+    if layout == "NHWC":
+        if len(D.shape_of(x)) != 4:
+            raise ValueError("x must be (N, H, W, C)")
+        dt = np.float64 if cfg.precision == "fp64" else np.float32
+        xt, hx = D.to_device(x, dt)
+        wt, hw = D.to_device(w, dt)
+        y = conv2d_layer(ts, xt.permute(0, 3, 1, 2).contiguous(), wt, cfg, pad, contraction)
+        return D.finish(y.permute(0, 2, 3, 1).contiguous(), hx or hw)
     xs, wsh = tuple(D.shape_of(x)), tuple(D.shape_of(w))
     if len(xs) != 4 or len(wsh) != 4:
         raise ValueError("x must be (N, C, H, W) and w (K, C, r, r)")

@@ -126,3 +126,20 @@ def test_layer_validation_errors():
         W.conv2d_layer(ts, np.zeros((1, 2, 5, 5), np.float32), np.zeros((1, 2, 5, 5), np.float32))
     with pytest.raises(ValueError):
         W.conv2d_layer(ts, np.zeros((1, 2, 2, 2), np.float32), np.zeros((1, 2, 3, 3), np.float32), pad=0)
+
+
+@pytest.mark.parametrize("mode", [("fp32", "huffman", "linear"), ("mixed", "huffman", "pairwise")],
+                         ids=lambda m: "-".join(m))
+def test_layer_nhwc_layout(mode):
+    """layout='NHWC' gives the NCHW results transposed, bit for bit."""
+    pts = "0,1,-1,1/2,-1/2,inf"
+    ts = W.build_transforms(3, 4, W.parse_points(pts))
+    trip = O.Triple.from_points(3, 4, pts)
+    x = O.synthetic((2, 9, 14, 11), 4, 0)
+    w = O.synthetic((5, 9, 3, 3), 4, 1)
+    want = O.layer_conv2d(trip, x, w, 1, *mode)
+    y = W.conv2d_layer(ts, np.ascontiguousarray(x.transpose(0, 2, 3, 1)), w, W.ConvConfig(*mode), pad=1,
+                       layout="NHWC")
+    assert G.same_bits(np.ascontiguousarray(y.transpose(0, 3, 1, 2)), want)
+    with pytest.raises(ValueError):
+        W.conv2d_layer(ts, x, w, W.ConvConfig(*mode), pad=1, layout="CHWN")
