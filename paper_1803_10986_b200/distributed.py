@@ -32,6 +32,31 @@ def shard_range(total: int, rank: int, size: int) -> tuple[int, int]:
     return start, start + base + (1 if rank < extra else 0)
 
 
+def layer_shard(N: int, K: int, rank: int, size: int, by: str = "batch") -> tuple[slice, slice]:
+    """(image slice, filter slice) of a layer a rank computes.  "batch": a
+    contiguous block of images, all filters; "filters": all images, a contiguous
+    block of output channels (for batches smaller than the GPU count).  Either
+    way every output is computed exactly as on one GPU (outputs are independent),
+    and the shards stay on their ranks -- no collective on the convolution path."""
+    if by == "batch":
+        a, b = shard_range(N, rank, size)
+        return slice(a, b), slice(0, K)
+    if by == "filters":
+        a, b = shard_range(K, rank, size)
+        return slice(0, N), slice(a, b)
+    raise ValueError("by must be 'batch' or 'filters'")
+
+
+def conv2d_layer_shard(ts, x, w, cfg, pad: int = 0, by: str = "batch", contraction: str = "exact"):
+    """This rank's shard of a layer: y[images, filters] for layer_shard(...);
+    x (N, C, H, W) and w (K, C, r, r) are the full tensors (each rank reads only
+    what its shard needs)."""
+    from .layer import conv2d_layer
+    rank, size = world()
+    ni, ki = layer_shard(x.shape[0], w.shape[0], rank, size, by)
+    return conv2d_layer(ts, x[ni], w[ki], cfg, pad, contraction), (ni, ki)
+
+
 def weak_image_indices(per_rank: int, rank: int) -> range:
     """Global image indices of a rank in a weak-scaling run (per-rank batch fixed)."""
     return range(rank * per_rank, (rank + 1) * per_rank)

@@ -62,3 +62,16 @@ def test_shard_range_partitions():
     assert list(Dd.weak_image_indices(32, 3)) == list(range(96, 128))
     with pytest.raises(ValueError):
         Dd.shard_range(10, 2, 2)
+
+
+def test_layer_shards_cover_outputs_once():
+    for N, K in ((8, 64), (3, 70), (1, 5)):
+        for size in (1, 2, 4, 8):
+            for by in ("batch", "filters"):
+                seen = np.zeros((N, K), dtype=int)
+                for r in range(size):
+                    ni, ki = Dd.layer_shard(N, K, r, size, by)
+                    seen[ni, ki] += 1
+                assert (seen == 1).all(), (N, K, size, by)
+    with pytest.raises(ValueError):
+        Dd.layer_shard(4, 4, 0, 2, "pixels")

@@ -143,3 +143,19 @@ def test_layer_nhwc_layout(mode):
     assert G.same_bits(np.ascontiguousarray(y.transpose(0, 3, 1, 2)), want)
     with pytest.raises(ValueError):
         W.conv2d_layer(ts, x, w, W.ConvConfig(*mode), pad=1, layout="CHWN")
+
+
+@pytest.mark.parametrize("by", ["batch", "filters"])
+def test_sharded_layer_assembles_to_the_full_layer(by):
+    """Per-rank shards (by images or by output channels) computed one after the
+    other on one GPU reassemble into the single-GPU result, bit for bit."""
+    from paper_1803_10986_b200 import distributed as Dd
+    ts = W.build_transforms(3, 2, W.parse_points("0,1,-1,inf"))
+    x = O.synthetic((5, 12, 10, 10), 6, 0)
+    w = O.synthetic((9, 12, 3, 3), 6, 1)
+    full = W.conv2d_layer(ts, x, w, W.ConvConfig(), pad=1)
+    out = np.zeros_like(full)
+    for r in range(4):
+        ni, ki = Dd.layer_shard(5, 9, r, 4, by)
+        out[ni, ki] = W.conv2d_layer(ts, x[ni], w[ki], W.ConvConfig(), pad=1)
+    assert G.same_bits(out, full)
