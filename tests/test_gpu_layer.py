@@ -159,3 +159,15 @@ def test_sharded_layer_assembles_to_the_full_layer(by):
         ni, ki = Dd.layer_shard(5, 9, r, 4, by)
         out[ni, ki] = W.conv2d_layer(ts, x[ni], w[ki], W.ConvConfig(), pad=1)
     assert G.same_bits(out, full)
+
+
+def test_empty_batch_layer_and_tiles():
+    """Empty inputs (N = 0 images, B = 0 tiles) give empty outputs of the right shape
+    and dtype, like the reference's ufunc composition on empty arrays."""
+    ts = W.build_transforms(3, 2, W.parse_points("0,1,-1,inf"))
+    for prec in ("fp32", "mixed"):
+        y = W.conv2d_layer(ts, np.zeros((0, 4, 9, 9), np.float32), O.synthetic((3, 4, 3, 3), 1, 1),
+                           W.ConvConfig(prec), pad=1)
+        assert y.shape == (0, 3, 9, 9) and y.dtype == (np.float32 if prec == "fp32" else np.float64)
+    z = W.conv_2d(ts, np.zeros((0, 2, 3, 3), np.float32), np.zeros((0, 2, 4, 4), np.float32))
+    assert z.shape == (0, 2, 2)
