@@ -171,3 +171,23 @@ def test_empty_batch_layer_and_tiles():
         assert y.shape == (0, 3, 9, 9) and y.dtype == (np.float32 if prec == "fp32" else np.float64)
     z = W.conv_2d(ts, np.zeros((0, 2, 3, 3), np.float32), np.zeros((0, 2, 4, 4), np.float32))
     assert z.shape == (0, 2, 2)
+
+
+def test_unsupported_combinations_fail_loudly():
+    """Unsupported plans / calls raise instead of silently falling back."""
+    import ctypes
+    from paper_1803_10986_b200 import _native
+    ts8 = W.build_transforms(3, 6, W.parse_points("0,-1,1,1/2,-1/2,2,-2,inf"))
+    with pytest.raises(RuntimeError):     # fused tcf needs alpha^2 <= 32
+        W.conv2d_layer(ts8, O.synthetic((1, 4, 12, 12), 1, 0), O.synthetic((2, 4, 3, 3), 1, 1), pad=1,
+                       contraction="tcf_bf16")
+    ts3 = W.build_transforms(3, 3, W.parse_points("0,1,-1,2,-2"))
+    op = W.layer_op(ts3, W.ConvConfig(), 1, 4, 12, 12, 2, 1)
+    M = torch.zeros((op.layout.P, op.layout.Kp, op.layout.Tp), device="cuda")
+    act = torch.zeros((1, 2, 6, 6), device="cuda")
+    rc = _native.lib().wino_output_transform_act(op.plan.handle, ctypes.byref(op.shape), _native.as_ptr(M),
+                                                 _native.as_ptr(act), 1, torch.cuda.current_stream().cuda_stream)
+    assert rc != 0                        # 2x2 pooling needs an even m
+    ts18 = W.curated_transform(18, 2, "fp32")
+    with pytest.raises(RuntimeError):     # layer kernels are generated for alpha <= 16 only
+        W.conv2d_layer(ts18, O.synthetic((1, 2, 20, 20), 1, 0), O.synthetic((2, 2, 3, 3), 1, 1), pad=1)
