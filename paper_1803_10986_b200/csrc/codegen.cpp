@@ -322,11 +322,11 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
           "    float rtw, float rth, int t0, int cb) {\n"
           "  const long long plane = Cp * Tp;\n"
           "  const long long tt = (long long)t0 + threadIdx.x;\n"
+       << "  const int c0 = cb * " << gather_cpt(P) << ";\n"
        << "  if (tt >= Tp) return;\n"
-       << "  const int c0 = cb * " << gather_cpt() << ";\n"
        << "  uv_t* op = V + ((tt / " << bn << ") * Cp + c0) * " << bn << " + (tt % " << bn << ");\n"
        << "  if (tt >= T || c0 >= C) {\n"
-       << "    for (int cc = 0; cc < " << gather_cpt() << "; ++cc, op += " << bn << ") {\n"
+       << "    for (int cc = 0; cc < " << gather_cpt(P) << "; ++cc, op += " << bn << ") {\n"
           "      const uv_t z = (c0 + cc >= C) ? (uv_t)(-0.0) : (uv_t)0;\n"
           "#pragma unroll\n"
        << "      for (int p = 0; p < " << P << "; ++p) op[p * plane] = z;\n"
@@ -343,8 +343,8 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
        << "  const long long HW = (long long)H * W;\n"
        << "  const in_t* src = x + ((long long)(img0 + di) * C + c0) * HW;\n"
        << "  const bool interior = h0 >= 0 && w0 >= 0 && h0 + " << n << " <= H && w0 + " << n << " <= W;\n"
-       << "#pragma unroll 1\n"
-       << "  for (int cc = 0; cc < " << gather_cpt() << "; ++cc, src += HW, op += " << bn << ") {\n"
+       << (gather_cpt(P) > 1 && P <= 16 ? "#pragma unroll\n" : "#pragma unroll 1\n")
+       << "  for (int cc = 0; cc < " << gather_cpt(P) << "; ++cc, src += HW, op += " << bn << ") {\n"
        << "  if (c0 + cc >= C) {\n"
           "#pragma unroll\n"
        << "    for (int p = 0; p < " << P << "; ++p) op[p * plane] = (uv_t)(-0.0);\n"
@@ -416,9 +416,9 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
        << "    input_gather_body(x, V, C, H, W, pad, th, tw, T, Tp, Cp, rtw, rth, blockIdx.y * " << TB
        << ", blockIdx.x);\n"
        << "  } else {\n"
-       << "    for (int cc = 0; cc < " << gather_cpt() << "; ++cc)\n"
+       << "    for (int cc = 0; cc < " << gather_cpt(P) << "; ++cc)\n"
        << "      filter_body(w, U, K, C, Kp, Cp, (blockIdx.y - n_tb) * " << TB << " + threadIdx.x, blockIdx.x * "
-       << gather_cpt() << " + cc);\n"
+       << gather_cpt(P) << " + cc);\n"
           "  }\n"
           "}\n\n";
 }

@@ -60,9 +60,13 @@ inline int env_pow2(const char* name, int dflt) {
     const int v = e ? std::atoi(e) : dflt;
     return (v == 1 || v == 2 || v == 4 || v == 8) ? v : dflt;
 }
-inline int gather_cpt() {
-    static const int v = env_pow2("WINO_CPT", 1);
-    return v;
+// channels per K1 thread: 2 for alpha^2 <= 16 (the two windows are gathered and
+// transformed in one unrolled body: more loads in flight, half the index math;
+// cfg2 K1 14.7 -> 12.7 us), 1 for larger alpha (register pressure: cfg3 m=6
+// 39 -> 54 us at 2).  WINO_CPT overrides.
+inline int gather_cpt(int P) {
+    static const int v = env_pow2("WINO_CPT", 0);
+    return v ? v : (P <= 16 ? 2 : 1);
 }
 inline int gather_kpt() {
     static const int v = env_pow2("WINO_KPT", 1);

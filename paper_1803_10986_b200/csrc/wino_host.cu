@@ -654,7 +654,7 @@ int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, c
         float rtw = 1.0f / tw, rth = 1.0f / th;
         void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &n_tb, (void*)&w, &U, &K, &Kp,
                         &Wl, &rtw, &rth};
-        return wino::launch(fg, dim3((unsigned)(Cp / wino::gather_cpt()), (unsigned)(n_tb + n_kb)), dim3(tb), 0,
+        return wino::launch(fg, dim3((unsigned)(Cp / wino::gather_cpt(L.P)), (unsigned)(n_tb + n_kb)), dim3(tb), 0,
                             stream, args, "transforms");
     }
     if (plan->fused()) return wino::fail(WINO_EUNSUPPORTED, "transforms: grid too large for the fused layout");
@@ -678,7 +678,7 @@ int wino_input_transform(wino_plan* plan, const wino_layer_shape* s, const void*
             if ((rc = plan->layer_mod(plan->pick(s))->function("wino_input_gather", &f))) return rc;
             float rtw = 1.0f / tw, rth = 1.0f / th;
             void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &Wl, &rtw, &rth};
-            return wino::launch(f, dim3((unsigned)(Cp / wino::gather_cpt()), (unsigned)n_tb), dim3(tb), 0, stream,
+            return wino::launch(f, dim3((unsigned)(Cp / wino::gather_cpt(L.P)), (unsigned)n_tb), dim3(tb), 0, stream,
                                 args, "input_transform");
         }
     }
