@@ -51,10 +51,9 @@ std::string gen_tile_source(int r, int m, const MatProg& G, const MatProg& BT, c
 
 // Gather transforms: channels per K1 thread / output channels per K4 thread (the
 // tile index math is amortised over them).  Must divide every channel padding
-// (Cp is a multiple of 8).  WINO_CPT / WINO_KPT override (1, 2, 4 or 8).  Default 1:
-// measured on B200 (tools/sweeps/sweep_xpt.sh) the kernels are bound by loads in flight,
-// not by index math -- cfg2 K1 14.2 / 14.7 / 16.2 us and cfg3 m=6 K4 38.9 / 65.8 /
-// 77.1 us at 1 / 4 / 8 channels per thread.
+// (Cp is a multiple of 8).  WINO_CPT / WINO_KPT override (1, 2, 4 or 8).  A rolled
+// loop over channels is slower (tools/sweeps/sweep_xpt.sh: fewer loads in flight --
+// cfg3 m=6 K4 38.9 / 65.8 / 77.1 us at 1 / 4 / 8 filters per thread); K4 keeps 1.
 inline int env_pow2(const char* name, int dflt) {
     const char* e = std::getenv(name);
     const int v = e ? std::atoi(e) : dflt;
