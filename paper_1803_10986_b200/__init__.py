@@ -27,7 +27,7 @@ from .engine import (
     tree_leaves,
 )
 from .exact import INFINITY, Point, Polynomial, parse_points, poly_product, to_nearest_float
-from .exact_oracle import check_exactness, conv_1d_exact, conv_2d_exact, conv_direct_exact
+from .exact_rational import check_exactness, conv_1d_exact, conv_2d_exact, conv_direct_exact
 from .harness import DirectSpec, ErrorReport, compare_reports, measure_error, measure_variants, trial_inputs
 from .layer import HostPipeline, LayerOp, conv2d_layer, direct_layer_f64, layer_error_stats, layer_op
 from .pointsets import curated_points, curated_transform
