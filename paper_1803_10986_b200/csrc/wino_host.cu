@@ -540,7 +540,9 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
         p->cands.push_back({4, 4, 16, 8, 16, 4, 0, 16, 0, 1});  // 64 x 32 (4x4): small layers (cfg1 20.4 -> 22.3)
         p->cands.push_back({8, 8, 16, 8, 8, 4, 0, 8, 0, 1});  // C <= 8 (first layers): 8-channel stages
     } else if (!env_gemm && contract_mode < WINO_CONTRACT_TC_BF16 && !dbl64) {
-        p->cands.push_back({4, 4, 16, 16, 8, 4, 168, 8, 0, 1});  // pairwise, C <= 8
+        // pairwise, C <= 8: 4x8 microtiles, 64 x 128 tiles (VGG-16 layer 1, M-store bound:
+        // 1.57 -> 1.24 ms vs 4x4 / 64 x 64, tools/probes/layer1_k3_sweep.sh)
+        p->cands.push_back({4, 8, 16, 16, 8, 4, 168, 8, 0, 1});
     }
     const std::string tag = "r" + std::to_string(r) + "m" + std::to_string(m) + "p" + std::to_string(precision);
     p->layer.name = "wino_layer_" + tag + ".cu";
