@@ -518,7 +518,9 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
     else if (dbl64)
         p->gemm = {4, 4, 8, 16, 16, 4, 0};       // DMUL/DADD linear: 14.8 TFLOP/s = 84% of the DMUL+DADD ceiling
     else if (channel_sum == WINO_SUM_PAIRWISE)
-        p->gemm = {4, 4, 16, 16, 32, 3, 168, 8, 0, 1};  // 8 consumer warps, 64x64 (27.7 -> 29.7 TFLOP/s)
+        // 8 consumer warps, 64x64, 64-channel stages x 2 (VGG-16 layer 6: 30.5 -> 33.0 TFLOP/s vs
+        // 32 x 3, tools/probes/vgg_l6_k3_sweep.sh)
+        p->gemm = {4, 4, 16, 16, 64, 2, 168, 8, 0, 1};
     else
         p->gemm = {8, 8, 16, 8, 16, 4, 0, 16, 0, 1};
     bool env_gemm = false;
@@ -543,6 +545,8 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
         // pairwise, C <= 8: 4x8 microtiles, 64 x 128 tiles (VGG-16 layer 1, M-store bound:
         // 1.57 -> 1.24 ms vs 4x4 / 64 x 64, tools/probes/layer1_k3_sweep.sh)
         p->cands.push_back({4, 8, 16, 16, 8, 4, 168, 8, 0, 1});
+        // C not a multiple of 64: 32-channel stages pad less
+        p->cands.push_back({4, 4, 16, 16, 32, 3, 168, 8, 0, 1});
     }
     const std::string tag = "r" + std::to_string(r) + "m" + std::to_string(m) + "p" + std::to_string(precision);
     p->layer.name = "wino_layer_" + tag + ".cu";

@@ -18,7 +18,8 @@ LINEAR = ["8,8,16,8,16,4,0,16,0,1",    # 128 x 64 (default)
           "4,4,16,8,16,4,0,16,0,1",    # 64 x 32
           "8,8,16,8,8,4,0,8,0,1",      # 8-channel stages (C <= 8)
           "8,8,16,8,16,4,0,8,0,0"]     # scalar FMUL + FADD
-PAIRWISE = ["4,4,16,16,32,3,168,8,0,1",  # default: 8 consumer warps, 64 x 64
+PAIRWISE = ["4,4,16,16,64,2,168,8,0,1",  # default: 8 consumer warps, 64 x 64, 64-channel stages
+            "4,4,16,16,32,3,168,8,0,1",  # 32-channel stages (C not a multiple of 64)
             "4,4,16,16,8,4,168,8,0,1",   # 8-channel stages
             "4,8,16,16,8,4,168,8,0,1",   # 8-channel stages, 64 x 128 (pairwise C <= 8 candidate)
             "4,4,8,16,32,4,168,8,0,1",   # 32 x 64
