@@ -1,5 +1,5 @@
 """VGG-16 layer-1 contraction probe (C=3, K=64, 224², batch 256, F(6,3) pairwise):
-times wino_contract alone (M = 6 GB written) under the current WINO_GEMM override."""
+times wino_contract alone (M = 6 GB written) and the K1+K2 launch under the current WINO_GEMM override."""
 import ctypes
 import os
 import sys
@@ -30,7 +30,15 @@ for _ in range(5):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 5
+xs = x.clone()
+e0.record()
+for _ in range(5):
+    _native.check(lib.wino_transforms(op.plan.handle, sh, _native.as_ptr(xs), _native.as_ptr(w), _native.as_ptr(U),
+                                      _native.as_ptr(V), s))
+e1.record()
+torch.cuda.synchronize()
+xf_ms = e0.elapsed_time(e1) / 5
 L = op.layout
 mb = L.m_bytes
 print(f"WINO_GEMM={os.environ.get('WINO_GEMM', 'default')} bm_bn={L.bm}x{L.bn} ms={ms:.3f} "
-      f"M_write_GBs={mb / ms / 1e6:.0f} sum={float(M.view(-1)[:: 9973].double().sum()):.6e}", flush=True)
+      f"M_write_GBs={mb / ms / 1e6:.0f} transforms_ms={xf_ms:.3f} sum={float(M.view(-1)[:: 9973].double().sum()):.6e}", flush=True)
