@@ -1,5 +1,5 @@
 """cfg2 contraction probe (F(2,3), N=32, C=K=128, 28², linear exact): wino_contract time
-under the current WINO_GEMM override, x in L2-cold state not controlled (K3 alone)."""
+under the current WINO_GEMM override (PROBE_PREC / PROBE_SUM select the mode), x in L2-cold state not controlled (K3 alone)."""
 import ctypes
 import os
 import sys
@@ -12,7 +12,8 @@ from paper_1803_10986_b200 import _native  # noqa: E402
 
 N, C, K, H = 32, 128, 128, 28
 ts = W.build_transforms(3, 2, W.parse_points("0,1,-1,inf"))
-op = W.layer_op(ts, W.ConvConfig("fp32", "huffman", "linear"), N, C, H, H, K, 1)
+PREC, CS = os.environ.get("PROBE_PREC", "fp32"), os.environ.get("PROBE_SUM", "linear")
+op = W.layer_op(ts, W.ConvConfig(PREC, "huffman", CS), N, C, H, H, K, 1)
 x = torch.rand(N, C, H, H, device="cuda") * 2 - 1
 w = torch.randn(K, C, 3, 3, device="cuda") * 0.2
 U, V = op.filter_transform(w), op.input_transform(x)
@@ -33,5 +34,5 @@ for i in range(23):
         ts_.append(e0.elapsed_time(e1))
 ts_.sort()
 L = op.layout
-print(f"WINO_GEMM={os.environ.get('WINO_GEMM', 'default')} bm_bn={L.bm}x{L.bn} median_ms={ts_[len(ts_) // 2]:.4f} "
+print(f"{PREC}/{CS} WINO_GEMM={os.environ.get('WINO_GEMM', 'default')} bm_bn={L.bm}x{L.bn} median_ms={ts_[len(ts_) // 2]:.4f} "
       f"min_ms={ts_[0]:.4f} tflops={op.contraction_flops / (ts_[len(ts_) // 2] * 1e-3) / 1e12:.1f}", flush=True)
