@@ -1,15 +1,19 @@
-"""Benchmark of the Winograd layer hot path (BASELINE.json metric:
-"Winograd conv direct-equiv TFLOP/s").
+"""Benchmark of the Winograd hot path (BASELINE.json metric:
+"Winograd conv direct-equiv TFLOP/s (1/2/4/8 GPU); rel. L1 error vs fp64 direct").
 
-Default workload = BASELINE.json configs[1]: F(2x2, 3x3), points {0,1,-1,inf},
-fp32 throughout (huffman transforms, linear channel sum, exact contraction),
-N=32 per GPU, C=K=128, H=W=28, pad 1, x ~ U[-1,1], w ~ He-normal, seeded.
-A step = filter transform + input transform + channel contraction + output
-transform of one batch (the four libwino kernels, inputs resident in HBM).
-Multi-GPU: one process per GPU, each rank runs its own batch (global image
-indices rank*N .. rank*N+N-1) -> weak scaling; NCCL only reduces timings and
-error statistics.  `--impl reference` times the CPU port of the reference's
-arithmetic (oracle/) on the host cores for the same workload.
+Default workload = BASELINE.json configs[4], the config the metric's 1/2/4/8-GPU
+figure is quoted on and that fits one B200: the VGG-16 conv stack (13 3x3 layers,
+ReLU, 2x2 max-pools after layers 2/4/7/10), every layer through Winograd
+F(6x6,3x3) with the P8 points {0,-1,1,1/2,-1/2,2,-2,inf}, fp32, Huffman-ordered
+transforms, pairwise channel sums, exact contraction; global batch 256 of
+224x224x3 synthetic U[-1,1] images, He-normal filters (seeded Philox).
+A step = one 13-layer forward (39 libwino kernels, input resident in HBM).
+Multi-GPU: one process per GPU (`--gpus N` re-execs under torch.distributed.run
+when no torchrun environment is set), the global batch sharded by images
+(strong scaling); NCCL only reduces timings.  `--impl reference` times the CPU
+port of the reference's arithmetic (oracle/) on the host cores on the
+BASELINE.md 2-image slice.  `--config cfg1|cfg2|...` selects the single-layer
+configs (configs[0..3]) as extra lines.
 """
 
 from __future__ import annotations
@@ -439,6 +443,83 @@ def run_gpu(args, cfg):
         dist.destroy_process_group()
 
 
+VGG_POINTS = "0,-1,1,1/2,-1/2,2,-2,inf"
+
+
+def vgg_inputs(a, b, seed=2024):
+    """Synthetic U[-1,1] 3x224x224 images a..b-1, keyed Philox(seed, global image index)."""
+    return np.ascontiguousarray(np.stack([synth((3, 224, 224), seed, i, "uniform") for i in range(a, b)]))
+
+
+def vgg_config(args, n_per_gpu, world):
+    return {"workload": "vgg16", "model": "VGG-16 conv stack (13 conv layers, ReLU, 4 max-pools; no FC head)",
+            "winograd": "F(6x6,3x3)", "points": VGG_POINTS, "global_batch": args.vgg_batch,
+            "batch_per_gpu": n_per_gpu, "image": [3, 224, 224], "precision": "fp32", "dot_order": "huffman",
+            "channel_sum": "pairwise", "contraction": args.contraction, "layers": 13, "pools_after": [2, 4, 7, 10],
+            "l2": "no flush needed: inputs and activations >> 126 MB L2 (layer-1 x 154 MB, M 6 GB)",
+            "parallelism": f"dp{world} (global batch sharded by images)"}
+
+
+def vgg_cpu_forward(x, weights, procs):
+    """The oracle port of the stack (reference arithmetic, oracle/stack_pool.py) on
+    images x over `procs` processes: (seconds, conv outputs, final activation)."""
+    from oracle import wino_oracle as O
+    from oracle.stack_pool import OraclePool
+    from paper_1803_10986_b200.stack import VGG16
+    trip = O.Triple.from_points(3, 6, VGG_POINTS)
+    with OraclePool(trip, weights, x.shape[0] * 64 * 226 * 226, procs=procs) as pool:
+        if procs > 1:
+            pool.layer(12, np.zeros((1, 512, 14, 14), np.float32))  # fork + warm the workers
+        t0 = time.perf_counter()
+        outs, act = pool.stack_forward(x, VGG16)
+        return time.perf_counter() - t0, outs, act
+
+
+def vgg_direct_flops(n):
+    from paper_1803_10986_b200.stack import VGG16
+    h, tot = 224, 0
+    for C, K, pool in VGG16:
+        tot += 2 * n * K * C * h * h * 9
+        if pool:
+            h //= 2
+    return tot
+
+
+def run_reference_vgg(args):
+    """--impl reference for vgg16: the reference's arithmetic (oracle port) on the
+    host cores; each step = the BASELINE.md 2-image slice through all 13 layers."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    from paper_1803_10986_b200.stack import VGG16, he_normal_weights
+    x = vgg_inputs(0, args.cpu_vgg_images)
+    ws = he_normal_weights(VGG16, 3)
+    procs = host_cores()
+    from oracle import wino_oracle as O
+    from oracle.stack_pool import OraclePool
+    trip = O.Triple.from_points(3, 6, VGG_POINTS)
+    times = []
+    with OraclePool(trip, ws, x.shape[0] * 64 * 226 * 226, procs=procs) as pool:
+        pool.layer(12, np.zeros((1, 512, 14, 14), np.float32))
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            pool.stack_forward(x, VGG16, keep=False)
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.mean(times))
+    val = vgg_direct_flops(x.shape[0]) / (ms * 1e-3) / 1e12
+    sample = (f"{x.shape[0]} of {args.vgg_batch} images per step through all 13 layers (BASELINE.md 2: 2-image "
+              f"slice), oracle/stack_pool.py (oracle/wino_oracle.py layer_conv2d = the reference's per-(filter, tile) "
+              f"arithmetic) over {procs} processes")
+    line = {"metric": METRIC, "value": val, "unit": "TFLOP/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded Philox U[-1,1] 224x224x3 images, He-normal filters)",
+            "config": vgg_config(args, args.vgg_batch, 1),
+            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": procs, "kind": "port", "sample": sample},
+            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
 def run_vgg(args):
     """BASELINE config 5: VGG-16 conv stack, F(6x6,3x3) P8, pairwise, fp32, global batch
     sharded across ranks (strong scaling); step = one 13-layer forward."""
@@ -454,114 +535,162 @@ def run_vgg(args):
     import paper_1803_10986_b200 as W
     from paper_1803_10986_b200 import _native
     from paper_1803_10986_b200.distributed import shard_range
-    from paper_1803_10986_b200.stack import VGG16, ConvStack, he_normal_weights
+    from paper_1803_10986_b200.stack import VGG16, ConvStack, StackPipeline, he_normal_weights
 
-    pts = "0,-1,1,1/2,-1/2,2,-2,inf"
-    ts = W.build_transforms(3, 6, W.parse_points(pts))
+    ts = W.build_transforms(3, 6, W.parse_points(VGG_POINTS))
+    wcfg = W.ConvConfig("fp32", "huffman", "pairwise")
     a, b = shard_range(args.vgg_batch, rank, world)
     n = b - a
-    st = ConvStack(ts, W.ConvConfig("fp32", "huffman", "pairwise"), VGG16, n, 224,
-                   contraction=args.contraction)
-    st.set_weights(he_normal_weights(VGG16, 3))
-    x = torch.empty((n, 3, 224, 224), dtype=torch.float32, device="cuda")
-    for i in range(n):  # synthetic U[-1,1] images keyed by global image index
-        x[i].copy_(torch.from_numpy(synth((3, 224, 224), 2024, a + i, "uniform")))
+    st = ConvStack(ts, wcfg, VGG16, n, 224, contraction=args.contraction)
+    ws_np = he_normal_weights(VGG16, 3)
+    st.set_weights(ws_np)
+    x_np = vgg_inputs(a, b)
+    x = torch.from_numpy(x_np).cuda()
     for _ in range(max(3, args.warmup)):
         st.forward(x)
     torch.cuda.synchronize()
+    if args.ncu:
+        for _ in range(args.steps):
+            st.forward(x)
+        torch.cuda.synchronize()
+        return
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph):
         st.forward(x)
     graph.replay()
     torch.cuda.synchronize()
     es = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stream = torch.cuda.current_stream()
     with ClockSampler(local) as clk:
+        t_end = time.perf_counter() + args.soak  # untimed load so the sampler sees the clocks under load
+        while time.perf_counter() < t_end:
+            graph.replay()
+            torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         for e0, e1 in es:  # inputs and activations >> L2: no flush needed
-            e0.record()
+            e0.record(stream)
             graph.replay()
-            e1.record()
+            e1.record(stream)
         torch.cuda.synchronize()
-    ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in es]))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+    ms_steps = [e0.elapsed_time(e1) for e0, e1 in es]
+    ms = float(np.mean(ms_steps))
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    total_flops = st.direct_flops * world if world == 1 else None
-    flops_all = 0
-    for op_ in st.ops:
-        flops_all += op_.direct_flops
     # whole-job direct-eq flops: every rank's shard (equal or +-1 image)
-    gflops = torch.tensor([float(flops_all)], dtype=torch.float64, device="cuda")
+    gflops = torch.tensor([float(st.direct_flops)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(gflops)
     value = float(gflops.item()) / (ms * 1e-3) / 1e12
-    # per-kernel shares from an instrumented forward (events around each contraction)
-    lib = _native.lib()
-    import ctypes
-    c_ms = 0.0
-    c_flops = 0
-    other_ms = 0.0
-    per_layer = []
+    y_dev = st.act[-1].clone()
+
+    # ---- per-layer stage times from an instrumented eager forward (events between stages)
+    per_layer, c_ms, c_flops, other_ms = [], 0.0, 0, 0.0
+    mp_ = measured_peaks()
+    hbm = mp_["hbm_gbs"]
     cur = x
-    s = torch.cuda.current_stream().cuda_stream
-    for i, op_ in enumerate(st.ops):
-        L = op_.layout
-        ws = st.workspace
-        al = lambda v: (v + 255) // 256 * 256
-        U = ws.data_ptr()
-        V = U + al(L.u_bytes)
-        M = V + al(L.v_bytes)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        ev[0].record()
-        _native.check(lib.wino_filter_transform(op_.plan.handle, ctypes.byref(op_.shape),
-                                                _native.as_ptr(st.weights[i]), ctypes.c_void_p(U), s))
-        _native.check(lib.wino_input_transform(op_.plan.handle, ctypes.byref(op_.shape), _native.as_ptr(cur),
-                                               ctypes.c_void_p(V), s))
-        ev[1].record()
-        _native.check(lib.wino_contract(op_.plan.handle, ctypes.byref(op_.shape), ctypes.c_void_p(U),
-                                        ctypes.c_void_p(V), ctypes.c_void_p(M), s))
-        ev[2].record()
-        C, K, h, w_, pool = st.shapes[i]
-        if st.fused_act:  # the forward's K4 with ReLU / max-pool fused
-            _native.check(lib.wino_output_transform_act(op_.plan.handle, ctypes.byref(op_.shape),
-                                                        ctypes.c_void_p(M), _native.as_ptr(st.act[i]),
-                                                        1 if pool else 0, s))
-        else:
-            _native.check(lib.wino_output_transform(op_.plan.handle, ctypes.byref(op_.shape), ctypes.c_void_p(M),
-                                                    _native.as_ptr(st.conv_out[i]), s))
-            _native.check(lib.wino_relu_pool(0, op_.N * K, L.Ho, L.Wo, 1 if pool else 0,
-                                             _native.as_ptr(st.conv_out[i]), _native.as_ptr(st.act[i]), s))
-        ev[3].record()
+    if st.fused_act:
+        for i, op_ in enumerate(st.ops):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            cur = st.layer_forward(i, cur, events=ev)
+            torch.cuda.synchronize()
+            C, K, h, w_, pool = st.shapes[i]
+            L = op_.layout
+            t_x, t_c, t_o = (ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]))
+            P, T = L.P, L.T
+            b_x = 4 * n * C * h * w_ + 4 * P * C * T + 4 * K * C * 9 + 4 * P * C * K  # x read, V + U written
+            out_el = n * K * (L.Ho // 2) * (L.Wo // 2) if pool else n * K * L.Ho * L.Wo
+            b_o = 4 * P * K * T + 4 * out_el                                             # M read, act written
+            per_layer.append({"layer": i + 1, "C": C, "K": K, "H": h, "tile_bm_bn": [L.bm, L.bn],
+                              "transforms_ms": t_x, "transforms_frac_hbm": b_x / (t_x * 1e-3) / 1e9 / hbm,
+                              "contract_ms": t_c, "contract_tflops": op_.contraction_flops / (t_c * 1e-3) / 1e12,
+                              "output_act_ms": t_o, "output_act_frac_hbm": b_o / (t_o * 1e-3) / 1e9 / hbm})
+            c_ms += t_c
+            other_ms += t_x + t_o
+            c_flops += op_.contraction_flops
+    peak = measure_peaks(_native.lib(), _native, torch)
+    ach = c_flops / (c_ms * 1e-3) / 1e12 if c_ms else 0.0
+
+    # ---- end to end through the public API: pinned host images in -> pinned host final activation out
+    xh = torch.from_numpy(x_np).pin_memory()
+    pipe = StackPipeline(ts, wcfg, VGG16, n, 224, chunks=args.vgg_chunks, contraction=args.contraction)
+    pipe.set_weights(ws_np)
+    yh = torch.empty(pipe.out_shape, dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        pipe(xh, yh)
+    torch.cuda.synchronize()
+    e2e_ms = []
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        pipe(xh, yh)
+        e1.record(stream)
         torch.cuda.synchronize()
-        c_ms += ev[1].elapsed_time(ev[2])
-        other_ms += ev[0].elapsed_time(ev[1]) + ev[2].elapsed_time(ev[3])
-        per_layer.append({"layer": i + 1, "C": C, "K": K, "H": h, "bm_bn": [L.bm, L.bn],
-                          "transforms_ms": ev[0].elapsed_time(ev[1]), "contract_ms": ev[1].elapsed_time(ev[2]),
-                          "contract_tflops": op_.contraction_flops / (ev[1].elapsed_time(ev[2]) * 1e-3) / 1e12,
-                          "output_relu_pool_ms": ev[2].elapsed_time(ev[3])})
-        c_flops += op_.contraction_flops
-        cur = st.act[i]
-    peak = measure_peaks(lib, _native, torch)
-    ach = c_flops / (c_ms * 1e-3) / 1e12
+        e2e_ms.append(e0.elapsed_time(e1))
+    e2e_t = float(np.median(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    e2e_val = float(gflops.item()) / (e2e_t * 1e-3) / 1e12
+    e2e_same = bool(torch.equal(yh, y_dev.cpu()))
+    del pipe
+
+    # ---- per-layer isolated error vs fp64 direct (device kernel), unfused forward keeps y per layer
     errs = st.layer_errors(x, images=args.err_images) if not args.no_err else None
+    conv_first = [st.conv_out[i][: args.cpu_vgg_images].cpu().numpy() for i in range(len(st.ops))] \
+        if (rank == 0 and world == 1 and not args.no_cpu) else None
+    st._conv_out = None
     if rank == 0:
+        roof = vgg_roof(args, ach, peak, c_ms / (c_ms + other_ms) if c_ms else None)
+        roof.update({"flops_per_forward": c_flops, "launches": len(st.ops),
+                     "achieved_note": "sum of the 13 contraction launches' algorithmic flops (2 P T C K each) / "
+                                      "sum of their CUDA-event durations (instrumented eager forward)"})
         line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (seeded Philox U[-1,1] 224x224x3 images, He-normal filters)",
-                "config": {"workload": "vgg16", "winograd": "F(6x6,3x3)", "points": pts,
-                           "global_batch": args.vgg_batch, "batch_per_gpu": n, "precision": "fp32",
-                           "dot_order": "huffman", "channel_sum": "pairwise", "contraction": args.contraction,
-                           "layers": 13, "pools_after": [2, 4, 7, 10],
-                           "l2": "inputs/activations >> L2 (no flush)",
-                           "parallelism": f"dp{world} (batch sharded)"},
-                "roofline": vgg_roof(args, ach, peak, c_ms / (c_ms + other_ms)),
-                "per_layer_error_vs_fp64": errs, "per_layer_timing": per_layer,
-                "gpu_launches": st.kernels_per_forward * args.steps,
-                "clocks": clk.summary(), "peaks": peak}
+                "config": vgg_config(args, n, world), "roofline": roof,
+                "stages": {"contract_ms": c_ms, "transforms_ms": sum(p["transforms_ms"] for p in per_layer),
+                           "output_act_ms": sum(p["output_act_ms"] for p in per_layer)},
+                "per_layer_timing": per_layer, "per_layer_error_vs_fp64": errs,
+                "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": int(xh.numel() * 4),
+                        "d2h_bytes_per_step": int(yh.numel() * 4), "ms_per_step": e2e_t,
+                        "ms_steps": [round(v, 3) for v in e2e_ms],
+                        "timing": "median of the K timed steps (CUDA events on the issuing stream)",
+                        "api": f"StackPipeline(chunks={args.vgg_chunks}): pinned host images -> H2D | 13 layers | "
+                               "D2H of the final activation, overlapped on 3 streams; weights resident",
+                        "bitwise_equal_to_device_path": e2e_same},
+                "timing": "value/ms_per_step: CUDA-graph replay of the 39-kernel forward, events around each step",
+                "ms_steps": [round(v, 3) for v in ms_steps],
+                "gpu_launches": st.kernels_per_forward * args.steps, "clocks": clk.summary(), "peaks": peak}
+        if world == 1 and not args.no_cpu:
+            procs = host_cores()
+            xs = x_np[: args.cpu_vgg_images]
+            t_all, outs, act = vgg_cpu_forward(xs, ws_np, procs)
+            fl = vgg_direct_flops(xs.shape[0])
+            line["cpu_baseline"] = {"value": fl / t_all / 1e12, "unit": "TFLOP/s", "cores": procs, "kind": "port",
+                                    "sample": f"{xs.shape[0]} of {n} images through all 13 layers "
+                                              f"(oracle/stack_pool.py over {procs} processes), {t_all:.2f} s"}
+            if args.cpu_1core_images > 0:
+                x1 = x_np[: args.cpu_1core_images]
+                t1, _, _ = vgg_cpu_forward(x1, ws_np, 1)
+                line["cpu_baseline_1core"] = {
+                    "value": vgg_direct_flops(x1.shape[0]) / t1 / 1e12, "unit": "TFLOP/s", "cores": 1,
+                    "kind": "port", "sample": f"{x1.shape[0]} image(s) through all 13 layers, one process "
+                                              f"(numpy ufuncs are single-threaded), {t1:.2f} s"}
+            same = [bool(outs[i].tobytes() == conv_first[i].tobytes()) for i in range(len(outs))]
+            line["parity_vs_oracle"] = {"images": int(xs.shape[0]), "layers_bitwise_equal": same,
+                                        "final_activation_bitwise_equal": bool(
+                                            act.tobytes() == y_dev[: xs.shape[0]].cpu().numpy().tobytes()),
+                                        "note": "the cpu_baseline's oracle outputs vs this run's batch-256 outputs "
+                                                "of the same images (pre-activation y per layer, final activation)"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -628,14 +757,30 @@ def measure_peaks(lib, _native, torch):
     return res
 
 
-def main():
+def spawn_ranks(args):
+    """`--gpus N` without a torchrun environment: re-exec this script under
+    torch.distributed.run with N local ranks (127.0.0.1 rendezvous); the ranks'
+    rank 0 prints the one JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS) + ["vgg16"])
+    ap.add_argument("--config", default="vgg16", choices=sorted(CONFIGS) + ["vgg16"])
     ap.add_argument("--vgg-batch", type=int, default=256)
+    ap.add_argument("--vgg-chunks", type=int, default=4, help="image chunks of the vgg16 e2e pipeline")
+    ap.add_argument("--cpu-vgg-images", type=int, default=2, help="vgg16 CPU sample (BASELINE.md: 2-image slice)")
+    ap.add_argument("--cpu-1core-images", type=int, default=1, help="vgg16 single-process CPU sample (0: skip)")
     ap.add_argument("--err-images", type=int, default=8)
     ap.add_argument("--no-err", action="store_true")
     ap.add_argument("--contraction", default="exact", choices=["exact", "ffma", "tc_bf16", "tc_fp16", "tcf_bf16", "tcf_fp16"])
@@ -644,12 +789,15 @@ def main():
     ap.add_argument("--soak", type=float, default=1.5, help="seconds of untimed load before the timed region")
     ap.add_argument("--e2e-chunks", default="4", help="image chunks of the e2e pipeline: a count or sizes a,b,...")
     ap.add_argument("--ncu", action="store_true", help="profiling mode: warm-up + K eager steps only, no output")
-    args = ap.parse_args()
+    return ap.parse_args(argv)
+
+
+def main():
+    args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     if args.config == "vgg16":
-        if args.impl == "reference":
-            print(json.dumps({"impl": "reference", "unavailable": "vgg16 CPU reference: use --config cfg2"}))
-            return
-        run_vgg(args)
+        (run_reference_vgg if args.impl == "reference" else run_vgg)(args)
         return
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

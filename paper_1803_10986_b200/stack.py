@@ -5,6 +5,10 @@ path (K2 K1 K3 K4), each followed by ReLU and, after layers 2, 4, 7 and 10, a
 2x2 max-pool (both in one libwino kernel).  Per-layer *isolated* error: every
 layer's Winograd output is compared with the fp64 direct convolution of the
 same fp32 input activation (SURVEY.md 7.2 "fp64 oracle at VGG scale").
+
+Each layer's arithmetic is the reference's per-(filter, tile) ``conv_2d``
+(engine.py:426-429 over the zero-padded image); the activation
+between layers is the oracle's ``relu_pool``.
 """
 
 from __future__ import annotations
@@ -42,6 +46,7 @@ class ConvStack:
             raise ValueError("ConvStack chains fp32 activations: use precision='fp32'")
         W = H if W is None else W
         self.ts, self.cfg, self.layers, self.N, self.pad = ts, cfg, list(layers), N, pad
+        self.H, self.W = H, W
         self.ops, self.shapes = [], []
         h, w = H, W
         for C, K, pool in self.layers:
@@ -54,19 +59,37 @@ class ConvStack:
         self.out_hw = (h, w)
         ws = max(op.layout.workspace_bytes for op in self.ops)
         self.workspace = D.torch.empty(ws, dtype=D.torch.uint8, device="cuda")
-        self.conv_out = [D.empty(op.out_shape, np.float32) for op in self.ops]
+        self._conv_out = None  # pre-activation outputs, allocated on first keep_conv_out forward
         self.act = []
         for op, (C, K, h, w, pool) in zip(self.ops, self.shapes):
             Ho, Wo = op.layout.Ho, op.layout.Wo
             self.act.append(D.empty((N, K, Ho // 2, Wo // 2) if pool else (N, K, Ho, Wo), np.float32))
         self.weights = None
 
+    @property
+    def conv_out(self):
+        if self._conv_out is None:
+            self._conv_out = [D.empty(op.out_shape, np.float32) for op in self.ops]
+        return self._conv_out
+
+    @property
+    def out_shape(self):
+        return tuple(self.act[-1].shape)
+
     def set_weights(self, weights):
         self.weights = [D.to_device(w, np.float32)[0] for w in weights]
+
+    def share_weights(self, other: "ConvStack"):
+        """Use another stack's device weights (same layers, e.g. a different batch size)."""
+        self.weights = other.weights
 
     @property
     def direct_flops(self) -> int:
         return sum(op.direct_flops for op in self.ops)
+
+    @property
+    def contraction_flops(self) -> int:
+        return sum(op.contraction_flops for op in self.ops)
 
     @property
     def fused_act(self) -> bool:
@@ -78,39 +101,64 @@ class ConvStack:
     def kernels_per_forward(self) -> int:
         return (3 if self.fused_act else 4) * len(self.ops)
 
-    def forward(self, x, keep_conv_out=False):
+    def _uvm(self, L):
+        al = lambda v: (v + 255) // 256 * 256
+        U = self.workspace.data_ptr()
+        V = U + al(L.u_bytes)
+        return U, V, V + al(L.v_bytes)
+
+    def layer_forward(self, i, cur, stream=None, events=None):
+        """Layer i on activation `cur` (fused path): K1+K2, K3, K4+ReLU(+pool) -> self.act[i].
+        events: optional 4 CUDA events recorded before K1+K2, before K3, before K4, after K4."""
+        lib = _native.lib()
+        s = D.stream_handle() if stream is None else stream
+        op = self.ops[i]
+        pool = self.shapes[i][4]
+        sh = ctypes.byref(op.shape)
+        U, V, M = self._uvm(op.layout)
+        if events is not None:
+            events[0].record()
+        _native.check(lib.wino_transforms(op.plan.handle, sh, D.ptr(cur), D.ptr(self.weights[i]),
+                                          ctypes.c_void_p(U), ctypes.c_void_p(V), s), f"layer {i + 1} K1/K2")
+        if events is not None:
+            events[1].record()
+        _native.check(lib.wino_contract(op.plan.handle, sh, ctypes.c_void_p(U), ctypes.c_void_p(V),
+                                        ctypes.c_void_p(M), s), f"layer {i + 1} K3")
+        if events is not None:
+            events[2].record()
+        _native.check(lib.wino_output_transform_act(op.plan.handle, sh, ctypes.c_void_p(M),
+                                                    D.ptr(self.act[i]), 1 if pool else 0, s),
+                      f"layer {i + 1} K4+act")
+        if events is not None:
+            events[3].record()
+        return self.act[i]
+
+    def forward(self, x, keep_conv_out=False, stream=None, before_last=None):
         """x: CUDA f32 tensor (N, C0, H, W) -> activation after the last layer.
 
         Per layer: K2+K1 (one launch), K3, then K4 with ReLU (+ max-pool) fused
         (wino_output_transform_act) -- bitwise the same activations as K4 followed
         by wino_relu_pool.  keep_conv_out=True takes the unfused path and keeps
-        every layer's pre-activation output in self.conv_out (layer_errors)."""
+        every layer's pre-activation output in self.conv_out (layer_errors).
+        before_last: called just before the last layer is issued (pipelines insert
+        a wait for the read-back of the previous chunk's final activation there)."""
         lib = _native.lib()
-        s = D.stream_handle()
+        s = D.stream_handle() if stream is None else stream
         cur = x
-        al = lambda v: (v + 255) // 256 * 256
         for i, op in enumerate(self.ops):
             C, K, h, w, pool = self.shapes[i]
-            sh = ctypes.byref(op.shape)
+            if before_last is not None and i == len(self.ops) - 1:
+                before_last()
             if keep_conv_out or not self.fused_act:
                 y = self.conv_out[i]
-                _native.check(lib.wino_conv2d(op.plan.handle, sh, D.ptr(cur), D.ptr(self.weights[i]), D.ptr(y),
-                                              D.ptr(self.workspace), self.workspace.numel(), s), f"layer {i + 1}")
+                _native.check(lib.wino_conv2d(op.plan.handle, ctypes.byref(op.shape), D.ptr(cur),
+                                              D.ptr(self.weights[i]), D.ptr(y), D.ptr(self.workspace),
+                                              self.workspace.numel(), s), f"layer {i + 1}")
                 _native.check(lib.wino_relu_pool(0, op.N * K, op.layout.Ho, op.layout.Wo, 1 if pool else 0,
                                                  D.ptr(y), D.ptr(self.act[i]), s), "relu_pool")
+                cur = self.act[i]
             else:
-                L = op.layout
-                U = self.workspace.data_ptr()
-                V = U + al(L.u_bytes)
-                M = V + al(L.v_bytes)
-                _native.check(lib.wino_transforms(op.plan.handle, sh, D.ptr(cur), D.ptr(self.weights[i]),
-                                                  ctypes.c_void_p(U), ctypes.c_void_p(V), s), f"layer {i + 1} K1/K2")
-                _native.check(lib.wino_contract(op.plan.handle, sh, ctypes.c_void_p(U), ctypes.c_void_p(V),
-                                                ctypes.c_void_p(M), s), f"layer {i + 1} K3")
-                _native.check(lib.wino_output_transform_act(op.plan.handle, sh, ctypes.c_void_p(M),
-                                                            D.ptr(self.act[i]), 1 if pool else 0, s),
-                              f"layer {i + 1} K4+act")
-            cur = self.act[i]
+                cur = self.layer_forward(i, cur, s)
         return cur
 
     def layer_errors(self, x, images=None):
@@ -130,3 +178,70 @@ class ConvStack:
                         "per_point_l1": float(st[:, 0].sum() / st[:, 2].sum()), "max_abs": float(st[:, 3].max())})
             inp = self.act[i]
         return res
+
+
+class StackPipeline:
+    """Host-buffer forward of a conv stack with the PCIe copies hidden: the batch is
+    split into image chunks; chunk i+1's H2D copy and chunk i-1's D2H copy of the
+    final activation run on their own streams while chunk i's 13 layers run on the
+    compute stream (the copy engines and the SMs overlap).
+
+    x_host (N, C0, H, W) and out_host (N, K_last, h, w) must be pinned f32 CPU
+    tensors.  Weights stay resident on the device (set_weights once)."""
+
+    def __init__(self, ts, cfg: ConvConfig, layers, N, H, W=None, chunks=4, pad=1, contraction="exact"):
+        chunks = max(1, min(int(chunks), N))
+        self.bounds = [(i * N // chunks, (i + 1) * N // chunks) for i in range(chunks)]
+        sizes = sorted({b - a for a, b in self.bounds})
+        self.stacks = {n: ConvStack(ts, cfg, layers, n, H, W, pad, contraction) for n in sizes}
+        first = self.stacks[sizes[0]]
+        self.N, self.layers = N, list(layers)
+        self.in_shape = (N, layers[0][0], H, H if W is None else W)
+        self.out_shape = (N,) + first.out_shape[1:]
+        self.x_dev = D.empty(self.in_shape, np.float32)
+        self.s_h2d, self.s_cmp, self.s_d2h = D.torch.cuda.Stream(), D.torch.cuda.Stream(), D.torch.cuda.Stream()
+        self.ev_in = [D.torch.cuda.Event() for _ in self.bounds]
+        self.ev_out = [D.torch.cuda.Event() for _ in self.bounds]
+        self.ev_d2h = [D.torch.cuda.Event() for _ in self.bounds]
+
+    def set_weights(self, weights):
+        stacks = list(self.stacks.values())
+        stacks[0].set_weights(weights)
+        for st in stacks[1:]:
+            st.share_weights(stacks[0])
+
+    @property
+    def direct_flops(self) -> int:
+        return sum(self.stacks[b - a].direct_flops for a, b in self.bounds)
+
+    @property
+    def kernels_per_forward(self) -> int:
+        return sum(self.stacks[b - a].kernels_per_forward for a, b in self.bounds)
+
+    def __call__(self, x_host, out_host):
+        torch = D.torch
+        cur = torch.cuda.current_stream()
+        for s in (self.s_h2d, self.s_cmp, self.s_d2h):
+            s.wait_stream(cur)
+        with torch.cuda.stream(self.s_h2d):
+            for (a, b), ev in zip(self.bounds, self.ev_in):
+                self.x_dev[a:b].copy_(x_host[a:b], non_blocking=True)
+                ev.record(self.s_h2d)
+        prev = {}  # stack size -> index of the last chunk whose final activation it holds
+        for j, ((a, b), e_in, e_out) in enumerate(zip(self.bounds, self.ev_in, self.ev_out)):
+            st = self.stacks[b - a]
+            with torch.cuda.stream(self.s_cmp):
+                self.s_cmp.wait_event(e_in)
+                hook = None
+                if (b - a) in prev:  # the final-activation buffer must have been read back
+                    hook = (lambda ev: lambda: self.s_cmp.wait_event(ev))(self.ev_d2h[prev[b - a]])
+                st.forward(self.x_dev[a:b], stream=self.s_cmp.cuda_stream, before_last=hook)
+                e_out.record(self.s_cmp)
+            with torch.cuda.stream(self.s_d2h):
+                self.s_d2h.wait_event(e_out)
+                out_host[a:b].copy_(st.act[-1], non_blocking=True)
+                self.ev_d2h[j].record(self.s_d2h)
+            prev[b - a] = j
+        cur.wait_stream(self.s_d2h)
+        cur.wait_stream(self.s_cmp)
+        return out_host

@@ -69,3 +69,30 @@ def test_vgg16_geometry():
     st = ConvStack(ts, W.ConvConfig("fp32", "huffman", "pairwise"), VGG16, 1, 224)
     assert st.out_hw == (14, 14)
     assert abs(st.direct_flops * 256 - 7.86e12) / 7.86e12 < 0.01   # 7.86 TFLOP per batch-256
+
+
+def test_vgg16_full_size_batch256_bitwise():
+    """BASELINE config 5 at its real shape (batch 256, 224x224x3, the default tile
+    picks of every layer): images 0 and 255 of the batch, every layer's
+    pre-activation output and the final activation, bit for bit against the oracle
+    (reference per-(filter, tile) arithmetic, run over host processes)."""
+    import os
+    from oracle.stack_pool import OraclePool
+    from paper_1803_10986_b200.stack import VGG16, ConvStack, he_normal_weights
+    ts = W.build_transforms(3, 6, W.parse_points(P8))
+    trip = O.Triple.from_points(3, 6, P8)
+    N = 256
+    x = np.stack([O.synthetic((3, 224, 224), 2024, i) for i in range(N)])
+    ws = he_normal_weights(VGG16, 3)
+    st = ConvStack(ts, W.ConvConfig("fp32", "huffman", "pairwise"), VGG16, N, 224)
+    st.set_weights(ws)
+    xt = torch.from_numpy(x).cuda()
+    fused = st.forward(xt).cpu().numpy()[[0, N - 1]]
+    st.forward(xt, keep_conv_out=True)
+    got = [st.conv_out[i][[0, N - 1]].cpu().numpy() for i in range(len(VGG16))]
+    sample = x[[0, N - 1]]
+    with OraclePool(trip, ws, 2 * 64 * 226 * 226, procs=min(16, len(os.sched_getaffinity(0)))) as pool:
+        outs, act = pool.stack_forward(sample, VGG16)
+    for i, (g, want) in enumerate(zip(got, outs)):
+        assert G.same_bits(g, want), f"layer {i + 1}"
+    assert G.same_bits(fused, act)
