@@ -125,6 +125,16 @@ int wino_plan_source(const wino_plan* plan, int which, char* buf, size_t cap, si
  * 2 = contraction kernel for a C-channel layer); CPU-only OK. */
 int wino_plan_cubin(wino_plan* plan, int which, int channels, void* buf, size_t cap, size_t* len);
 
+/* Compile, concurrently on host threads, the generated kernels a layer shape
+ * will launch (flags: WINO_PREPARE_*).  Optional -- every entry point compiles
+ * what it needs on first use; this only overlaps the NVRTC work.  CPU-only OK.
+ * Compiled cubins are cached on disk ($WINO_CACHE_DIR, else kcache/ next to
+ * libwino.so), keyed by a hash of the generated source and NVRTC options. */
+#define WINO_PREPARE_CONV 1   /* K1+K2, K3, K4 of wino_conv2d */
+#define WINO_PREPARE_ACT 2    /* K4 with ReLU / max-pool (wino_output_transform_act) */
+#define WINO_PREPARE_STAGES 4 /* wino_filter_transform / wino_input_transform alone */
+int wino_plan_prepare(wino_plan* plan, const wino_layer_shape* s, int flags);
+
 /* ---- layer-level Winograd convolution (new entry point; the reference
  *      composes it from engine.py:401-429 per tile) --------- */
 int wino_layer_layout_query(const wino_plan* plan, const wino_layer_shape* s,

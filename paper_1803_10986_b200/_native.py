@@ -43,6 +43,8 @@ class LayerLayout(ctypes.Structure):
                 ("workspace_bytes", c_size_t)]
 
 
+PREPARE_CONV, PREPARE_ACT, PREPARE_STAGES = 1, 2, 4  # wino_plan_prepare flags (include/wino.h)
+
 # (name, restype, argtypes) of every exported symbol, in include/wino.h order
 SIGNATURES = [
     ("wino_plan_create", c_int, [c_int, c_int, c_int, c_int, c_int, POINTER(WinoProg), POINTER(WinoProg),
@@ -50,6 +52,7 @@ SIGNATURES = [
     ("wino_plan_destroy", None, [c_void_p]),
     ("wino_plan_source", c_int, [c_void_p, c_int, c_char_p, c_size_t, POINTER(c_size_t)]),
     ("wino_plan_cubin", c_int, [c_void_p, c_int, c_int, c_void_p, c_size_t, POINTER(c_size_t)]),
+    ("wino_plan_prepare", c_int, [c_void_p, POINTER(LayerShape), c_int]),
     ("wino_layer_layout_query", c_int, [c_void_p, POINTER(LayerShape), POINTER(LayerLayout)]),
     ("wino_filter_transform", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p]),
     ("wino_input_transform", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p]),

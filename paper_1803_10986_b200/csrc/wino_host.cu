@@ -9,8 +9,13 @@
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
+#include <dlfcn.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <atomic>
+#include <cctype>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -19,6 +24,7 @@
 #include <mutex>
 #include <sstream>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "codegen.h"
@@ -91,14 +97,85 @@ struct Compiled {
     std::string log;
 };
 
+static const char* const kNvrtcOpts[] = {"-arch=sm_100a", "-fmad=false", "-lineinfo", "-std=c++17",
+                                         "-default-device", "--ptxas-options=-v"};
+
+// ---- on-disk cubin cache: <dir>/<module>-<128-bit FNV-1a of (options, source)>.cubin.
+// dir = $WINO_CACHE_DIR, else kcache/ next to libwino.so (in-tree, git-ignored, so a
+// cache filled here by build() travels with the snapshot to the GPU box).  Entries
+// are written atomically (temp file + rename); unreadable or short files are ignored.
+static std::string cache_dir() {
+    static const std::string dir = [] {
+        if (const char* e = std::getenv("WINO_CACHE_DIR")) return std::string(e);
+        Dl_info info;
+        if (dladdr((void*)&cache_dir, &info) && info.dli_fname) {
+            std::string so = info.dli_fname;
+            const size_t k = so.rfind('/');
+            return (k == std::string::npos ? std::string(".") : so.substr(0, k)) + "/kcache";
+        }
+        return std::string();
+    }();
+    return dir;
+}
+
+static std::string cache_key(const std::string& text) {
+    uint64_t a = 1469598103934665603ull, b = 0x9ae16a3b2f90404full;
+    for (unsigned char c : text) {
+        a = (a ^ c) * 1099511628211ull;
+        b = (b ^ c) * 0x100000001b3ull + 0x2545f4914f6cdd1dull;
+    }
+    char buf[40];
+    std::snprintf(buf, sizeof buf, "%016llx%016llx", (unsigned long long)a, (unsigned long long)b);
+    return buf;
+}
+
+static bool cache_load(const std::string& path, std::vector<char>* out) {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) return false;
+    std::vector<char> data;
+    char tmp[1 << 16];
+    size_t k;
+    while ((k = std::fread(tmp, 1, sizeof tmp, f)) > 0) data.insert(data.end(), tmp, tmp + k);
+    std::fclose(f);
+    // ELF magic + a sane size: a torn or foreign file is recompiled
+    if (data.size() < 64 || data[0] != 0x7f || data[1] != 'E' || data[2] != 'L' || data[3] != 'F') return false;
+    out->swap(data);
+    return true;
+}
+
+static void cache_store(const std::string& path, const std::vector<char>& cubin) {
+    const std::string dir = path.substr(0, path.rfind('/'));
+    mkdir(dir.c_str(), 0775);
+    const std::string tmp = path + ".tmp" + std::to_string((long long)getpid()) + "_" +
+                            std::to_string((unsigned long long)std::hash<std::thread::id>{}(std::this_thread::get_id()));
+    FILE* f = std::fopen(tmp.c_str(), "wb");
+    if (!f) return;
+    const bool ok = std::fwrite(cubin.data(), 1, cubin.size(), f) == cubin.size();
+    if (std::fclose(f) == 0 && ok) {
+        std::rename(tmp.c_str(), path.c_str());
+    } else {
+        std::remove(tmp.c_str());
+    }
+}
+
 static int nvrtc_compile(const std::string& src, const std::string& name, Compiled* out, int maxreg = 0) {
+    std::vector<const char*> opts(std::begin(kNvrtcOpts), std::end(kNvrtcOpts));
+    std::string mr = "-maxrregcount=" + std::to_string(maxreg);
+    if (maxreg > 0) opts.push_back(mr.c_str());
+    int major = 0, minor = 0;
+    nvrtcVersion(&major, &minor);
+    std::string keytext = "nvrtc " + std::to_string(major) + "." + std::to_string(minor);
+    for (const char* o : opts) keytext += std::string(" ") + o;
+    keytext += "\n" + src;
+    const std::string dir = cache_dir();
+    const std::string path = dir.empty() ? std::string() : dir + "/" + name + "-" + cache_key(keytext) + ".cubin";
+    if (!path.empty() && cache_load(path, &out->cubin)) {
+        out->log = "(cubin cache: " + path + ")";
+        return WINO_OK;
+    }
     nvrtcProgram prog;
     nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), name.c_str(), 0, nullptr, nullptr);
     if (r != NVRTC_SUCCESS) return fail(WINO_ECOMPILE, std::string("nvrtcCreateProgram: ") + nvrtcGetErrorString(r));
-    std::vector<const char*> opts = {"-arch=sm_100a", "-fmad=false", "-lineinfo", "-std=c++17", "-default-device",
-                                     "--ptxas-options=-v"};
-    std::string mr = "-maxrregcount=" + std::to_string(maxreg);
-    if (maxreg > 0) opts.push_back(mr.c_str());
     r = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
     size_t ls = 0;
     nvrtcGetProgramLogSize(prog, &ls);
@@ -113,29 +190,112 @@ static int nvrtc_compile(const std::string& src, const std::string& name, Compil
     out->cubin.resize(cs);
     nvrtcGetCUBIN(prog, out->cubin.data());
     nvrtcDestroyProgram(&prog);
+    if (!path.empty()) cache_store(path, out->cubin);
     return WINO_OK;
 }
 
-// A generated module: source, cubin, and per-device loaded CUmodule/functions.
+// Wrap every `extern "C" __global__` definition of a generated source in
+//   #if defined(WINO_KALL) || defined(WINO_K_<name>) ... #endif
+// so one NVRTC program per kernel compiles only that kernel (the shared device
+// functions are static inline: unreferenced ones cost nothing).  Straight-line
+// transform code makes NVRTC time grow steeply with alpha, and a layer source
+// holds up to nine kernel variants of which a call path uses two or three.
+static std::string wrap_kernels(const std::string& s) {
+    static const std::string tag = "extern \"C\" __global__";
+    std::string out;
+    out.reserve(s.size() + 4096);
+    size_t i = 0;
+    while (true) {
+        const size_t j = s.find(tag, i);
+        if (j == std::string::npos) {
+            out.append(s, i, std::string::npos);
+            break;
+        }
+        out.append(s, i, j - i);
+        size_t p = s.find('(', j + tag.size());
+        // `__launch_bounds__(...)` precedes the kernel name
+        const size_t lb = s.find("__launch_bounds__", j);
+        if (lb != std::string::npos && lb < p) {
+            int d = 0;
+            size_t q = p;
+            for (; q < s.size(); ++q) {
+                if (s[q] == '(') ++d;
+                if (s[q] == ')' && --d == 0) break;
+            }
+            p = s.find('(', q + 1);
+        }
+        size_t ne = p;
+        while (ne > 0 && (s[ne - 1] == ' ' || s[ne - 1] == '\n')) --ne;
+        size_t nb = ne;
+        while (nb > 0 && (std::isalnum((unsigned char)s[nb - 1]) || s[nb - 1] == '_')) --nb;
+        const std::string name = s.substr(nb, ne - nb);
+        int d = 0;
+        size_t q = p;
+        for (; q < s.size(); ++q) {  // end of the parameter list
+            if (s[q] == '(') ++d;
+            if (s[q] == ')' && --d == 0) break;
+        }
+        size_t e = s.find('{', q);
+        d = 0;
+        for (; e < s.size(); ++e) {  // matching brace of the body (generated code: no braces in comments)
+            if (s[e] == '/' && e + 1 < s.size() && s[e + 1] == '/') {
+                e = s.find('\n', e);
+                continue;
+            }
+            if (s[e] == '{') ++d;
+            if (s[e] == '}' && --d == 0) break;
+        }
+        out += "#if defined(WINO_KALL) || defined(WINO_K_" + name + ")\n";
+        out.append(s, j, e + 1 - j);
+        out += "\n#endif\n";
+        i = e + 1;
+    }
+    return out;
+}
+
+// A generated module: source, and one cubin per kernel (compiled on first use,
+// concurrently for different kernels), loaded per device.
 struct Module {
     std::string name, source;
     int maxreg = 0;  // NVRTC -maxrregcount (0 = compiler default)
-    Compiled bin;
-    bool compiled = false;
-    std::mutex mu;
-    std::map<int, CUmodule> mods;
+    struct Bin {
+        std::mutex mu;
+        bool done = false;
+        Compiled bin;
+    };
+    std::mutex mu;  // guards the maps below (never held while compiling)
+    std::string wrapped;
+    std::map<std::string, std::unique_ptr<Bin>> bins;  // kernel name ("*": all kernels)
+    std::map<std::pair<int, std::string>, CUmodule> mods;
     std::map<std::pair<int, std::string>, CUfunction> fns;
 
-    int ensure_compiled() {
+    Bin* bin_of(const std::string& kernel) {
         std::lock_guard<std::mutex> g(mu);
-        if (compiled) return WINO_OK;
-        int rc = nvrtc_compile(source, name, &bin, maxreg);
-        if (rc == WINO_OK) compiled = true;
-        return rc;
+        if (wrapped.empty()) wrapped = wrap_kernels(source);
+        auto& b = bins[kernel];
+        if (!b) b = std::make_unique<Bin>();
+        return b.get();
+    }
+
+    // cubin holding `kernel` ("*": every kernel of the source)
+    int ensure_compiled(const std::string& kernel, const Compiled** out = nullptr) {
+        Bin* b = bin_of(kernel);
+        std::lock_guard<std::mutex> g(b->mu);
+        if (!b->done) {
+            const std::string def = kernel == "*" ? std::string("#define WINO_KALL 1\n")
+                                                  : "#define WINO_K_" + kernel + " 1\n";
+            const std::string nm = name.substr(0, name.size() - 3) + (kernel == "*" ? "" : "." + kernel) + ".cu";
+            int rc = nvrtc_compile(def + wrapped, nm, &b->bin, maxreg);
+            if (rc) return rc;
+            b->done = true;
+        }
+        if (out) *out = &b->bin;
+        return WINO_OK;
     }
 
     int function(const char* fname, CUfunction* f) {
-        int rc = ensure_compiled();
+        const Compiled* bin = nullptr;
+        int rc = ensure_compiled(fname, &bin);
         if (rc) return rc;
         Driver& d = driver();
         if (!d.ok) return fail(WINO_ECUDA, d.err);
@@ -149,21 +309,39 @@ struct Module {
             *f = it->second;
             return WINO_OK;
         }
-        if (!mods.count(dev)) {
+        if (!mods.count(key)) {
             cudaFree(nullptr);  // make the runtime's primary context current
             CUmodule mod;
-            CUresult cr = d.ModuleLoadData(&mod, bin.cubin.data());
+            CUresult cr = d.ModuleLoadData(&mod, bin->cubin.data());
             if (cr != CUDA_SUCCESS) return fail(WINO_ECUDA, "cuModuleLoadData(" + name + "): " + cu_err(cr));
-            mods[dev] = mod;
+            mods[key] = mod;
         }
         CUfunction fn;
-        CUresult cr = d.ModuleGetFunction(&fn, mods[dev], fname);
+        CUresult cr = d.ModuleGetFunction(&fn, mods[key], fname);
         if (cr != CUDA_SUCCESS) return fail(WINO_ECUDA, std::string("cuModuleGetFunction(") + fname + "): " + cu_err(cr));
         fns[key] = fn;
         *f = fn;
         return WINO_OK;
     }
 };
+
+// Compile (module, kernel) pairs concurrently, one host thread each (NVRTC is
+// thread-safe; a layer plan needs two to four kernels whose compile times add up).
+static int compile_all(const std::vector<std::pair<Module*, std::string>>& work) {
+    if (work.size() <= 1) return work.empty() ? WINO_OK : work[0].first->ensure_compiled(work[0].second);
+    std::vector<int> rcs(work.size(), WINO_OK);
+    std::vector<std::string> errs(work.size());
+    std::vector<std::thread> th;
+    for (size_t i = 0; i < work.size(); ++i)
+        th.emplace_back([&, i] {
+            rcs[i] = work[i].first->ensure_compiled(work[i].second);
+            if (rcs[i]) errs[i] = g_last_error;  // thread-local: carry it to the caller's thread
+        });
+    for (auto& t : th) t.join();
+    for (size_t i = 0; i < work.size(); ++i)
+        if (rcs[i]) return fail(rcs[i], errs[i]);
+    return WINO_OK;
+}
 
 static int launch(CUfunction f, dim3 grid, dim3 block, unsigned smem, void* stream, void** args, const char* what) {
     if (grid.x == 0 || grid.y == 0 || grid.z == 0) return WINO_OK;
@@ -584,11 +762,39 @@ int wino_plan_cubin(wino_plan* plan, int which, int channels, void* buf, size_t 
     wino::Module* mod = which == 0 ? &plan->layer
                         : which == 1 ? &plan->tile
                                      : plan->contract_module(round_up(channels > 0 ? channels : 1, plan->gemm.bk));
-    int rc = mod->ensure_compiled();
+    const wino::Compiled* bin = nullptr;
+    int rc = mod->ensure_compiled("*", &bin);
     if (rc) return rc;
-    if (len) *len = mod->bin.cubin.size();
-    if (buf && cap >= mod->bin.cubin.size()) std::memcpy(buf, mod->bin.cubin.data(), mod->bin.cubin.size());
+    if (len) *len = bin->cubin.size();
+    if (buf && cap >= bin->cubin.size()) std::memcpy(buf, bin->cubin.data(), bin->cubin.size());
     return WINO_OK;
+}
+
+int wino_plan_prepare(wino_plan* plan, const wino_layer_shape* s, int flags) {
+    wino_layer_layout L;
+    int rc = layout_of(plan, s, &L);
+    if (rc) return rc;
+    if (plan->mode >= WINO_CONTRACT_TC_BF16) return WINO_OK;  // tensor-core plans compile on first use
+    const int ci = plan->pick(s);
+    wino::Module* lm = plan->layer_mod(ci);
+    std::vector<std::pair<wino::Module*, std::string>> work;
+    int smem = 0;
+    const int tb = xform_block(plan, &smem);
+    const long long n_tb = (L.Tp + tb - 1) / tb, n_kb = (L.Kp + tb - 1) / tb;
+    if (flags & WINO_PREPARE_CONV) {
+        work.push_back({lm, k1_gather() && n_tb + n_kb <= 65535 && L.Cp <= 65535 ? "wino_transforms_gather"
+                                                                                  : "wino_transforms"});
+        work.push_back({plan->contract_module(L.Cp, ci), "wino_contract"});
+        work.push_back({lm, k4_gather() && s->K <= 65535 ? "wino_output_gather"
+                            : plan->m <= 2               ? "wino_output_flat"
+                                                         : "wino_output_xform"});
+    }
+    if ((flags & WINO_PREPARE_ACT) && !plan->ty.y_double) work.push_back({lm, "wino_output_gather_act"});
+    if (flags & WINO_PREPARE_STAGES) {
+        work.push_back({lm, "wino_filter_xform"});
+        work.push_back({lm, k1_gather() && n_tb <= 65535 && L.Cp <= 65535 ? "wino_input_gather" : "wino_input_xform"});
+    }
+    return wino::compile_all(work);
 }
 
 int wino_layer_layout_query(const wino_plan* plan, const wino_layer_shape* s, wino_layer_layout* out) {

@@ -52,6 +52,12 @@ class LayerOp:
         self.out_shape = (N, K, self.layout.Ho, self.layout.Wo)
         self.in_dtype = _input_dtype(cfg)
         self.out_dtype = _output_dtype(cfg)
+        self.prepare(_native.PREPARE_CONV)
+
+    def prepare(self, flags):
+        """Compile (concurrently, cached on disk) the generated kernels this layer launches."""
+        _native.check(_native.lib().wino_plan_prepare(self.plan.handle, ctypes.byref(self.shape), flags),
+                      "plan_prepare")
 
     @property
     def direct_flops(self) -> int:

@@ -51,6 +51,8 @@ class ConvStack:
         h, w = H, W
         for C, K, pool in self.layers:
             op = layer_op(ts, cfg, N, C, h, w, K, pad, contraction)
+            if not op.tensor_core:
+                op.prepare(_native.PREPARE_CONV | _native.PREPARE_ACT)
             self.ops.append(op)
             self.shapes.append((C, K, h, w, pool))
             h, w = op.layout.Ho, op.layout.Wo
