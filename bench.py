@@ -757,6 +757,58 @@ def measure_peaks(lib, _native, torch):
     return res
 
 
+def run_dryrun(args):
+    """--dry-run: the multi-rank plumbing of the vgg16 bench on CPU ranks (gloo):
+    rank environment, the batch shard of each rank, barrier + MAX-over-ranks step
+    time, and the ordered all-gather of per-image error partials -- with the device
+    forward replaced by the oracle's first VGG layer on small synthetic images.
+    No GPU is touched; used by the launcher test."""
+    import torch
+    import torch.distributed as dist
+    from oracle import wino_oracle as O
+    from paper_1803_10986_b200 import distributed as Dd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    a, b = Dd.shard_range(args.vgg_batch, rank, world)
+    trip = O.Triple.from_points(3, 6, VGG_POINTS)
+    w = O.synthetic((8, 3, 3, 3), 2024, 10_000_000)
+
+    def step(idx):
+        x = np.stack([synth((3, 12, 12), 2024, i, "uniform") for i in idx]) if len(idx) else \
+            np.zeros((0, 3, 12, 12), np.float32)
+        y = O.layer_conv2d(trip, x, w, 1, "fp32", "huffman", "pairwise") if len(idx) else \
+            np.zeros((0, 8, 12, 12), np.float32)
+        return x, y
+
+    for _ in range(args.warmup):
+        step(range(a, b))
+    ts = []
+    for _ in range(args.steps):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        x, y = step(range(a, b))
+        ts.append(time.perf_counter() - t0)
+    ms = Dd.max_over_ranks(1e3 * float(np.mean(ts)))
+    y64 = O.layer_direct_fp64(x, w, 1) if b > a else np.zeros((0, 8, 12, 12))
+    st = np.stack(O.layer_error_stats(y, y64), axis=1).astype(np.float64) if b > a else np.zeros((0, 4))
+    allst = Dd.gather_ordered(torch.from_numpy(np.ascontiguousarray(st))).numpy()
+    spans = Dd.gather_ordered(torch.tensor([[a, b]], dtype=torch.int64)).tolist()
+    err = Dd.combine_layer_stats(allst)
+    if rank == 0:
+        xa, ya = step(range(args.vgg_batch))  # one-process reference of the same statistics
+        one = Dd.combine_layer_stats(np.stack(O.layer_error_stats(ya, O.layer_direct_fp64(xa, w, 1)), axis=1))
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": ms, "shards": spans,
+                          "error_images": err["images"], "error": err, "error_equals_one_process": err == one}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def spawn_ranks(args):
     """`--gpus N` without a torchrun environment: re-exec this script under
     torch.distributed.run with N local ranks (127.0.0.1 rendezvous); the ranks'
@@ -789,6 +841,7 @@ def parse_args(argv=None):
     ap.add_argument("--soak", type=float, default=1.5, help="seconds of untimed load before the timed region")
     ap.add_argument("--e2e-chunks", default="4", help="image chunks of the e2e pipeline: a count or sizes a,b,...")
     ap.add_argument("--ncu", action="store_true", help="profiling mode: warm-up + K eager steps only, no output")
+    ap.add_argument("--dry-run", action="store_true", help="CPU/gloo rehearsal of the multi-rank plumbing (no GPU)")
     return ap.parse_args(argv)
 
 
@@ -796,6 +849,9 @@ def main():
     args = parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args))
+    if args.dry_run:
+        run_dryrun(args)
+        return
     if args.config == "vgg16":
         (run_reference_vgg if args.impl == "reference" else run_vgg)(args)
         return

@@ -457,9 +457,10 @@ def trial_draw(seed, trial, dims, r, n, channels=1):
 
 
 def measure_error(trip, dims, precision="fp32", order="huffman", csum="linear",
-                  trials=5000, seed=0, channels=1, direct=False, chunk=None):
+                  trials=5000, seed=0, channels=1, direct=False, chunk=None, t0=0):
     """Returns (per_trial L1 array, total_l1_mean, per_point_l1_mean)
-    (harness.py:116-183).  `trip` may be None with direct=True (DirectSpec)."""
+    (harness.py:116-183).  `trip` may be None with direct=True (DirectSpec).
+    t0 > 0: trials t0 .. t0+trials-1 (one rank's shard; draws keyed by trial index)."""
     r = 3 if trip is None else trip.r
     m = 1 if trip is None else trip.m
     n = r + m - 1
@@ -469,7 +470,7 @@ def measure_error(trip, dims, precision="fp32", order="huffman", csum="linear",
     per = np.empty(trials, dtype=np.float64)
     for s in range(0, trials, chunk):
         e = min(trials, s + chunk)
-        pairs = [trial_draw(seed, t, dims, r, n, channels) for t in range(s, e)]
+        pairs = [trial_draw(seed, t0 + t, dims, r, n, channels) for t in range(s, e)]
         hb = np.stack([p[0] for p in pairs])
         xb = np.stack([p[1] for p in pairs])
         ref = reduce_channels(direct_products(hb, xb, dims, "fp64"), -(dims + 1), "linear")

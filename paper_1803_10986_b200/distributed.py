@@ -105,31 +105,66 @@ def combine_layer_stats(stats: np.ndarray) -> dict:
             "max_abs": mx, "images": int(s.shape[0])}
 
 
-def measure_error_sharded(spec, dims, cfg, trials=5000, seed=0, channels=1):
+def trial_counts(trials: int, size: int) -> list[int]:
+    """Trials per rank of a contiguous split (shard_range)."""
+    return [shard_range(trials, r, size)[1] - shard_range(trials, r, size)[0] for r in range(size)]
+
+
+def gather_trials(local: torch.Tensor, trials: int) -> torch.Tensor:
+    """This rank's per-trial L1 values -> the full per-trial vector in trial order
+    (identical on every rank).  Trials are keyed Philox(seed, trial) by the
+    reference (harness.py:97-107), so the gathered vector equals the one-process
+    vector bit for bit whatever the world size."""
+    rank, size = world()
+    counts = trial_counts(trials, size)
+    if local.shape[0] != counts[rank]:
+        raise ValueError("local trial count does not match this rank's shard")
+    return gather_ordered(local, counts).contiguous()
+
+
+def measure_error_sharded(spec, dims, cfg, trials=5000, seed=0, channels=1, local_eval=None, mean=None):
     """measure_error with the trials split across ranks: each rank evaluates a
     contiguous slice, the per-trial L1 values are gathered in trial order and
     the mean is taken over the full vector on every rank -- the report equals
-    the single-GPU one bit for bit."""
-    from . import _native
-    from . import device as D
-    from .harness import ErrorReport, _measure_variants
+    the single-GPU one bit for bit.
+
+    local_eval(start, stop) -> per-trial L1 (float64) of trials start..stop-1 and
+    mean(vector) -> float default to the device paths (libwino Monte-Carlo kernels,
+    numpy-ordered device mean); tests substitute host versions to exercise the
+    sharding and gather logic on CPU ranks (gloo)."""
+    from .harness import ErrorReport
 
     rank, size = world()
     start, stop = shard_range(trials, rank, size)
-    if stop > start:
-        part = _measure_variants(spec, dims, cfg, stop - start, seed, channels, (cfg.channel_sum,),
-                                 t0=start)[cfg.channel_sum]
-        local = torch.from_numpy(part.per_trial).to("cuda")
+    if local_eval is None:
+        local_eval = _device_trials(spec, dims, cfg, seed, channels)
+        dev = "cuda"
     else:
-        local = torch.empty(0, dtype=torch.float64, device="cuda")
-    counts = [shard_range(trials, r, size)[1] - shard_range(trials, r, size)[0] for r in range(size)]
-    per = gather_ordered(local, counts).contiguous()
-    mean = D.torch.empty(1, dtype=D.torch.float64, device="cuda")
-    _native.check(_native.lib().wino_mean_f64(trials, D.ptr(per), D.ptr(mean), D.stream_handle()), "mean")
-    total = float(mean.item())
+        dev = "cpu"
+    part = local_eval(start, stop) if stop > start else np.zeros(0, dtype=np.float64)
+    local = torch.as_tensor(np.ascontiguousarray(part, dtype=np.float64), device=dev)
+    per = gather_trials(local, trials)
+    total = float(mean(per) if mean is not None else _device_mean(per))
     n_out = spec.n_o ** dims
     return ErrorReport(descriptor=spec.descriptor(), dims=dims, channels=channels,
                        config={"precision": cfg.precision, "dot_order": cfg.dot_order,
                                "channel_sum": cfg.channel_sum},
                        trials=trials, seed=seed, total_l1_mean=total, per_point_l1_mean=total / n_out,
                        n_outputs=n_out, per_trial=per.cpu().numpy())
+
+
+def _device_trials(spec, dims, cfg, seed, channels):
+    from .harness import _measure_variants
+
+    def run(start, stop):
+        return _measure_variants(spec, dims, cfg, stop - start, seed, channels, (cfg.channel_sum,),
+                                 t0=start)[cfg.channel_sum].per_trial
+    return run
+
+
+def _device_mean(per: torch.Tensor) -> float:
+    from . import _native
+    from . import device as D
+    mean = D.torch.empty(1, dtype=D.torch.float64, device="cuda")
+    _native.check(_native.lib().wino_mean_f64(per.shape[0], D.ptr(per), D.ptr(mean), D.stream_handle()), "mean")
+    return float(mean.item())

@@ -75,3 +75,64 @@ def test_layer_shards_cover_outputs_once():
                 assert (seen == 1).all(), (N, K, size, by)
     with pytest.raises(ValueError):
         Dd.layer_shard(4, 4, 0, 2, "pixels")
+
+
+def _measure_worker(rank, size, port, out):
+    import paper_1803_10986_b200 as W
+    from oracle import wino_oracle as O
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    try:
+        pts = "0,1,-1,1/2,-1/2,inf"
+        ts = W.build_transforms(3, 4, W.parse_points(pts))
+        trip = O.Triple.from_points(3, 4, pts)
+        cfg = W.ConvConfig("fp32", "huffman", "pairwise")
+
+        def local_eval(a, b):  # host stand-in for the device Monte-Carlo kernels
+            return O.measure_error(trip, 2, "fp32", "huffman", "pairwise", trials=b - a, seed=3, channels=4,
+                                   t0=a)[0]
+
+        rep = Dd.measure_error_sharded(ts, 2, cfg, trials=37, seed=3, channels=4, local_eval=local_eval,
+                                       mean=lambda per: float(np.mean(per.numpy())))
+        out[rank] = (rep.per_trial.tobytes(), repr(rep.total_l1_mean), rep.trials, rep.per_point_l1_mean)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world_size_2_measure_error_sharded_equals_one_process():
+    """The sharded Monte-Carlo measurement (contiguous trial shards, per-trial L1
+    gathered in trial order) reproduces the one-process report bit for bit
+    (reference harness.py:97-107: draws keyed by (seed, trial))."""
+    from oracle import wino_oracle as O
+    size = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_measure_worker, args=(size, port, out), nprocs=size, join=True)
+    trip = O.Triple.from_points(3, 4, "0,1,-1,1/2,-1/2,inf")
+    per, tot, pp = O.measure_error(trip, 2, "fp32", "huffman", "pairwise", trials=37, seed=3, channels=4)
+    for r in range(size):
+        per_b, tot_r, trials, pp_r = out[r]
+        assert per_b == per.tobytes() and tot_r == repr(tot) and trials == 37 and pp_r == tot / 16
+
+
+def test_bench_launcher_spawns_ranks():
+    """`bench.py --gpus 2` with no torchrun environment re-execs itself under
+    torch.distributed.run; the --dry-run rehearsal runs the multi-rank plumbing
+    (rank env, batch shards, MAX-over-ranks timing, ordered gather of per-image
+    error partials) on CPU/gloo and rank 0 prints one JSON line."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    res = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run",
+                          "--vgg-batch", "6", "--steps", "2", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, res.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["dry_run"] is True
+    assert d["shards"] == [[0, 3], [3, 6]]
+    assert d["error_images"] == 6 and d["error_equals_one_process"] is True
