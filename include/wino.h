@@ -139,7 +139,13 @@ int wino_plan_prepare(wino_plan* plan, const wino_layer_shape* s, int flags);
  *      composes it from engine.py:401-429 per tile) --------- */
 int wino_layer_layout_query(const wino_plan* plan, const wino_layer_shape* s,
                             wino_layer_layout* out);
-/* K2: U = (G w) G^T per (k, c)                 -- engine.py:409,411 */
+/* K2: U = (G w) G^T per (k, c)                 -- engine.py:409,411
+ * U's blocking ([P][Kp/bm][Cp][bm]) follows the contraction tile the plan picks
+ * for the WHOLE shape, batch size N included (wino_layer_layout_query: bm, Cp,
+ * Kp).  A U computed for one shape may be reused with wino_contract for another
+ * shape only if both layout queries report the same (bm, Cp, Kp); wino_contract
+ * cannot detect a mismatch from the pointer.  HostPipeline keeps one U per
+ * blocking for this reason. */
 int wino_filter_transform(wino_plan* plan, const wino_layer_shape* s, const void* w,
                           void* U, void* stream);
 /* K1: V = (B^T d) B per (tile, c), tile gather + zero padding fused -- engine.py:410,412 */
@@ -237,6 +243,13 @@ int wino_peak_probe(int mode, int blocks, int iters, float* out, void* stream);
 /* number of kernels this library has launched in the calling process */
 int64_t wino_launch_count(void);
 const char* wino_last_error(void);
+/* Tuning hooks for tools/ sweeps and variant tests (the product never sets them):
+ * key "gemm" = contraction tile "tm,tn,thm,thn,bk,stages,maxreg[,ku,noprod,pack]"
+ * (plans created afterwards), "dbuf", "tcf_nk" (same), "k1" = "tile", "k1order" =
+ * "t", "k4" = "staged", "k1tc" = "4x8", "tile_interp" = "0|1", "cpt" / "kpt" =
+ * 1|2|4|8, "tcf_dbg", "tc_epi" (read once per process, before the first launch).
+ * value NULL or "" clears the key.  Unknown keys -> WINO_EINVAL. */
+int wino_tuning_set(const char* key, const char* value);
 const char* wino_version(void);
 
 #ifdef __cplusplus

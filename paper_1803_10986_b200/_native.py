@@ -81,6 +81,7 @@ SIGNATURES = [
     ("wino_peak_probe", c_int, [c_int, c_int, c_int, c_void_p, c_void_p]),
     ("wino_launch_count", c_int64, []),
     ("wino_last_error", c_char_p, []),
+    ("wino_tuning_set", c_int, [c_char_p, c_char_p]),
     ("wino_version", c_char_p, []),
 ]
 
@@ -165,6 +166,12 @@ class Plan:
         out = LayerLayout()
         check(lib().wino_layer_layout_query(self.handle, ctypes.byref(s), ctypes.byref(out)), "layout")
         return out
+
+
+def set_tuning(key: str, value) -> None:
+    """Tools / variant tests only: select an alternative kernel form or tile config
+    (include/wino.h wino_tuning_set); value None clears the key."""
+    check(lib().wino_tuning_set(key.encode(), None if value is None else str(value).encode()), "tuning_set")
 
 
 def launch_count() -> int:

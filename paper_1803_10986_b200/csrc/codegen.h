@@ -51,24 +51,26 @@ std::string gen_tile_source(int r, int m, const MatProg& G, const MatProg& BT, c
 
 // Gather transforms: channels per K1 thread / output channels per K4 thread (the
 // tile index math is amortised over them).  Must divide every channel padding
-// (Cp is a multiple of 8).  WINO_CPT / WINO_KPT override (1, 2, 4 or 8).  A rolled
+// (Cp is a multiple of 8).  Tuning keys "cpt" / "kpt" override (1, 2, 4 or 8; read
+// once per process, before the first plan, so generated code and launch grids agree).  A rolled
 // loop over channels is slower (tools/sweeps/sweep_xpt.sh: fewer loads in flight --
 // cfg3 m=6 K4 38.9 / 65.8 / 77.1 us at 1 / 4 / 8 filters per thread); K4 keeps 1.
-inline int env_pow2(const char* name, int dflt) {
-    const char* e = std::getenv(name);
-    const int v = e ? std::atoi(e) : dflt;
+std::string tuning(const char* key);  // wino_host.cu registry (wino_tuning_set)
+inline int tuning_pow2(const char* name, int dflt) {
+    const std::string e = tuning(name);
+    const int v = e.empty() ? dflt : std::atoi(e.c_str());
     return (v == 1 || v == 2 || v == 4 || v == 8) ? v : dflt;
 }
 // channels per K1 thread: 2 for alpha^2 <= 16 (the two windows are gathered and
 // transformed in one unrolled body: more loads in flight, half the index math;
 // cfg2 K1 14.7 -> 12.7 us), 1 for larger alpha (register pressure: cfg3 m=6
-// 39 -> 54 us at 2).  WINO_CPT overrides.
+// 39 -> 54 us at 2).  Tuning key "cpt" overrides.
 inline int gather_cpt(int P) {
-    static const int v = env_pow2("WINO_CPT", 0);
+    static const int v = tuning_pow2("cpt", 0);
     return v ? v : (P <= 16 ? 2 : 1);
 }
 inline int gather_kpt() {
-    static const int v = env_pow2("WINO_KPT", 1);
+    static const int v = tuning_pow2("kpt", 1);
     return v;
 }
 

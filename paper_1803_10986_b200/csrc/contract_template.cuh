@@ -283,6 +283,8 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
         // Z: static counter inside a stage (a stage = WINO_BK/8 chunks of 8 channels);
         // slot: dynamic counter over stages (slot j holds 2^j stages)
 #define ZL (WINO_BK == 8 ? 1 : WINO_BK == 16 ? 1 : WINO_BK == 32 ? 2 : 3)
+        static_assert(WINO_BK == 8 || WINO_BK == 16 || WINO_BK == 32 || WINO_BK == 64,
+                      "pairwise stages: the in-stage counter covers 8, 16, 32 or 64 channels");
         acc_t zs[ZL][WINO_TM][NJ];
         acc_t slot[WINO_LEVELS][WINO_TM][NJ];
 #endif

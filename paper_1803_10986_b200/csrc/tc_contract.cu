@@ -19,6 +19,9 @@
 //               the smem stage / publishes the finished accumulator
 //   warps 2-5   epilogue: tcgen05.ld TMEM -> registers -> M (fp32) while the
 //               next tile accumulates into the other TMEM buffer
+#include <mutex>
+#include <set>
+#include <string>
 #include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -290,15 +293,28 @@ __global__ void __launch_bounds__(192, 1) tc_contract_kernel(const unsigned shor
 
 namespace wino {
 
-// epilogue store form (WINO_TC_EPI): 0 direct per-lane stores, 1 per-row bulk copies,
-// 2 (default) staged in smem and stored as full 128-byte lines
+// epilogue store form (tuning key "tc_epi"): 0 direct per-lane stores, 1 per-row bulk
+// copies, 2 (default) staged in smem and stored as full 128-byte lines
 static int epi_mode() {
     static const int v = [] {
-        const char* e = std::getenv("WINO_TC_EPI");
-        const int x = e ? std::atoi(e) : 2;
+        const std::string e = tuning("tc_epi");
+        const int x = e.empty() ? 2 : std::atoi(e.c_str());
         return (x >= 0 && x <= 2) ? x : 2;
     }();
     return v;
+}
+
+// cudaFuncSetAttribute is per device: opt in once for every device a process drives
+int tc_contract_prepare_device(int dev) {
+    static std::mutex mu;
+    static std::set<int> done;
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count(dev)) return WINO_OK;
+    const size_t smem = (size_t)kEpiOffset + kEpiBytes;
+    cudaError_t e = cudaFuncSetAttribute(tc_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(WINO_ECUDA, std::string("tc_contract: set smem: ") + cudaGetErrorString(e));
+    done.insert(dev);
+    return WINO_OK;
 }
 
 int tc_contract_launch(const void* U, const void* V, void* M, long long Kp, long long Tp, long long Cp, int P,
@@ -307,13 +323,9 @@ int tc_contract_launch(const void* U, const void* V, void* M, long long Kp, long
     const long long tiles = (long long)P * (Kp / TBM) * (Tp / TBN);
     if (tiles > (1LL << 30)) return fail(WINO_EUNSUPPORTED, "tc_contract: too many tiles");
     const size_t smem = (size_t)kEpiOffset + kEpiBytes;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(tc_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
+    if (int rc = tc_contract_prepare_device(dev)) return rc;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = (int)(tiles < sms ? tiles : sms);
     tc_contract_kernel<<<grid, 192, smem, (cudaStream_t)stream>>>((const unsigned short*)U,

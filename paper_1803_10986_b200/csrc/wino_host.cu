@@ -43,6 +43,15 @@ int fail(int code, const std::string& msg) {
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+static std::mutex g_tune_mu;
+static std::map<std::string, std::string> g_tune;
+
+std::string tuning(const char* key) {
+    std::lock_guard<std::mutex> g(g_tune_mu);
+    auto it = g_tune.find(key);
+    return it == g_tune.end() ? std::string() : it->second;
+}
+
 int after_launch(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(WINO_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -501,7 +510,7 @@ struct wino_plan {
            << gemm.stages << "\n#define WINO_SUM " << sum_mode() << "\n#define WINO_LEVELS "
            << (levels > 0 ? levels : 1) << "\n#define WINO_MAXREG " << gemm.maxreg << "\n#define WINO_KU " << (gemm.ku > 0 ? gemm.ku : gemm.bk) << "\n#define WINO_NOPROD " << gemm.noprod
            << "\n#define WINO_PACK " << (gemm.pack && !dbl ? 1 : 0) << "\n"
-           << (std::getenv("WINO_DBUF") ? std::string("#define WINO_DBUF ") + std::getenv("WINO_DBUF") + "\n" : "")
+           << (!wino::tuning("dbuf").empty() ? "#define WINO_DBUF " + wino::tuning("dbuf") + "\n" : std::string())
            << ""
            << wino::kContractTemplate;
         mod->source = os.str();
@@ -590,7 +599,8 @@ int xform_block(const wino_plan* p, int* smem) {
 // block order of the tile kernel: channel fastest (default) or tile chunk fastest (WINO_K1ORDER=t)
 int k1_cfast() {
     static const int v = [] {
-        const char* e = std::getenv("WINO_K1ORDER");
+        const std::string es = wino::tuning("k1order");
+        const char* e = es.empty() ? nullptr : es.c_str();
         return (e && std::string(e) == "t") ? 0 : 1;
     }();
     return v;
@@ -601,7 +611,8 @@ int k1_cfast() {
 // otherwise; WINO_K4=staged)
 bool k4_gather() {
     static const bool v = [] {
-        const char* e = std::getenv("WINO_K4");
+        const std::string es = wino::tuning("k4");
+        const char* e = es.empty() ? nullptr : es.c_str();
         return !(e && std::string(e) == "staged");
     }();
     return v;
@@ -609,7 +620,8 @@ bool k4_gather() {
 
 bool k1_no8() {  // WINO_K1TC=4x8: use the 4-tiles x 8-channels TC kernel also for P <= 16
     static const bool v = [] {
-        const char* e = std::getenv("WINO_K1TC");
+        const std::string es = wino::tuning("k1tc");
+        const char* e = es.empty() ? nullptr : es.c_str();
         return e && std::string(e) == "4x8";
     }();
     return v;
@@ -620,8 +632,8 @@ bool k1_no8() {  // WINO_K1TC=4x8: use the 4-tiles x 8-channels TC kernel also f
 // above that (alpha <= 24) or everywhere with WINO_TILE_INTERP=1.
 bool tile_interp(const wino_plan* p) {
     static const int force = [] {
-        const char* e = std::getenv("WINO_TILE_INTERP");
-        return e ? std::atoi(e) : -1;
+        const std::string e = wino::tuning("tile_interp");
+        return e.empty() ? -1 : std::atoi(e.c_str());
     }();
     if (force >= 0) return force > 0 || p->n > 16;
     return p->n > 10;
@@ -629,7 +641,8 @@ bool tile_interp(const wino_plan* p) {
 
 bool k1_gather() {
     static const bool v = [] {
-        const char* e = std::getenv("WINO_K1");
+        const std::string es = wino::tuning("k1");
+        const char* e = es.empty() ? nullptr : es.c_str();
         return !(e && std::string(e) == "tile");
     }();
     return v;
@@ -641,6 +654,22 @@ bool k1_gather() {
 extern "C" {
 
 const char* wino_last_error(void) { return wino::g_last_error.c_str(); }
+
+int wino_tuning_set(const char* key, const char* value) {
+    static const char* const keys[] = {"gemm", "dbuf", "k1", "k1order", "k4", "k1tc", "tile_interp",
+                                       "cpt", "kpt", "tcf_nk", "tcf_dbg", "tc_epi"};
+    if (!key) return wino::fail(WINO_EINVAL, "tuning_set: null key");
+    bool known = false;
+    for (const char* k : keys) known = known || std::strcmp(k, key) == 0;
+    if (!known) return wino::fail(WINO_EINVAL, std::string("tuning_set: unknown key '") + key + "'");
+    std::lock_guard<std::mutex> g(wino::g_tune_mu);
+    if (value && *value) {
+        wino::g_tune[key] = value;
+    } else {
+        wino::g_tune.erase(key);
+    }
+    return WINO_OK;
+}
 const char* wino_version(void) { return "libwino 0.1 (sm_100a)"; }
 int64_t wino_launch_count(void) { return wino::g_launches.load(); }
 
@@ -667,8 +696,9 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
     if (p->fused()) {
         const int P = n * n;
         p->nk = std::min(256, (512 / P) / 16 * 16);
-        if (const char* e = getenv("WINO_TCF_NK")) {  // tuning: smaller blocks (16 x P <= 256: double-buffered TMEM)
-            const int v = atoi(e);
+        const std::string e = wino::tuning("tcf_nk");  // smaller blocks (16 x P <= 256: double-buffered TMEM)
+        if (!e.empty()) {
+            const int v = atoi(e.c_str());
             if (v >= 16 && v % 16 == 0 && v <= p->nk) p->nk = v;
         }
         if (p->nk < 16) return wino::fail(WINO_EUNSUPPORTED, "fused tensor-core mode needs alpha^2 <= 32");
@@ -702,14 +732,17 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
     else
         p->gemm = {8, 8, 16, 8, 16, 4, 0, 16, 0, 1};
     bool env_gemm = false;
-    if (const char* env = getenv("WINO_GEMM")) {  // tuning override: tm,tn,thm,thn,bk,stages,maxreg
+    const std::string tg = wino::tuning("gemm");  // tuning override: tm,tn,thm,thn,bk,stages,maxreg[,ku,noprod,pack]
+    if (!tg.empty()) {
         wino::GemmCfg g{};
-        const int got = sscanf(env, "%d,%d,%d,%d,%d,%d,%d,%d,%d,%d", &g.tm, &g.tn, &g.thm, &g.thn, &g.bk,
+        const int got = sscanf(tg.c_str(), "%d,%d,%d,%d,%d,%d,%d,%d,%d,%d", &g.tm, &g.tn, &g.thm, &g.thn, &g.bk,
                                &g.stages, &g.maxreg, &g.ku, &g.noprod, &g.pack);
-        if (got >= 7 && g.bk % 8 == 0 && g.tm % 4 == 0 && g.tn % 4 == 0 && (g.ku == 0 || g.bk % g.ku == 0)) {
-            p->gemm = g;
-            env_gemm = true;
-        }
+        // the pairwise in-stage counter (contract_template.cuh) covers stages of 8, 16, 32 or 64 channels
+        const bool bk_ok = channel_sum != WINO_SUM_PAIRWISE || g.bk == 8 || g.bk == 16 || g.bk == 32 || g.bk == 64;
+        if (got < 7 || g.bk % 8 || g.tm % 4 || g.tn % 4 || (g.ku != 0 && g.bk % g.ku) || !bk_ok)
+            return wino::fail(WINO_EINVAL, "tuning gemm: bad tile config '" + tg + "'");
+        p->gemm = g;
+        env_gemm = true;
     }
     p->cands = {p->gemm};
     if (!env_gemm && contract_mode < WINO_CONTRACT_TC_BF16 && !dbl64 && channel_sum != WINO_SUM_PAIRWISE) {
@@ -1064,8 +1097,8 @@ int wino_contract_output(wino_plan* plan, const wino_layer_shape* s, const void*
     long long T = L.T, Tp = L.Tp, Kp = L.Kp, Cp = L.Cp;
     float rtw = 1.0f / tw, rth = 1.0f / th;
     static const int dbg = [] {  // timing experiments only: 1 = no MMAs, 2 = no epilogue, 4 = no y stores
-        const char* e = std::getenv("WINO_TCF_DBG");
-        return e ? atoi(e) : 0;
+        const std::string e = wino::tuning("tcf_dbg");
+        return e.empty() ? 0 : atoi(e.c_str());
     }();
     int dbgv = dbg;
     void* args[] = {(void*)&U, (void*)&V, &y, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp, &Cp, &n_tiles, &rtw, &rth, &dbgv};

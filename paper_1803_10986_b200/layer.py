@@ -27,15 +27,31 @@ _ws_lock = threading.Lock()
 _workspaces: dict = {}
 
 
-def _workspace(nbytes: int):
-    """Per-device grow-only scratch for U, V and M."""
-    dev = D.torch.cuda.current_device()
+def _workspace(nbytes: int, stream: int):
+    """Grow-only scratch for U, V and M, one per (device, stream): calls on different
+    streams (or threads using different streams) never share it.  The buffer is
+    allocated while its stream is current, so when it grows the caching allocator
+    recycles the old block only after the work queued on that stream."""
+    torch = D.torch
+    dev = torch.cuda.current_device()
+    key = (dev, stream)
     with _ws_lock:
-        buf = _workspaces.get(dev)
+        buf = _workspaces.get(key)
         if buf is None or buf.numel() < nbytes:
-            buf = D.torch.empty(max(nbytes, 1 << 20), dtype=D.torch.uint8, device=f"cuda:{dev}")
-            _workspaces[dev] = buf
+            _workspaces.pop(key, None)
+            s = torch.cuda.ExternalStream(stream) if stream != torch.cuda.current_stream().cuda_stream else None
+            with torch.cuda.stream(s) if s is not None else _nullcontext():
+                buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=f"cuda:{dev}")
+            _workspaces[key] = buf
         return buf
+
+
+class _nullcontext:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False
 
 
 class LayerOp:
@@ -75,8 +91,8 @@ class LayerOp:
         L = self.layout
         if out is None:
             out = D.empty(self.out_shape, self.out_dtype)
-        ws = workspace if workspace is not None else _workspace(L.workspace_bytes)
         s = D.stream_handle() if stream is None else stream
+        ws = workspace if workspace is not None else _workspace(L.workspace_bytes, s)
         _native.check(_native.lib().wino_conv2d(self.plan.handle, ctypes.byref(self.shape), D.ptr(x), D.ptr(w),
                                                 D.ptr(out), D.ptr(ws), ws.numel(), s), "conv2d")
         return out

@@ -88,12 +88,12 @@ def _pack_tag(pack):
 @pytest.mark.parametrize("prec", ["fp32", "mixed", "fp64"])
 @pytest.mark.parametrize("cs", ["linear", "pairwise"])
 @pytest.mark.parametrize("pack", ["tile", "pack", "scalar"])
-def test_sass_gate_exact_kernels_have_no_fma(built, prec, cs, pack, monkeypatch):
+def test_sass_gate_exact_kernels_have_no_fma(built, prec, cs, pack, gemm_tuning):
     """Exactness needs every product and sum rounded separately: FMUL/FADD
     (DMUL/DADD) or the packed exact product FFMA2(a, b, uniform -0), never a
     multiply fused into a running sum."""
     if _pack_tag(pack):
-        monkeypatch.setenv("WINO_GEMM", _pack_tag(pack))
+        gemm_tuning(_pack_tag(pack))
     plan = _plan(3, 4, "0,1,-1,1/2,-1/2,inf", prec, cs)
     for which in (0, 1, 2):
         sass = _sass(plan.cubin(which, 128))

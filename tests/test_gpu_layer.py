@@ -50,7 +50,8 @@ RANDOM_CASES = [
 
 @pytest.mark.parametrize("case", RANDOM_CASES, ids=lambda c: f"r{c[0]}m{c[1]}C{c[4]}K{c[5]}")
 @pytest.mark.parametrize("mode", [("fp32", "huffman", "linear"), ("fp32", "linear", "pairwise"),
-                                  ("mixed", "huffman", "pairwise"), ("fp64", "linear", "linear")],
+                                  ("mixed", "huffman", "pairwise"), ("fp64", "linear", "linear"),
+                                  ("fp64", "huffman", "pairwise")],
                          ids=lambda m: "-".join(m))
 def test_layer_vs_oracle(case, mode):
     r, m, pts, N, C, K, H, Wd, pad = case

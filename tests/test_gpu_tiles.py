@@ -1,8 +1,8 @@
 """Every contraction tile configuration a plan can pick (wino_host.cu cands: the
 layout is chosen per layer shape) and the scalar (unpacked) form must give the
 oracle's bits: the tile shape, stage depth and packed f32x2 arithmetic change
-the schedule, never the per-output operation order.  WINO_GEMM forces one
-config for plans created while it is set."""
+the schedule, never the per-output operation order.  The "gemm" tuning key
+(wino_tuning_set) forces one config for plans created while it is set."""
 import numpy as np
 import pytest
 
@@ -35,8 +35,8 @@ CASES = [
 
 @pytest.mark.parametrize("cs,gemm", [("linear", g) for g in LINEAR] + [("pairwise", g) for g in PAIRWISE])
 @pytest.mark.parametrize("prec", ["fp32", "mixed"])
-def test_tile_config_bits(cs, gemm, prec, monkeypatch):
-    monkeypatch.setenv("WINO_GEMM", gemm)
+def test_tile_config_bits(cs, gemm, prec, gemm_tuning):
+    gemm_tuning(gemm)
     for r, m, pts, N, C, K, H, Wd, pad in CASES:
         ts = W.build_transforms(r, m, W.parse_points(pts))   # fresh plan cache
         trip = O.Triple.from_points(r, m, pts)

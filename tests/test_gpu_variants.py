@@ -1,11 +1,11 @@
-"""The alternative transform kernels (selected by environment variables, read
-once per process) must produce the same bits as the default kernels:
+"""The alternative transform kernels (selected by libwino tuning keys, read once
+per process -- wino_tuning_set) must produce the same bits as the default kernels:
 
-  WINO_K1=tile     K1 parks V in smem and writes 16-byte rows (input_body) --
+  k1=tile          K1 parks V in smem and writes 16-byte rows (input_body) --
                    also the fallback for grids beyond 65535 tile chunks
-  WINO_K4=staged   K4 stages M in smem (flat for m <= 2, banded otherwise)
-  WINO_K1TC=4x8    TC K1 with 4 tiles x 8 channels per warp also for P <= 16
-  WINO_CPT/KPT     gather K1 / K4 threads looping over several channels / filters
+  k4=staged        K4 stages M in smem (flat for m <= 2, banded otherwise)
+  k1tc=4x8         TC K1 with 4 tiles x 8 channels per warp also for P <= 16
+  cpt / kpt        gather K1 / K4 threads looping over several channels / filters
 
 Each variant runs in a subprocess; its outputs are compared bitwise with the
 default kernels' outputs computed here (exact mode also with the oracle)."""
@@ -36,6 +36,8 @@ import numpy as np
 import paper_1803_10986_b200 as W
 from oracle import wino_oracle as O
 cases, modes, out = json.loads(sys.argv[1]), json.loads(sys.argv[2]), sys.argv[3]
+for k, v in json.loads(sys.argv[4]).items():
+    W._native.set_tuning(k, v)
 res = {}
 for i, (r, m, pts, N, C, K, H, Wd, pad) in enumerate(cases):
     ts = W.build_transforms(r, m, W.parse_points(pts))
@@ -47,18 +49,17 @@ np.savez(out, **res)
 """
 
 
-def _run_variant(env_extra, tmp_path):
+def _run_variant(tuning, tmp_path):
     out = str(tmp_path / "variant.npz")
-    env = dict(os.environ, **env_extra)
+    env = dict(os.environ)
     here = os.path.dirname(os.path.abspath(__file__))
     env["PYTHONPATH"] = os.pathsep.join([os.path.dirname(here), env.get("PYTHONPATH", "")])
-    subprocess.run([sys.executable, "-c", _CHILD, json.dumps(CASES), json.dumps(MODES), out], check=True, env=env,
-                   timeout=600)
+    subprocess.run([sys.executable, "-c", _CHILD, json.dumps(CASES), json.dumps(MODES), out, json.dumps(tuning)],
+                   check=True, env=env, timeout=600)
     return np.load(out)
 
 
-@pytest.mark.parametrize("env", [{"WINO_K1": "tile"}, {"WINO_K4": "staged"}, {"WINO_K1TC": "4x8"},
-                                 {"WINO_CPT": "4", "WINO_KPT": "8"}],
+@pytest.mark.parametrize("env", [{"k1": "tile"}, {"k4": "staged"}, {"k1tc": "4x8"}, {"cpt": "4", "kpt": "8"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_variant_bits(env, tmp_path):
     got = _run_variant(env, tmp_path)
@@ -75,12 +76,12 @@ def test_variant_bits(env, tmp_path):
 
 
 def test_interpreted_tile_transforms_pass_the_tile_goldens():
-    """WINO_TILE_INTERP=1: the tile-level API through the program interpreter
+    """tile_interp=1: the tile-level API through the program interpreter
     (used for alpha > 10) reproduces every tile golden of test_gpu_tile.py --
     z and y bits of hadamard_2d / output_2d / conv_2d / conv_1d, and the
     reference's measure_error values repr for repr."""
     here = os.path.dirname(os.path.abspath(__file__))
-    env = dict(os.environ, WINO_TILE_INTERP="1")
+    env = dict(os.environ, WINO_TEST_TUNING="tile_interp=1")
     env["PYTHONPATH"] = os.pathsep.join([os.path.dirname(here), env.get("PYTHONPATH", "")])
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_tile.py"), "-m", "gpu", "-q",
                         "-x", "-k", "golden"], env=env, cwd=os.path.dirname(here), capture_output=True, text=True,

@@ -1,6 +1,9 @@
 import ctypes, sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
+import os as _os, sys as _sys  # noqa: E401
+_sys.path.insert(0, _os.path.dirname(_os.path.abspath(__file__)))
+import tuning_env  # noqa: E402,F401  (WINO_* env -> libwino tuning keys)
 import paper_1803_10986_b200 as W
 from paper_1803_10986_b200 import _native
 ts = W.build_transforms(3, 2, W.parse_points("0,1,-1,inf"))

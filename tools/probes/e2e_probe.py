@@ -3,6 +3,9 @@ import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
+import os as _os, sys as _sys  # noqa: E401
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
+import tuning_env  # noqa: E402,F401  (WINO_* env -> libwino tuning keys)
 import paper_1803_10986_b200 as W
 from paper_1803_10986_b200 import pointsets
 

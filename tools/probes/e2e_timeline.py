@@ -4,6 +4,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 import ctypes
 import numpy as np
 import torch
+import os as _os, sys as _sys  # noqa: E401
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
+import tuning_env  # noqa: E402,F401  (WINO_* env -> libwino tuning keys)
 import paper_1803_10986_b200 as W
 from paper_1803_10986_b200 import pointsets, _native
 from paper_1803_10986_b200 import device as D

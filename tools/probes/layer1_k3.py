@@ -7,6 +7,9 @@ import sys
 import torch
 
 sys.path.insert(0, ".")
+import os as _os, sys as _sys  # noqa: E401
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
+import tuning_env  # noqa: E402,F401  (WINO_* env -> libwino tuning keys)
 import paper_1803_10986_b200 as W  # noqa: E402
 from paper_1803_10986_b200 import _native  # noqa: E402
 

@@ -15,6 +15,9 @@ sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402
 
+import os as _os, sys as _sys  # noqa: E401
+_sys.path.insert(0, _os.path.dirname(_os.path.abspath(__file__)))
+import tuning_env  # noqa: E402,F401  (WINO_* env -> libwino tuning keys)
 from paper_1803_10986_b200 import sweep  # noqa: E402
 
 

@@ -1,0 +1,22 @@
+"""tools/ only: map WINO_<KEY> environment variables onto libwino tuning keys
+(include/wino.h wino_tuning_set) so the sweep scripts can select kernel variants
+from the shell (e.g. WINO_GEMM=8,8,16,8,16,4,0,16,0,1 python tools/contract_bench.py).
+The product package never reads these variables."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KEYS = ("gemm", "dbuf", "k1", "k1order", "k4", "k1tc", "tile_interp", "cpt", "kpt", "tcf_nk", "tcf_dbg", "tc_epi")
+
+
+def apply():
+    if ROOT not in sys.path:
+        sys.path.insert(0, ROOT)
+    from paper_1803_10986_b200 import _native
+    for k in KEYS:
+        v = os.environ.get("WINO_" + k.upper())
+        if v:
+            _native.set_tuning(k, v)
+
+
+apply()
