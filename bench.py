@@ -809,6 +809,102 @@ def run_dryrun(args):
         dist.destroy_process_group()
 
 
+# --------------------------------------------------------------------- block-size sweeps
+def sweep_variants(which):
+    """BASELINE configs[2] / configs[3] as concrete layer variants:
+    (label, r, m, points, N, C, K, H, pad, x_dist, precision, dot_order, channel_sum)."""
+    from paper_1803_10986_b200.pointsets import canonical_text, curated_text
+    out = []
+    if which == "sweep_cfg3":
+        # F(m,3), m = 2..9, N64 C=K=256 28^2, U[-1,1]: good vs canonical points, Huffman vs
+        # linear (the reference's "arbitrary order" baseline), fp32 vs mixed
+        for m in range(2, 10):
+            n = m + 2
+            good, good_mx, canon = curated_text(n, 2, "fp32"), curated_text(n, 2, "mixed"), canonical_text(n)
+            for tag, pts, prec, order in (("good", good, "fp32", "huffman"), ("good", good, "fp32", "linear"),
+                                          ("canonical", canon, "fp32", "huffman"),
+                                          ("good", good_mx, "mixed", "huffman")):
+                out.append((f"m{m}-{tag}-{prec}-{order}", 3, m, pts, 64, 256, 256, 28, 1, "uniform", prec, order,
+                            "linear"))
+    else:
+        # F(m,5), m = 2..6, N32 C=K=512 14^2 pad 2: linear vs pairwise channel sums on
+        # U[0,1] (post-ReLU-like) and N(0,1) inputs; curated 2D set with n = alpha points
+        for m in range(2, 7):
+            pts = curated_text(m + 4, 2, "fp32")
+            for dist in ("uniform01", "normal"):
+                for cs in ("linear", "pairwise"):
+                    out.append((f"m{m}-{dist}-{cs}", 5, m, pts, 32, 512, 512, 14, 2, dist, "fp32", "huffman", cs))
+    return out
+
+
+def run_sweep(args):
+    """One JSON line per variant (time + error vs fp64 direct), then a summary line
+    with the error directions SPEC.md:454 predicts (huffman < linear order, mixed <
+    fp32, pairwise < linear channel sum) checked at layer scale."""
+    import torch
+    import paper_1803_10986_b200 as W
+    from paper_1803_10986_b200 import _native
+    torch.cuda.set_device(0)
+    lines = []
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for label, r, m, pts, N, C, K, H, pad, xd, prec, order, cs in sweep_variants(args.config):
+        ts = W.build_transforms(r, m, W.parse_points(pts))
+        cfg = W.ConvConfig(prec, order, cs)
+        op = W.layer_op(ts, cfg, N, C, H, H, K, pad, args.contraction)
+        x_np = np.stack([synth((C, H, H), 2024, i, xd) for i in range(N)])
+        w_np = synth((K, C, r, r), 2024, 10_000_000, "normal") * np.float32(np.sqrt(2.0 / (r * r * C)))
+        x, w = torch.from_numpy(x_np).cuda(), torch.from_numpy(w_np).cuda()
+        y = torch.empty(op.out_shape, dtype=torch.float32 if prec == "fp32" else torch.float64, device="cuda")
+        ws = torch.empty(op.layout.workspace_bytes, dtype=torch.uint8, device="cuda")
+        for _ in range(3):
+            op(x, w, out=y, workspace=ws)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            op(x, w, out=y, workspace=ws)
+        ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        t = float(np.median(ms))
+        st = W.layer_error_stats(y, W.direct_layer_f64(x, w, pad)).cpu().numpy()
+        line = {"metric": METRIC, "workload": args.config, "variant": label, "winograd": f"F({m}x{m},{r}x{r})",
+                "points": pts, "N": N, "C": C, "K": K, "H": H, "pad": pad, "x_dist": xd, "precision": prec,
+                "dot_order": order, "channel_sum": cs, "contraction": args.contraction, "ms_per_step": t,
+                "value": op.direct_flops / (t * 1e-3) / 1e12, "unit": "TFLOP/s",
+                "contraction_tflops_note": "whole layer (K1+K2, K3, K4) as a CUDA graph, L2 flushed between steps",
+                "error_vs_fp64": {"rel_l1": float(st[:, 0].sum() / st[:, 1].sum()),
+                                  "per_point_l1": float(st[:, 0].sum() / st[:, 2].sum()),
+                                  "max_abs": float(st[:, 3].max()), "images": int(N)}}
+        lines.append(line)
+        print(json.dumps(line), flush=True)
+        del ws, y, x, w, g
+    # error directions (SPEC.md:454), per block size
+    err = {ln["variant"]: ln["error_vs_fp64"]["rel_l1"] for ln in lines}
+    checks = []
+
+    def check(name, a, b, bound):
+        if a in err and b in err:
+            ratio = err[a] / err[b]
+            checks.append({"check": name, "num": a, "den": b, "ratio": ratio, "bound": bound, "ok": ratio < bound})
+    if args.config == "sweep_cfg3":
+        for m in range(2, 10):
+            check("huffman < linear order (SPEC: >= 5%)", f"m{m}-good-fp32-huffman", f"m{m}-good-fp32-linear", 0.95)
+            check("mixed < fp32 (SPEC: ratio < 0.85)", f"m{m}-good-mixed-huffman", f"m{m}-good-fp32-huffman", 0.85)
+            check("good < canonical points", f"m{m}-good-fp32-huffman", f"m{m}-canonical-fp32-huffman", 1.0)
+    else:
+        for m in range(2, 7):
+            for dist in ("uniform01", "normal"):
+                check("pairwise < linear channel sum (SPEC: ratio < 0.9)", f"m{m}-{dist}-pairwise",
+                      f"m{m}-{dist}-linear", 0.9)
+    print(json.dumps({"workload": args.config, "summary": True, "lines": len(lines), "direction_checks": checks,
+                      "all_ok": all(c["ok"] for c in checks)}), flush=True)
+
+
 def spawn_ranks(args):
     """`--gpus N` without a torchrun environment: re-exec this script under
     torch.distributed.run with N local ranks (127.0.0.1 rendezvous); the ranks'
@@ -828,7 +924,7 @@ def parse_args(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="vgg16", choices=sorted(CONFIGS) + ["vgg16"])
+    ap.add_argument("--config", default="vgg16", choices=sorted(CONFIGS) + ["vgg16", "sweep_cfg3", "sweep_cfg4"])
     ap.add_argument("--vgg-batch", type=int, default=256)
     ap.add_argument("--vgg-chunks", type=int, default=4, help="image chunks of the vgg16 e2e pipeline")
     ap.add_argument("--cpu-vgg-images", type=int, default=2, help="vgg16 CPU sample (BASELINE.md: 2-image slice)")
@@ -854,6 +950,9 @@ def main():
         return
     if args.config == "vgg16":
         (run_reference_vgg if args.impl == "reference" else run_vgg)(args)
+        return
+    if args.config.startswith("sweep_"):
+        run_sweep(args)
         return
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

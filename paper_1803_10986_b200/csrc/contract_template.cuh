@@ -48,6 +48,9 @@
 #ifndef WINO_PACK
 #define WINO_PACK 0
 #endif
+#ifndef WINO_SLOTS_SMEM
+#define WINO_SLOTS_SMEM 0  // pairwise: dynamic-counter slots in shared memory instead of registers
+#endif
 #ifndef WINO_DBUF
 #define WINO_DBUF (WINO_SUM == 1 || WINO_SUM == 3)  // explicit fragment double buffer (pairwise)
 #endif
@@ -286,7 +289,15 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
         static_assert(WINO_BK == 8 || WINO_BK == 16 || WINO_BK == 32 || WINO_BK == 64,
                       "pairwise stages: the in-stage counter covers 8, 16, 32 or 64 channels");
         acc_t zs[ZL][WINO_TM][NJ];
+#if WINO_SLOTS_SMEM
+        // dynamic-counter slots in shared memory (touched once per stage): thread-major
+        // so a warp's access is 32 consecutive words; frees LEVELS * TM * NJ registers
+        acc_t* const slot_s = reinterpret_cast<acc_t*>(empty + WINO_STAGES);
+#define SLOT(L, i, j) slot_s[((L) * (WINO_TM * NJ) + (i) * NJ + (j)) * NTHR + tid]
+#else
         acc_t slot[WINO_LEVELS][WINO_TM][NJ];
+#define SLOT(L, i, j) slot[L][i][j]
+#endif
 #endif
 
 #pragma unroll 1
@@ -420,8 +431,8 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
                                         for (int j = 0; j < NJ; ++j) {
                                             acc_t cy = pa[i][j];
 #pragma unroll
-                                            for (int e = 0; e < L; ++e) cy = AADD(slot[e][i][j], cy);
-                                            slot[L][i][j] = cy;
+                                            for (int e = 0; e < L; ++e) cy = AADD(SLOT(e, i, j), cy);
+                                            SLOT(L, i, j) = cy;
                                         }
                                 }
                             }
@@ -457,7 +468,7 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
                     for (int i = 0; i < WINO_TM; ++i)
 #pragma unroll
                         for (int j = 0; j < NJ; ++j)
-                            acc[i][j] = have ? AADD(slot[L][i][j], acc[i][j]) : slot[L][i][j];
+                            acc[i][j] = have ? AADD(SLOT(L, i, j), acc[i][j]) : SLOT(L, i, j);
                     have = true;
                 }
             }

@@ -374,6 +374,16 @@ struct GemmCfg {
     int tm, tn, thm, thn, bk, stages, maxreg, ku = 0;  // ku: k-steps unrolled per inner loop (0 = bk)
     int noprod = 0;  // 1: no producer warp (last consumer warp to release a stage refills it)
     int pack = 0;    // 1: packed f32x2 arithmetic (float U/V only)
+    // Dynamic shared memory of a contraction kernel: the operand ring, 2 mbarriers per
+    // stage, and (pairwise, when it fits) the dynamic-counter slots -- `levels` x the
+    // consumer threads' accumulator tiles -- which otherwise live in registers.
+    // Returns the byte count; *slots_smem tells which form the module is generated in.
+    long long smem_bytes(int levels, int eb, bool* slots_smem) const {
+        const long long ring = (long long)stages * bk * (bm() + bn()) * eb + 2LL * stages * 8;
+        const long long slots = (long long)levels * tm * tn * eb * threads();
+        *slots_smem = levels > 0 && ring + slots <= 200 * 1024;
+        return ring + (*slots_smem ? slots : 0);
+    }
     int bm() const { return thm * tm; }
     int bn() const { return thn * tn; }
     int threads() const { return thm * thn; }
@@ -497,6 +507,8 @@ struct wino_plan {
         const long long Q = Cp / gemm.bk;  // pairwise: the dynamic counter runs over stages
         while ((1LL << levels) <= Q) ++levels;  // bit_length(Q)
         if (chsum != WINO_SUM_PAIRWISE) levels = 0;
+        bool slots_smem = false;
+        gemm.smem_bytes(levels, ty.uv_double ? 8 : 4, &slots_smem);
         std::lock_guard<std::mutex> g(mu);
         const int key = levels * 16 + ci;
         auto it = contract.find(key);
@@ -509,7 +521,7 @@ struct wino_plan {
            << "\n#define WINO_THN " << gemm.thn << "\n#define WINO_BK " << gemm.bk << "\n#define WINO_STAGES "
            << gemm.stages << "\n#define WINO_SUM " << sum_mode() << "\n#define WINO_LEVELS "
            << (levels > 0 ? levels : 1) << "\n#define WINO_MAXREG " << gemm.maxreg << "\n#define WINO_KU " << (gemm.ku > 0 ? gemm.ku : gemm.bk) << "\n#define WINO_NOPROD " << gemm.noprod
-           << "\n#define WINO_PACK " << (gemm.pack && !dbl ? 1 : 0) << "\n"
+           << "\n#define WINO_PACK " << (gemm.pack && !dbl ? 1 : 0) << "\n#define WINO_SLOTS_SMEM " << slots_smem << "\n"
            << (!wino::tuning("dbuf").empty() ? "#define WINO_DBUF " + wino::tuning("dbuf") + "\n" : std::string())
            << ""
            << wino::kContractTemplate;
@@ -973,7 +985,11 @@ int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, con
     const long long tiles = (long long)L.P * (Kp / g.bm()) * (Tp / g.bn());
     if (tiles > (1LL << 30)) return wino::fail(WINO_EUNSUPPORTED, "contract: too many tiles");
     int n_tiles = (int)tiles;
-    const unsigned smem = (unsigned)(g.stages * g.bk * (g.bm() + g.bn()) * L.elem_bytes_uv + 2 * g.stages * 8);
+    int levels = 1;  // must match contract_module()
+    while ((1LL << levels) <= Cp / g.bk) ++levels;
+    if (plan->chsum != WINO_SUM_PAIRWISE) levels = 0;
+    bool slots_smem = false;
+    const unsigned smem = (unsigned)g.smem_bytes(levels, L.elem_bytes_uv, &slots_smem);
     const int threads = g.block();
     // persistent grid: as many CTAs as can be co-resident (one wave), each walks tiles
     int per_sm = 0, sms = 0, dev = 0;
