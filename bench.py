@@ -554,6 +554,19 @@ def run_vgg(args):
             st.forward(x)
         torch.cuda.synchronize()
         return
+    if args.traffic:
+        # DRAM-traffic capture mode (run under ncu --cache-control none, tools/traffic.py):
+        # one forward with an L2 eviction after every libwino kernel -- a read of a clean
+        # 256 MiB buffer, whose DRAM writes are exactly the previous kernel's dirty lines
+        # still in L2 (the deferred write-back a per-kernel capture would miss)
+        clean = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
+        clean.sum()
+        cur = x
+        for i in range(len(st.ops)):
+            cur = st.layer_forward(i, cur, after_kernel=lambda: clean.sum())
+        clean.sum()
+        torch.cuda.synchronize()
+        return
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph):
         st.forward(x)
@@ -937,6 +950,8 @@ def parse_args(argv=None):
     ap.add_argument("--soak", type=float, default=1.5, help="seconds of untimed load before the timed region")
     ap.add_argument("--e2e-chunks", default="4", help="image chunks of the e2e pipeline: a count or sizes a,b,...")
     ap.add_argument("--ncu", action="store_true", help="profiling mode: warm-up + K eager steps only, no output")
+    ap.add_argument("--traffic", action="store_true", help="vgg16: one forward with an L2 eviction after each "
+                    "kernel, for the ncu DRAM-traffic capture (tools/traffic.py)")
     ap.add_argument("--dry-run", action="store_true", help="CPU/gloo rehearsal of the multi-rank plumbing (no GPU)")
     return ap.parse_args(argv)
 

@@ -171,6 +171,15 @@ int wino_output_transform_act(wino_plan* plan, const wino_layer_shape* s, const 
  * from the tensor-memory accumulators -- engine.py:415-423 */
 int wino_contract_output(wino_plan* plan, const wino_layer_shape* s, const void* U, const void* V,
                          void* y, void* stream);
+/* K3 + K4 (+ activation) in one launch for small channel counts (C <= 8, e.g.
+ * VGG-16 layer 1): M never goes to memory.  mode 0: y (as wino_output_transform),
+ * 1: ReLU (as wino_output_transform_act pool=0), 2: ReLU + 2x2 max-pool (even m).
+ * Bitwise equal to the unfused kernels.  Exact fp32 plans; wino_smallc_supported()
+ * says whether a shape qualifies (all of U must fit in shared memory). */
+int wino_smallc_supported(wino_plan* plan, const wino_layer_shape* s);
+int wino_contract_output_smallc(wino_plan* plan, const wino_layer_shape* s, const void* U, const void* V,
+                                void* out, int mode, void* stream);
+
 /* K2 -> K1 -> K3 -> K4 with a caller-provided workspace of
  * layout.workspace_bytes bytes (256-byte aligned). */
 int wino_conv2d(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w,

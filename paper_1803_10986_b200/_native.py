@@ -60,6 +60,9 @@ SIGNATURES = [
     ("wino_contract", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_void_p]),
     ("wino_output_transform", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p]),
     ("wino_output_transform_act", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_int, c_void_p]),
+    ("wino_smallc_supported", c_int, [c_void_p, POINTER(LayerShape)]),
+    ("wino_contract_output_smallc", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_int,
+                                            c_void_p]),
     ("wino_contract_output", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_void_p]),
     ("wino_conv2d", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                             c_void_p]),

@@ -549,6 +549,157 @@ static void emit_output_gather_act(std::ostringstream& os, int r, int m, const M
     os << "}\n\n";
 }
 
+// K3 + K4 (+ ReLU, + 2x2 max-pool) in one kernel for small channel counts (C <= 8,
+// e.g. VGG-16 layer 1 with C = 3): the contraction is a few products per point, so
+// the unfused pair is bound by writing and re-reading M (alpha^2 x K x T floats,
+// 6 GB at VGG layer 1).  Persistent CTAs keep all of U in shared memory
+// ([P][Kp][CW], loaded once), stage the V values of 64 tiles at a time
+// ([P][64][CW]), and each thread turns one (tile, filter) pair into its P channel
+// sums -- the plan's linear order, or the pairwise halving tree of the padded
+// 8-channel stage with the -0 leaves pruned (x + -0 == x exactly, so the result
+// is the contraction kernel's bit for bit) -- then (A^T M) A, the activation and
+// the store.  A warp covers 8 tiles x 4 filters, so its shared-memory reads are
+// broadcasts of 8 V vectors and 4 U vectors.  fp32 plans only.
+static void emit_smallc(std::ostringstream& os, int r, int m, const MatProg& AT, const GenTypes& ty, int& ctr) {
+    const int n = r + m - 1, P = n * n;
+    os << "template <int L, int R, int C>\n"
+          "static __device__ __forceinline__ float sc_tree(const float* z) {\n"
+          "  if constexpr (R - L == 1) {\n    return z[L];\n  } else {\n"
+          "    constexpr int Mid = (L + R) / 2;\n"
+          "    if constexpr (Mid >= C) return sc_tree<L, Mid, C>(z);\n"
+          "    else return __fadd_rn(sc_tree<L, Mid, C>(z), sc_tree<Mid, R, C>(z));\n  }\n}\n"
+          "template <int C, int PW, int CW>\n"
+          "static __device__ __forceinline__ float sc_sum(const float* __restrict__ u, const float* __restrict__ v) {\n"
+          "  float uu[CW], vv[CW], z[8];\n"
+          "#pragma unroll\n"
+          "  for (int q = 0; q < CW; q += 4) {\n"
+          "    const float4 a = *reinterpret_cast<const float4*>(u + q), b = *reinterpret_cast<const float4*>(v + q);\n"
+          "    uu[q] = a.x; uu[q + 1] = a.y; uu[q + 2] = a.z; uu[q + 3] = a.w;\n"
+          "    vv[q] = b.x; vv[q + 1] = b.y; vv[q + 2] = b.z; vv[q + 3] = b.w;\n  }\n"
+          "#pragma unroll\n"
+          "  for (int c = 0; c < C; ++c) z[c] = __fmul_rn(uu[c], vv[c]);\n"
+          "  if constexpr (PW) {\n    return sc_tree<0, 8, C>(z);\n  } else {\n"
+          "    float a = z[0];\n"
+          "#pragma unroll\n"
+          "    for (int c = 1; c < C; ++c) a = __fadd_rn(a, z[c]);\n    return a;\n  }\n}\n";
+    os << "template <int C, int PW>\n"
+          "static __device__ __forceinline__ void sc_body(const float* __restrict__ U, const float* __restrict__ V,\n"
+          "    float* __restrict__ out, int K, int Ho, int Wo, int th, int tw, long long T, long long Tp, long long Kp,\n"
+          "    long long Cp, int bm, int bn, float rtw, float rth, int mode, int n_blocks) {\n"
+          "  constexpr int CW = C <= 4 ? 4 : 8;\n"
+          "  constexpr int NW = C <= 4 ? 12 : 4;       // warps per CTA (one CTA per SM)\n"
+          "  constexpr int SC_TT = 8 * NW;             // tiles per block: a warp = 8 tiles x 4 filters\n"
+       << "  constexpr int P = " << P << ";\n"
+          "  constexpr int STR = P * CW + 4;  // per-filter / per-tile row (+16 B: conflict-free for 8 rows)\n"
+          "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
+          "  float* sU = reinterpret_cast<float*>(smem_raw);   // [Kp][STR]\n"
+          "  float* sV = sU + (long long)Kp * STR;             // [SC_TT][STR]\n"
+          "  const long long plu = Cp * Kp, plv = Cp * Tp;\n"
+          "  // U once per CTA: thread = one filter k (the blocked row offset computed once)\n"
+          "  for (int k = threadIdx.x; k < Kp; k += blockDim.x) {\n"
+          "    const float* src = U + (long long)(k / bm) * Cp * bm + (k % bm);\n"
+          "    float* dst = sU + (long long)k * STR;\n"
+          "#pragma unroll 4\n"
+          "    for (int pc = 0; pc < P * CW; ++pc) {\n"
+          "      const int p = pc / CW, c = pc % CW;\n"
+          "      dst[pc] = c < C ? src[p * plu + (long long)c * bm] : 0.f;\n"
+          "    }\n"
+          "  }\n"
+          "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n"
+          "  const int tl = warp * 8 + (lane & 7), k0 = lane >> 3;\n"
+          "  // V staging: thread -> one tile column q and every (32 * NW / SC_TT)-th (p, c) row\n"
+          "  const int sq = threadIdx.x % SC_TT, srow = threadIdx.x / SC_TT;\n"
+          "#pragma unroll 1\n"
+          "  for (int blk = blockIdx.x; blk < n_blocks; blk += gridDim.x) {\n"
+          "    const long long t0 = (long long)blk * SC_TT;\n"
+          "    __syncthreads();  // previous block's readers are done with sV\n"
+          "    {\n"
+          "      const long long ts = t0 + sq;\n"
+          "      const bool ok = ts < Tp;\n"
+          "      const float* src = V + (ok ? (ts / bn) * Cp * bn + (ts % bn) : 0);\n"
+          "      float* dst = sV + sq * STR;\n"
+          "#pragma unroll 4\n"
+          "      for (int pc = srow; pc < P * CW; pc += 32 * NW / SC_TT) {\n"
+          "        const int p = pc / CW, c = pc % CW;\n"
+          "        dst[pc] = (ok && c < C) ? src[p * plv + (long long)c * bn] : 0.f;\n"
+          "      }\n"
+          "    }\n"
+          "    __syncthreads();\n"
+          "    const long long t = t0 + tl;\n"
+          "    if (t >= T) continue;\n"
+          "    const int per = th * tw;\n"
+          "    const int img = (int)(t / per), rem = (int)(t - (long long)img * per);\n"
+          "    const int ti = idiv_small(rem, tw, rtw), tj = rem - ti * tw;\n"
+          "    const float* vp = sV + tl * STR;\n"
+          "#pragma unroll 1\n"
+          "    for (int k = k0; k < K; k += 4) {\n"
+          "      const float* up = sU + (long long)k * STR;\n";
+    // channel sums computed lazily, column by column, right before the left pass
+    // consumes them (keeps the live set to one column of M + the left-pass results)
+    Emitter em(os, false, ctr);
+    std::vector<std::vector<std::string>> left(AT.rows, std::vector<std::string>(n));
+    for (int b = 0; b < n; ++b) {
+        std::vector<std::string> col(n);
+        for (int a = 0; a < n; ++a) {
+            col[a] = "m" + std::to_string(a) + "_" + std::to_string(b);
+            os << "      const float " << col[a] << " = sc_sum<C, PW, CW>(up + " << (a * n + b) << " * CW, vp + "
+               << (a * n + b) << " * CW);\n";
+        }
+        auto res = em.apply(AT, col);
+        for (int i = 0; i < AT.rows; ++i) left[i][b] = res[i];
+    }
+    std::vector<std::vector<std::string>> yv(AT.rows);
+    for (int i = 0; i < AT.rows; ++i) yv[i] = em.apply(AT, left[i]);
+    os << "      const int y0 = ti * " << m << ", x0 = tj * " << m << ";\n"
+          "      if (mode < 2) {\n"
+          "        float* dst = out + (((long long)img * K + k) * Ho + y0) * Wo + x0;\n"
+       << "        if (y0 + " << m << " <= Ho && x0 + " << m << " <= Wo) {\n";
+    for (int a = 0; a < m; ++a)
+        for (int b = 0; b < m; ++b)
+            os << "          dst[" << a << " * Wo + " << b << "] = mode ? wino_relu(" << yv[a][b] << ") : " << yv[a][b]
+               << ";\n";
+    os << "        } else {\n";
+    for (int a = 0; a < m; ++a) {
+        os << "          if (y0 + " << a << " < Ho) {\n";
+        for (int b = 0; b < m; ++b)
+            os << "            if (x0 + " << b << " < Wo) dst[" << a << " * Wo + " << b << "] = mode ? wino_relu("
+               << yv[a][b] << ") : " << yv[a][b] << ";\n";
+        os << "          }\n";
+    }
+    os << "        }\n        continue;\n      }\n";
+    if (m % 2 == 0) {
+        os << "      const int Hp = Ho >> 1, Wp = Wo >> 1, py0 = y0 >> 1, px0 = x0 >> 1;\n"
+              "      float* dst = out + (((long long)img * K + k) * Hp + py0) * Wp + px0;\n";
+        auto pv = [&](int a, int b) {
+            return "wino_relu(fmaxf(fmaxf(" + yv[2 * a][2 * b] + ", " + yv[2 * a][2 * b + 1] + "), fmaxf(" +
+                   yv[2 * a + 1][2 * b] + ", " + yv[2 * a + 1][2 * b + 1] + ")))";
+        };
+        os << "      if (py0 + " << m / 2 << " <= Hp && px0 + " << m / 2 << " <= Wp) {\n";
+        for (int a = 0; a < m / 2; ++a)
+            for (int b = 0; b < m / 2; ++b) os << "        dst[" << a << " * Wp + " << b << "] = " << pv(a, b) << ";\n";
+        os << "      } else {\n";
+        for (int a = 0; a < m / 2; ++a) {
+            os << "        if (py0 + " << a << " < Hp) {\n";
+            for (int b = 0; b < m / 2; ++b)
+                os << "          if (px0 + " << b << " < Wp) dst[" << a << " * Wp + " << b << "] = " << pv(a, b)
+                   << ";\n";
+            os << "        }\n";
+        }
+        os << "      }\n";
+    }
+    os << "    }\n  }\n}\n";
+    for (int C = 1; C <= 8; ++C)
+        for (int pw = 0; pw < 2; ++pw)
+            os << "extern \"C\" __global__ void __launch_bounds__(" << (C <= 4 ? 384 : 128) << ", 1) wino_smallc_c" << C
+               << (pw ? "p" : "l")
+               << "(\n    const float* __restrict__ U, const float* __restrict__ V, float* __restrict__ out, int K,\n"
+                  "    int Ho, int Wo, int th, int tw, long long T, long long Tp, long long Kp, long long Cp, int bm,\n"
+                  "    int bn, float rtw, float rth, int mode, int n_blocks) {\n"
+               << "  sc_body<" << C << ", " << pw << ">(U, V, out, K, Ho, Wo, th, tw, T, Tp, Kp, Cp, bm, bn, rtw, rth,"
+                  " mode, n_blocks);\n}\n";
+    os << "\n";
+}
+
 std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
                              const GenTypes& ty, int bm, int bn) {
     const int n = r + m - 1, P = n * n;
@@ -695,6 +846,7 @@ std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, 
         emit_output_flat(os, r, m, AT, ty, tbf, ctr);
         emit_output_gather(os, r, m, AT, ty, 128, ctr);
         if (!ty.y_double) emit_output_gather_act(os, r, m, AT, ty, 128, ctr);
+        if (!ty.compute_double && !ty.uv_double && !ty.y_double) emit_smallc(os, r, m, AT, ty, ctr);
     }
     return os.str();
 }

@@ -381,7 +381,7 @@ struct GemmCfg {
     long long smem_bytes(int levels, int eb, bool* slots_smem) const {
         const long long ring = (long long)stages * bk * (bm() + bn()) * eb + 2LL * stages * 8;
         const long long slots = (long long)levels * tm * tn * eb * threads();
-        *slots_smem = levels > 0 && ring + slots <= 200 * 1024;
+        *slots_smem = levels > 0 && ring + slots <= 232448 - 1024;  // B200: 227 KB of opt-in smem per CTA
         return ring + (*slots_smem ? slots : 0);
     }
     int bm() const { return thm * tm; }
@@ -835,6 +835,8 @@ int wino_plan_prepare(wino_plan* plan, const wino_layer_shape* s, int flags) {
                                                          : "wino_output_xform"});
     }
     if ((flags & WINO_PREPARE_ACT) && !plan->ty.y_double) work.push_back({lm, "wino_output_gather_act"});
+    if ((flags & (WINO_PREPARE_ACT | WINO_PREPARE_CONV)) && wino_smallc_supported(plan, s))
+        work.push_back({lm, "wino_smallc_c" + std::to_string(s->C) + (plan->chsum == WINO_SUM_PAIRWISE ? "p" : "l")});
     if (flags & WINO_PREPARE_STAGES) {
         work.push_back({lm, "wino_filter_xform"});
         work.push_back({lm, k1_gather() && n_tb <= 65535 && L.Cp <= 65535 ? "wino_input_gather" : "wino_input_xform"});
@@ -1087,6 +1089,55 @@ int wino_conv2d(wino_plan* plan, const wino_layer_shape* s, const void* x, const
     if (plan->fused()) return wino_contract_output(plan, s, U, V, y, stream);
     if ((rc = wino_contract(plan, s, U, V, M, stream))) return rc;
     return wino_output_transform(plan, s, M, y, stream);
+}
+
+int wino_smallc_supported(wino_plan* plan, const wino_layer_shape* s) {
+    wino_layer_layout L;
+    if (!plan || !s || layout_of(plan, s, &L)) return 0;
+    if (plan->mode != WINO_CONTRACT_EXACT || plan->precision != WINO_FP32 || s->C > 8) return 0;
+    const long long cw = s->C <= 4 ? 4 : 8;
+    const long long tt = s->C <= 4 ? 96 : 32;  // codegen.cpp emit_smallc: SC_TT
+    return (L.P * cw + 4) * (L.Kp + tt) * 4 <= 232448 ? 1 : 0;
+}
+
+int wino_contract_output_smallc(wino_plan* plan, const wino_layer_shape* s, const void* U, const void* V, void* out,
+                                int mode, void* stream) {
+    wino_layer_layout L;
+    int rc = layout_of(plan, s, &L);
+    if (rc) return rc;
+    if (!wino_smallc_supported(plan, s))
+        return wino::fail(WINO_EUNSUPPORTED, "contract_output_smallc: needs an exact fp32 plan, C <= 8 and U in smem");
+    if (mode < 0 || mode > 2) return wino::fail(WINO_EINVAL, "contract_output_smallc: mode must be 0, 1 or 2");
+    if (mode == 2 && (plan->m & 1)) return wino::fail(WINO_EUNSUPPORTED, "contract_output_smallc: pooling needs an even m");
+    if (((uintptr_t)U | (uintptr_t)V) & 15) return wino::fail(WINO_EINVAL, "contract_output_smallc: U, V must be 16-byte aligned");
+    if (s->N == 0) return WINO_OK;
+    const std::string kname = "wino_smallc_c" + std::to_string(s->C) + (plan->chsum == WINO_SUM_PAIRWISE ? "p" : "l");
+    CUfunction f;
+    if ((rc = plan->layer_mod(plan->pick(s))->function(kname.c_str(), &f))) return rc;
+    const long long cw = s->C <= 4 ? 4 : 8;
+    const long long tt = s->C <= 4 ? 96 : 32;  // tiles per block (SC_TT); threads = 4 * tt
+    const unsigned smem = (unsigned)((L.P * cw + 4) * (L.Kp + tt) * 4);  // codegen.cpp emit_smallc: [Kp + TT][P*CW + 4]
+    int K = s->K, Ho = L.Ho, Wo = L.Wo, th = L.th, tw = L.tw, bm = L.bm, bn = L.bn;
+    long long T = L.T, Tp = L.Tp, Kp = L.Kp, Cp = L.Cp;
+    float rtw = 1.0f / tw, rth = 1.0f / th;
+    const long long nb = (T + tt - 1) / tt;
+    if (nb > (1LL << 30)) return wino::fail(WINO_EUNSUPPORTED, "contract_output_smallc: too many tiles");
+    int n_blocks = (int)nb, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    void* args[] = {(void*)&U, (void*)&V, &out, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp, &Cp, &bm, &bn, &rtw, &rth,
+                    &mode, &n_blocks};
+    int per_sm = 1;  // persistent: as many CTAs as fit (2 per SM for C <= 4)
+    if (smem > 48 * 1024) {
+        CUresult cr = wino::driver().FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
+        if (cr != CUDA_SUCCESS) return wino::fail(WINO_ECUDA, "contract_output_smallc: set smem: " + wino::cu_err(cr));
+    }
+    const int threads = (int)(4 * tt);
+    if (wino::driver().OccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, threads, smem) != CUDA_SUCCESS ||
+        per_sm < 1)
+        per_sm = 1;
+    return wino::launch(f, dim3((unsigned)std::min<long long>(nb, (long long)sms * per_sm)), dim3(threads), smem,
+                        stream, args, "contract_output_smallc");
 }
 
 int wino_contract_output(wino_plan* plan, const wino_layer_shape* s, const void* U, const void* V, void* y,

@@ -59,6 +59,10 @@ class ConvStack:
             if pool:
                 h, w = h // 2, w // 2
         self.out_hw = (h, w)
+        # small-C layers (VGG-16 layer 1) can run K3 + K4 + activation in one kernel (M never
+        # stored, wino_contract_output_smallc); off by default: at VGG layer 1 it is still
+        # slower than K3 + K4act (3.45 vs 2.84 ms, register-spill / latency bound)
+        self.use_smallc(False)
         ws = max(op.layout.workspace_bytes for op in self.ops)
         self.workspace = D.torch.empty(ws, dtype=D.torch.uint8, device="cuda")
         self._conv_out = None  # pre-activation outputs, allocated on first keep_conv_out forward
@@ -67,6 +71,13 @@ class ConvStack:
             Ho, Wo = op.layout.Ho, op.layout.Wo
             self.act.append(D.empty((N, K, Ho // 2, Wo // 2) if pool else (N, K, Ho, Wo), np.float32))
         self.weights = None
+
+    def use_smallc(self, on: bool = True):
+        """Route qualifying small-C layers through the fused K3 + K4 + activation kernel."""
+        self.smallc = [on and not op.tensor_core and
+                       bool(_native.lib().wino_smallc_supported(op.plan.handle, ctypes.byref(op.shape)))
+                       for op in self.ops]
+        return self
 
     @property
     def conv_out(self):
@@ -101,7 +112,9 @@ class ConvStack:
 
     @property
     def kernels_per_forward(self) -> int:
-        return (3 if self.fused_act else 4) * len(self.ops)
+        if not self.fused_act:
+            return 4 * len(self.ops)
+        return sum(2 if sc else 3 for sc in self.smallc)
 
     def _uvm(self, L):
         al = lambda v: (v + 255) // 256 * 256
@@ -109,9 +122,11 @@ class ConvStack:
         V = U + al(L.u_bytes)
         return U, V, V + al(L.v_bytes)
 
-    def layer_forward(self, i, cur, stream=None, events=None):
+    def layer_forward(self, i, cur, stream=None, events=None, after_kernel=None):
         """Layer i on activation `cur` (fused path): K1+K2, K3, K4+ReLU(+pool) -> self.act[i].
-        events: optional 4 CUDA events recorded before K1+K2, before K3, before K4, after K4."""
+        events: optional 4 CUDA events recorded before K1+K2, before K3, before K4, after K4.
+        after_kernel: optional callable issued after each of the three kernels (profiling)."""
+        hook = after_kernel if after_kernel is not None else (lambda: None)
         lib = _native.lib()
         s = D.stream_handle() if stream is None else stream
         op = self.ops[i]
@@ -122,15 +137,27 @@ class ConvStack:
             events[0].record()
         _native.check(lib.wino_transforms(op.plan.handle, sh, D.ptr(cur), D.ptr(self.weights[i]),
                                           ctypes.c_void_p(U), ctypes.c_void_p(V), s), f"layer {i + 1} K1/K2")
+        hook()
         if events is not None:
             events[1].record()
+        if self.smallc[i]:  # K3 + K4 + ReLU (+ pool) in one launch
+            _native.check(lib.wino_contract_output_smallc(op.plan.handle, sh, ctypes.c_void_p(U), ctypes.c_void_p(V),
+                                                          D.ptr(self.act[i]), 2 if pool else 1, s),
+                          f"layer {i + 1} K3+K4+act")
+            hook()
+            if events is not None:
+                events[2].record()
+                events[3].record()
+            return self.act[i]
         _native.check(lib.wino_contract(op.plan.handle, sh, ctypes.c_void_p(U), ctypes.c_void_p(V),
                                         ctypes.c_void_p(M), s), f"layer {i + 1} K3")
+        hook()
         if events is not None:
             events[2].record()
         _native.check(lib.wino_output_transform_act(op.plan.handle, sh, ctypes.c_void_p(M),
                                                     D.ptr(self.act[i]), 1 if pool else 0, s),
                       f"layer {i + 1} K4+act")
+        hook()
         if events is not None:
             events[3].record()
         return self.act[i]

@@ -27,6 +27,10 @@ def test_small_vgg_like_stack_bitwise():
     out = st.forward(xt).cpu().numpy()                       # K4 + ReLU / max-pool fused
     ref_outs, ref = O.stack_forward(trip, x, ws, layers)
     assert G.same_bits(out, ref)
+    st.use_smallc(True)                                      # layer 1 (C = 3): K3 + K4 + act fused
+    assert st.smallc[0] and not any(st.smallc[1:])
+    assert G.same_bits(st.forward(xt).cpu().numpy(), ref)
+    st.use_smallc(False)
     out2 = st.forward(xt, keep_conv_out=True).cpu().numpy()  # unfused: y stored, wino_relu_pool
     for i, y in enumerate(ref_outs):
         assert G.same_bits(st.conv_out[i].cpu().numpy(), y), i
@@ -96,3 +100,39 @@ def test_vgg16_full_size_batch256_bitwise():
     for i, (g, want) in enumerate(zip(got, outs)):
         assert G.same_bits(g, want), f"layer {i + 1}"
     assert G.same_bits(fused, act)
+
+
+@pytest.mark.parametrize("cs", ["linear", "pairwise"])
+def test_smallc_fused_kernel_matches_unfused(cs):
+    """wino_contract_output_smallc (K3 + K4 + activation in one kernel for C <= 8) is
+    bitwise equal to wino_contract + wino_output_transform[_act] for every C <= 8,
+    modes y / ReLU / ReLU + max-pool, partial edge tiles, K not a multiple of 4."""
+    import ctypes
+    from paper_1803_10986_b200 import _native
+    lib = _native.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    for m, pts in ((6, P8), (4, "0,1,-1,1/2,-1/2,inf"), (3, "0,1,-1,2,-2")):
+        ts = W.build_transforms(3, m, W.parse_points(pts))
+        for C in range(1, 9):
+            N, K, H, Wd = 2, 7 + C, 17 + C, 23
+            op = W.layer_op(ts, W.ConvConfig("fp32", "huffman", cs), N, C, H, Wd, K, 1)
+            assert lib.wino_smallc_supported(op.plan.handle, ctypes.byref(op.shape))
+            x = torch.from_numpy(O.synthetic((N, C, H, Wd), 12, C)).cuda()
+            w = torch.from_numpy(O.synthetic((K, C, 3, 3), 12, 100 + C)).cuda()
+            U, V = op.filter_transform(w), op.input_transform(x)
+            M = op.contract(U, V)
+            Ho, Wo = op.layout.Ho, op.layout.Wo
+            for mode in ((0, 1, 2) if m % 2 == 0 else (0, 1)):
+                if mode == 0:
+                    want = op.output_transform(M)
+                else:
+                    shp = (N, K, Ho // 2, Wo // 2) if mode == 2 else (N, K, Ho, Wo)
+                    want = torch.empty(shp, device="cuda")
+                    _native.check(lib.wino_output_transform_act(op.plan.handle, ctypes.byref(op.shape),
+                                                                _native.as_ptr(M), _native.as_ptr(want), mode - 1, s))
+                got = torch.full_like(want, 7.0)
+                _native.check(lib.wino_contract_output_smallc(op.plan.handle, ctypes.byref(op.shape),
+                                                              _native.as_ptr(U), _native.as_ptr(V),
+                                                              _native.as_ptr(got), mode, s))
+                torch.cuda.synchronize()
+                assert torch.equal(got.view(torch.int32), want.view(torch.int32)), (m, C, cs, mode)
