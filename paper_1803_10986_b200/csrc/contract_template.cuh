@@ -48,6 +48,9 @@
 #ifndef WINO_PACK
 #define WINO_PACK 0
 #endif
+#ifndef WINO_WN
+#define WINO_WN 0  // > 0: warp-tiled thread map, WINO_WN lanes along t x 32/WINO_WN lanes along k
+#endif
 #ifndef WINO_SLOTS_SMEM
 #define WINO_SLOTS_SMEM 0  // pairwise: dynamic-counter slots in shared memory instead of registers
 #endif
@@ -255,8 +258,15 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
     }
 
     // ---------------------------------------------------- consumer warps
+#if WINO_WN
+    static_assert(32 % WINO_WN == 0 && WINO_THN % WINO_WN == 0 && WINO_THM % (32 / WINO_WN) == 0,
+                  "warp-tiled thread map: WINO_WN x 32/WINO_WN lanes must tile the thread grid");
+    const int tn = (warp % (WINO_THN / WINO_WN)) * WINO_WN + lane % WINO_WN;
+    const int tm = (warp / (WINO_THN / WINO_WN)) * (32 / WINO_WN) + lane / WINO_WN;
+#else
     const int tn = tid % WINO_THN;
     const int tm = tid / WINO_THN;
+#endif
     int g = 0;
 
 #pragma unroll 1

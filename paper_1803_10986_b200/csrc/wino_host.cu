@@ -374,6 +374,7 @@ struct GemmCfg {
     int tm, tn, thm, thn, bk, stages, maxreg, ku = 0;  // ku: k-steps unrolled per inner loop (0 = bk)
     int noprod = 0;  // 1: no producer warp (last consumer warp to release a stage refills it)
     int pack = 0;    // 1: packed f32x2 arithmetic (float U/V only)
+    int wn = 0;      // > 0: warp-tiled thread map, wn lanes along t x 32/wn lanes along k
     // Dynamic shared memory of a contraction kernel: the operand ring, 2 mbarriers per
     // stage, and (pairwise, when it fits) the dynamic-counter slots -- `levels` x the
     // consumer threads' accumulator tiles -- which otherwise live in registers.
@@ -521,7 +522,7 @@ struct wino_plan {
            << "\n#define WINO_THN " << gemm.thn << "\n#define WINO_BK " << gemm.bk << "\n#define WINO_STAGES "
            << gemm.stages << "\n#define WINO_SUM " << sum_mode() << "\n#define WINO_LEVELS "
            << (levels > 0 ? levels : 1) << "\n#define WINO_MAXREG " << gemm.maxreg << "\n#define WINO_KU " << (gemm.ku > 0 ? gemm.ku : gemm.bk) << "\n#define WINO_NOPROD " << gemm.noprod
-           << "\n#define WINO_PACK " << (gemm.pack && !dbl ? 1 : 0) << "\n#define WINO_SLOTS_SMEM " << slots_smem << "\n"
+           << "\n#define WINO_PACK " << (gemm.pack && !dbl ? 1 : 0) << "\n#define WINO_WN " << gemm.wn << "\n#define WINO_SLOTS_SMEM " << slots_smem << "\n"
            << (!wino::tuning("dbuf").empty() ? "#define WINO_DBUF " + wino::tuning("dbuf") + "\n" : std::string())
            << ""
            << wino::kContractTemplate;
@@ -744,14 +745,16 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
     else
         p->gemm = {8, 8, 16, 8, 16, 4, 0, 16, 0, 1};
     bool env_gemm = false;
-    const std::string tg = wino::tuning("gemm");  // tuning override: tm,tn,thm,thn,bk,stages,maxreg[,ku,noprod,pack]
+    const std::string tg = wino::tuning("gemm");  // tuning override: tm,tn,thm,thn,bk,stages,maxreg[,ku,noprod,pack,wn]
     if (!tg.empty()) {
         wino::GemmCfg g{};
-        const int got = sscanf(tg.c_str(), "%d,%d,%d,%d,%d,%d,%d,%d,%d,%d", &g.tm, &g.tn, &g.thm, &g.thn, &g.bk,
-                               &g.stages, &g.maxreg, &g.ku, &g.noprod, &g.pack);
+        const int got = sscanf(tg.c_str(), "%d,%d,%d,%d,%d,%d,%d,%d,%d,%d,%d", &g.tm, &g.tn, &g.thm, &g.thn, &g.bk,
+                               &g.stages, &g.maxreg, &g.ku, &g.noprod, &g.pack, &g.wn);
+        const bool wn_ok = g.wn == 0 || (g.wn > 0 && 32 % g.wn == 0 && g.thn % g.wn == 0 && g.thm % (32 / g.wn) == 0);
         // the pairwise in-stage counter (contract_template.cuh) covers stages of 8, 16, 32 or 64 channels
         const bool bk_ok = channel_sum != WINO_SUM_PAIRWISE || g.bk == 8 || g.bk == 16 || g.bk == 32 || g.bk == 64;
-        if (got < 7 || g.bk % 8 || g.tm % 4 || g.tn % 4 || (g.ku != 0 && g.bk % g.ku) || !bk_ok)
+        if (got < 7 || g.bk % 8 || g.tm % 4 || g.tn % 4 || (g.ku != 0 && g.bk % g.ku) || !bk_ok || !wn_ok ||
+            g.noprod < 0 || g.noprod > 1 || (g.thm * g.thn) % 32)
             return wino::fail(WINO_EINVAL, "tuning gemm: bad tile config '" + tg + "'");
         p->gemm = g;
         env_gemm = true;
