@@ -133,6 +133,7 @@ int wino_plan_cubin(wino_plan* plan, int which, int channels, void* buf, size_t 
 #define WINO_PREPARE_CONV 1   /* K1+K2, K3, K4 of wino_conv2d */
 #define WINO_PREPARE_ACT 2    /* K4 with ReLU / max-pool (wino_output_transform_act) */
 #define WINO_PREPARE_STAGES 4 /* wino_filter_transform / wino_input_transform alone */
+#define WINO_PREPARE_NHWC 8   /* K2, K1, K3, K4 of wino_conv2d_nhwc */
 int wino_plan_prepare(wino_plan* plan, const wino_layer_shape* s, int flags);
 
 /* ---- layer-level Winograd convolution (new entry point; the reference
@@ -184,6 +185,18 @@ int wino_contract_output_smallc(wino_plan* plan, const wino_layer_shape* s, cons
  * layout.workspace_bytes bytes (256-byte aligned). */
 int wino_conv2d(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w,
                 void* y, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- NHWC activations: x[N][H][W][C], y[N][Ho][Wo][K] (w, U, V, M and the
+ * contraction are layout-independent).  Native gather / store kernels: the
+ * same straight-line transforms, hence the same bits, as the NCHW entry points
+ * (engine.py:401-423 per (filter, tile)).  FP32-pipe contraction modes only
+ * (exact, ffma); tensor-core plans return WINO_EUNSUPPORTED. */
+int wino_input_transform_nhwc(wino_plan* plan, const wino_layer_shape* s, const void* x,
+                              void* V, void* stream);
+int wino_output_transform_nhwc(wino_plan* plan, const wino_layer_shape* s, const void* M,
+                               void* y, void* stream);
+int wino_conv2d_nhwc(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w,
+                     void* y, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- tile-level drop-in (reference public API on (..., C, n) tiles) ------ */
 /* hadamard_2d: z[B][C][n][n] = (G h G^T) o (B^T x B)      -- engine.py:401-415 */

@@ -43,7 +43,7 @@ class LayerLayout(ctypes.Structure):
                 ("workspace_bytes", c_size_t)]
 
 
-PREPARE_CONV, PREPARE_ACT, PREPARE_STAGES = 1, 2, 4  # wino_plan_prepare flags (include/wino.h)
+PREPARE_CONV, PREPARE_ACT, PREPARE_STAGES, PREPARE_NHWC = 1, 2, 4, 8  # wino_plan_prepare flags (include/wino.h)
 
 # (name, restype, argtypes) of every exported symbol, in include/wino.h order
 SIGNATURES = [
@@ -64,6 +64,10 @@ SIGNATURES = [
     ("wino_contract_output_smallc", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_int,
                                             c_void_p]),
     ("wino_contract_output", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("wino_input_transform_nhwc", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p]),
+    ("wino_output_transform_nhwc", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p]),
+    ("wino_conv2d_nhwc", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
+                          c_void_p]),
     ("wino_conv2d", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                             c_void_p]),
     ("wino_tile_hadamard2d", c_int, [c_void_p, c_int64, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),

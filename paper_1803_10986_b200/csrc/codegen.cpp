@@ -549,6 +549,112 @@ static void emit_output_gather_act(std::ostringstream& os, int r, int m, const M
     os << "}\n\n";
 }
 
+// ---- NHWC layer kernels (activations x[N][H][W][C], y[N][Ho][Wo][K]; w, U, V, M as for NCHW)
+//
+// Channels are the contiguous axis of x and y, tiles the contiguous axis of V and M, so no
+// thread-to-(tile, channel) map is unit-stride on both sides.  A block is 8 tiles x 16
+// channels, a warp 8 tiles x 4 channels: the larger tensor (V written by K1, M read by K4;
+// alpha^2 / m^2 times the activation) moves in full 32-byte sectors (8 consecutive t), the
+// activation in 16-byte runs (4 consecutive channels) whose other half-sector is touched by
+// the neighbouring warp of the same block (L1 for the K1 loads, merged in L2 for the K4
+// stores).  Same generated straight-line transforms, same bits as the NCHW kernels.
+static void emit_nhwc(std::ostringstream& os, int r, int m, const MatProg& BT, const MatProg& AT, const GenTypes& ty,
+                      int bn, int& ctr) {
+    const int n = r + m - 1, P = n * n;
+    // K1
+    os << "extern \"C\" __global__ void __launch_bounds__(128) wino_input_gather_nhwc(\n"
+          "    const in_t* __restrict__ x, uv_t* __restrict__ V, int C, int H, int W, int pad, int th,\n"
+          "    int tw, long long T, long long Tp, long long Cp) {\n"
+          "  const long long plane = Cp * Tp;\n"
+          "  const long long tt = (long long)blockIdx.x * 8 + (threadIdx.x & 7);\n"
+          "  const int c = blockIdx.y * 16 + (threadIdx.x >> 3);\n"
+          "  if (tt >= Tp || c >= Cp) return;\n"
+       << "  uv_t* op = V + ((tt / " << bn << ") * Cp + c) * " << bn << " + (tt % " << bn << ");\n"
+       << "  if (tt >= T || c >= C) {\n"
+          "    const uv_t z = (c >= C) ? (uv_t)(-0.0) : (uv_t)0;\n"
+          "#pragma unroll\n"
+       << "    for (int p = 0; p < " << P << "; ++p) op[p * plane] = z;\n"
+          "    return;\n"
+          "  }\n"
+          "  const int t = (int)tt;\n"
+          "  const int g = t / tw, tj = t - g * tw;\n"
+          "  const int img = g / th, ti = g - img * th;\n"
+       << "  const int h0 = ti * " << m << " - pad, w0 = tj * " << m << " - pad;\n"
+       << "  const in_t* src = x + (long long)img * H * W * C + c;\n"
+       << "  const bool interior = h0 >= 0 && w0 >= 0 && h0 + " << n << " <= H && w0 + " << n << " <= W;\n";
+    std::vector<std::vector<std::string>> d(n, std::vector<std::string>(n));
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+            d[a][b] = "x" + std::to_string(a) + "_" + std::to_string(b);
+            os << "  ct_t " << d[a][b] << ";\n";
+        }
+    os << "  if (interior) {\n"
+          "    const in_t* rp = src + ((long long)h0 * W + w0) * C;\n"
+          "    const long long rs = (long long)W * C;\n";
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b)
+            os << "    " << d[a][b] << " = (ct_t)__ldg(rp + " << a << " * rs + " << b << " * (long long)C);\n";
+    os << "  } else {\n";
+    for (int a = 0; a < n; ++a)
+        os << "    const bool r" << a << " = (unsigned)(h0 + " << a << ") < (unsigned)H;\n";
+    for (int b = 0; b < n; ++b)
+        os << "    const bool c" << b << " = (unsigned)(w0 + " << b << ") < (unsigned)W;\n";
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b)
+            os << "    " << d[a][b] << " = (r" << a << " && c" << b << ") ? (ct_t)__ldg(src + ((long long)(h0 + " << a
+               << ") * W + (w0 + " << b << ")) * C) : (ct_t)0;\n";
+    os << "  }\n";
+    {
+        Emitter em(os, ty.compute_double, ctr);
+        auto v = em.apply2d(BT, d);
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j)
+                os << "  op[" << (i * n + j) << " * plane] = " << store_cvt(ty.compute_double, ty.uv_double, v[i][j])
+                   << ";\n";
+    }
+    os << "}\n\n";
+    // K4
+    os << "extern \"C\" __global__ void __launch_bounds__(128) wino_output_gather_nhwc(\n"
+          "    const uv_t* __restrict__ Mm, y_t* __restrict__ y, int K, int Ho, int Wo, int th, int tw,\n"
+          "    long long T, long long Tp, long long Kp) {\n"
+          "  const long long tt = (long long)blockIdx.x * 8 + (threadIdx.x & 7);\n"
+          "  const int k = blockIdx.y * 16 + (threadIdx.x >> 3);\n"
+          "  if (tt >= T || k >= K) return;\n"
+          "  const long long plane = Kp * Tp;\n"
+          "  const uv_t* src = Mm + (long long)k * Tp + tt;\n";
+    std::vector<std::vector<std::string>> mm(n, std::vector<std::string>(n));
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+            mm[a][b] = "m" + std::to_string(a) + "_" + std::to_string(b);
+            os << "  const ct_t " << mm[a][b] << " = (ct_t)__ldg(src + " << (a * n + b) << " * plane);\n";
+        }
+    os << "  const int t = (int)tt;\n"
+          "  const int g = t / tw, tj = t - g * tw;\n"
+          "  const int img = g / th, ti = g - img * th;\n"
+       << "  const int y0 = ti * " << m << ", x0 = tj * " << m << ";\n";
+    {
+        Emitter em(os, ty.compute_double, ctr);
+        auto yv = em.apply2d(AT, mm);
+        os << "  y_t* dst = y + (((long long)img * Ho + y0) * Wo + x0) * K + k;\n"
+           << "  const long long rs = (long long)Wo * K;\n"
+           << "  if (y0 + " << m << " <= Ho && x0 + " << m << " <= Wo) {\n";
+        for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; ++b)
+                os << "    dst[" << a << " * rs + " << b << " * (long long)K] = "
+                   << store_cvt(ty.compute_double, ty.y_double, yv[a][b]) << ";\n";
+        os << "  } else {\n";
+        for (int a = 0; a < m; ++a) {
+            os << "    if (y0 + " << a << " < Ho) {\n";
+            for (int b = 0; b < m; ++b)
+                os << "      if (x0 + " << b << " < Wo) dst[" << a << " * rs + " << b << " * (long long)K] = "
+                   << store_cvt(ty.compute_double, ty.y_double, yv[a][b]) << ";\n";
+            os << "    }\n";
+        }
+        os << "  }\n";
+    }
+    os << "}\n\n";
+}
+
 // K3 + K4 (+ ReLU, + 2x2 max-pool) in one kernel for small channel counts (C <= 8,
 // e.g. VGG-16 layer 1 with C = 3): the contraction is a few products per point, so
 // the unfused pair is bound by writing and re-reading M (alpha^2 x K x T floats,
@@ -846,6 +952,7 @@ std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, 
         emit_output_flat(os, r, m, AT, ty, tbf, ctr);
         emit_output_gather(os, r, m, AT, ty, 128, ctr);
         if (!ty.y_double) emit_output_gather_act(os, r, m, AT, ty, 128, ctr);
+        emit_nhwc(os, r, m, BT, AT, ty, bn, ctr);
         if (!ty.compute_double && !ty.uv_double && !ty.y_double) emit_smallc(os, r, m, AT, ty, ctr);
     }
     return os.str();

@@ -840,6 +840,12 @@ int wino_plan_prepare(wino_plan* plan, const wino_layer_shape* s, int flags) {
     if ((flags & WINO_PREPARE_ACT) && !plan->ty.y_double) work.push_back({lm, "wino_output_gather_act"});
     if ((flags & (WINO_PREPARE_ACT | WINO_PREPARE_CONV)) && wino_smallc_supported(plan, s))
         work.push_back({lm, "wino_smallc_c" + std::to_string(s->C) + (plan->chsum == WINO_SUM_PAIRWISE ? "p" : "l")});
+    if (flags & WINO_PREPARE_NHWC) {
+        work.push_back({lm, "wino_filter_xform"});
+        work.push_back({lm, "wino_input_gather_nhwc"});
+        work.push_back({plan->contract_module(L.Cp, ci), "wino_contract"});
+        work.push_back({lm, "wino_output_gather_nhwc"});
+    }
     if (flags & WINO_PREPARE_STAGES) {
         work.push_back({lm, "wino_filter_xform"});
         work.push_back({lm, k1_gather() && n_tb <= 65535 && L.Cp <= 65535 ? "wino_input_gather" : "wino_input_xform"});
@@ -1092,6 +1098,58 @@ int wino_conv2d(wino_plan* plan, const wino_layer_shape* s, const void* x, const
     if (plan->fused()) return wino_contract_output(plan, s, U, V, y, stream);
     if ((rc = wino_contract(plan, s, U, V, M, stream))) return rc;
     return wino_output_transform(plan, s, M, y, stream);
+}
+
+int wino_input_transform_nhwc(wino_plan* plan, const wino_layer_shape* s, const void* x, void* V, void* stream) {
+    wino_layer_layout L;
+    int rc = layout_of(plan, s, &L);
+    if (rc) return rc;
+    if (plan->mode >= WINO_CONTRACT_TC_BF16)
+        return wino::fail(WINO_EUNSUPPORTED, "input_transform_nhwc: FP32-pipe contraction modes only");
+    if ((uintptr_t)V & 15) return wino::fail(WINO_EINVAL, "input_transform_nhwc: V must be 16-byte aligned");
+    CUfunction f;
+    if ((rc = plan->layer_mod(plan->pick(s))->function("wino_input_gather_nhwc", &f))) return rc;
+    int C = s->C, H = s->H, W = s->W, pad = s->pad, th = L.th, tw = L.tw;
+    long long T = L.T, Tp = L.Tp, Cp = L.Cp;
+    if (cdiv(Cp, 16) > 65535) return wino::fail(WINO_EUNSUPPORTED, "input_transform_nhwc: too many channels");
+    void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp};
+    // block = 8 tiles x 16 channels (codegen.cpp emit_nhwc)
+    return wino::launch(f, dim3(cdiv(Tp, 8), cdiv(Cp, 16), 1), dim3(128), 0, stream, args, "input_transform_nhwc");
+}
+
+int wino_output_transform_nhwc(wino_plan* plan, const wino_layer_shape* s, const void* M, void* y, void* stream) {
+    wino_layer_layout L;
+    int rc = layout_of(plan, s, &L);
+    if (rc) return rc;
+    if (plan->mode >= WINO_CONTRACT_TC_BF16)
+        return wino::fail(WINO_EUNSUPPORTED, "output_transform_nhwc: FP32-pipe contraction modes only");
+    CUfunction f;
+    if ((rc = plan->layer_mod(plan->pick(s))->function("wino_output_gather_nhwc", &f))) return rc;
+    int K = s->K, Ho = L.Ho, Wo = L.Wo, th = L.th, tw = L.tw;
+    long long T = L.T, Tp = L.Tp, Kp = L.Kp;
+    if (cdiv(K, 16) > 65535) return wino::fail(WINO_EUNSUPPORTED, "output_transform_nhwc: too many filters");
+    void* args[] = {(void*)&M, &y, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp};
+    return wino::launch(f, dim3(cdiv(T, 8), cdiv(K, 16), 1), dim3(128), 0, stream, args, "output_transform_nhwc");
+}
+
+int wino_conv2d_nhwc(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w, void* y,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+    wino_layer_layout L;
+    int rc = layout_of(plan, s, &L);
+    if (rc) return rc;
+    if (plan->mode >= WINO_CONTRACT_TC_BF16)
+        return wino::fail(WINO_EUNSUPPORTED, "conv2d_nhwc: FP32-pipe contraction modes only");
+    if (s->N == 0) return WINO_OK;
+    if (!workspace || workspace_bytes < L.workspace_bytes || ((uintptr_t)workspace & 255))
+        return wino::fail(WINO_EINVAL, "conv2d_nhwc: workspace missing, too small or not 256-byte aligned");
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    char* U = (char*)workspace;
+    char* V = U + al(L.u_bytes);
+    char* M = V + al(L.v_bytes);
+    if ((rc = wino_filter_transform(plan, s, w, U, stream))) return rc;
+    if ((rc = wino_input_transform_nhwc(plan, s, x, V, stream))) return rc;
+    if ((rc = wino_contract(plan, s, U, V, M, stream))) return rc;
+    return wino_output_transform_nhwc(plan, s, M, y, stream);
 }
 
 int wino_smallc_supported(wino_plan* plan, const wino_layer_shape* s) {

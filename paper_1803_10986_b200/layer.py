@@ -97,6 +97,22 @@ class LayerOp:
                                                 D.ptr(out), D.ptr(ws), ws.numel(), s), "conv2d")
         return out
 
+    def call_nhwc(self, x, w, out=None, workspace=None, stream=None):
+        """x (N, H, W, C), w (K, C, r, r) contiguous CUDA tensors -> y (N, Ho, Wo, K): the
+        NHWC-native gather / store kernels (wino_conv2d_nhwc), no permuted copies."""
+        L = self.layout
+        N, K, Ho, Wo = self.out_shape
+        if not getattr(self, "_nhwc_ready", False):
+            self.prepare(_native.PREPARE_NHWC)  # compile the four kernels concurrently
+            self._nhwc_ready = True
+        if out is None:
+            out = D.empty((N, Ho, Wo, K), self.out_dtype)
+        s = D.stream_handle() if stream is None else stream
+        ws = workspace if workspace is not None else _workspace(L.workspace_bytes, s)
+        _native.check(_native.lib().wino_conv2d_nhwc(self.plan.handle, ctypes.byref(self.shape), D.ptr(x), D.ptr(w),
+                                                     D.ptr(out), D.ptr(ws), ws.numel(), s), "conv2d_nhwc")
+        return out
+
     # -- individual stages (tests, profiling) --------------------------------
     @property
     def tensor_core(self) -> bool:
@@ -323,18 +339,32 @@ def conv2d_layer(ts: TransformSet, x, w, cfg: ConvConfig = ConvConfig(), pad: in
     x (N, C, H, W), w (K, C, r, r) -> y (N, K, Ho, Wo): numpy in -> numpy out
     (host<->device copies included), CUDA tensors in -> CUDA tensor out.
     Output dtype f32 in fp32 mode, f64 in mixed / fp64 mode (reference engine.py:378-387).
-    layout="NHWC": x (N, H, W, C) -> y (N, Ho, Wo, K); the layer kernels run on NCHW,
-    so the activations are permuted on the device (same values, bit for bit)."""
+    layout="NHWC": x (N, H, W, C) -> y (N, Ho, Wo, K) through NHWC-native K1 / K4 kernels
+    (wino_conv2d_nhwc; same values as the NCHW path, bit for bit).  Tensor-core
+    contraction modes have no NHWC kernels: there the activations are permuted on the
+    device around the NCHW kernels."""
     if layout not in ("NCHW", "NHWC"):
         raise ValueError("layout must be 'NCHW' or 'NHWC'")
     if layout == "NHWC":
-        if len(D.shape_of(x)) != 4:
-            raise ValueError("x must be (N, H, W, C)")
-        dt = np.float64 if cfg.precision == "fp64" else np.float32
-        xt, hx = D.to_device(x, dt)
-        wt, hw = D.to_device(w, dt)
-        y = conv2d_layer(ts, xt.permute(0, 3, 1, 2).contiguous(), wt, cfg, pad, contraction)
-        return D.finish(y.permute(0, 2, 3, 1).contiguous(), hx or hw)
+        xs, wsh = tuple(D.shape_of(x)), tuple(D.shape_of(w))
+        if len(xs) != 4 or len(wsh) != 4:
+            raise ValueError("x must be (N, H, W, C) and w (K, C, r, r)")
+        N, H, W, C = xs
+        K, C2, r1, r2 = wsh
+        if C2 != C:
+            raise ValueError("x and w disagree on the channel count")
+        if r1 != ts.n_h or r2 != ts.n_h:
+            raise ValueError(f"filter must be {ts.n_h}x{ts.n_h} for this transform set")
+        if contraction.startswith(("tc_", "tcf_")):
+            dt = np.float64 if cfg.precision == "fp64" else np.float32
+            xt, hx = D.to_device(x, dt)
+            wt, hw = D.to_device(w, dt)
+            y = conv2d_layer(ts, xt.permute(0, 3, 1, 2).contiguous(), wt, cfg, pad, contraction)
+            return D.finish(y.permute(0, 2, 3, 1).contiguous(), hx or hw)
+        op = layer_op(ts, cfg, N, C, H, W, K, pad, contraction)
+        xt, hx = D.to_device(x, op.in_dtype)
+        wt, hw = D.to_device(w, op.in_dtype)
+        return D.finish(op.call_nhwc(xt, wt), hx or hw)
     xs, wsh = tuple(D.shape_of(x)), tuple(D.shape_of(w))
     if len(xs) != 4 or len(wsh) != 4:
         raise ValueError("x must be (N, C, H, W) and w (K, C, r, r)")

@@ -129,21 +129,70 @@ def test_layer_validation_errors():
         W.conv2d_layer(ts, np.zeros((1, 2, 2, 2), np.float32), np.zeros((1, 2, 3, 3), np.float32), pad=0)
 
 
-@pytest.mark.parametrize("mode", [("fp32", "huffman", "linear"), ("mixed", "huffman", "pairwise")],
+NHWC_CASES = [
+    # r, m, points, N, C, K, H, W, pad  (odd C / K around the 16-channel block, partial edge tiles, pad 0 / 2)
+    (3, 4, "0,1,-1,1/2,-1/2,inf", 2, 9, 5, 14, 11, 1),
+    (3, 2, "0,1,-1,inf", 3, 33, 70, 15, 17, 1),
+    (3, 6, "0,-1,1,1/2,-1/2,2,-2,inf", 1, 40, 19, 29, 23, 1),
+    (5, 2, "0,-1,1,1/2,-2,inf", 2, 20, 12, 14, 14, 2),
+    (2, 3, "0,1,-1,inf", 2, 7, 9, 11, 11, 0),
+]
+
+
+@pytest.mark.parametrize("case", NHWC_CASES, ids=lambda c: f"r{c[0]}m{c[1]}C{c[4]}K{c[5]}")
+@pytest.mark.parametrize("mode", [("fp32", "huffman", "linear"), ("fp32", "linear", "pairwise"),
+                                  ("mixed", "huffman", "pairwise"), ("fp64", "huffman", "linear")],
                          ids=lambda m: "-".join(m))
-def test_layer_nhwc_layout(mode):
-    """layout='NHWC' gives the NCHW results transposed, bit for bit."""
+def test_layer_nhwc_layout(case, mode):
+    """layout='NHWC' (native NHWC gather / store kernels, wino_conv2d_nhwc) gives the
+    oracle's NCHW results transposed, bit for bit."""
+    r, m, pts, N, C, K, H, Wd, pad = case
+    ts = W.build_transforms(r, m, W.parse_points(pts))
+    trip = O.Triple.from_points(r, m, pts)
+    x = O.synthetic((N, C, H, Wd), 4, 0)
+    w = O.synthetic((K, C, r, r), 4, 1)
+    want = O.layer_conv2d(trip, x, w, pad, *mode)
+    y = W.conv2d_layer(ts, np.ascontiguousarray(x.transpose(0, 2, 3, 1)), w, W.ConvConfig(*mode), pad=pad,
+                       layout="NHWC")
+    assert y.shape == (N,) + want.shape[2:] + (K,)
+    assert G.same_bits(np.ascontiguousarray(y.transpose(0, 3, 1, 2)), want)
+
+
+def test_layer_nhwc_stages_and_errors():
+    """The NHWC stage entry points produce the NCHW stages' V (same blocked layout, padding
+    signs included) and y; bad layouts and tensor-core plans are rejected loudly."""
+    import ctypes
+    from paper_1803_10986_b200 import _native
+    from paper_1803_10986_b200 import device as D
     pts = "0,1,-1,1/2,-1/2,inf"
     ts = W.build_transforms(3, 4, W.parse_points(pts))
-    trip = O.Triple.from_points(3, 4, pts)
-    x = O.synthetic((2, 9, 14, 11), 4, 0)
-    w = O.synthetic((5, 9, 3, 3), 4, 1)
-    want = O.layer_conv2d(trip, x, w, 1, *mode)
-    y = W.conv2d_layer(ts, np.ascontiguousarray(x.transpose(0, 2, 3, 1)), w, W.ConvConfig(*mode), pad=1,
-                       layout="NHWC")
-    assert G.same_bits(np.ascontiguousarray(y.transpose(0, 3, 1, 2)), want)
+    cfg = W.ConvConfig("fp32", "huffman", "pairwise")
+    N, C, K, H, Wd = 2, 19, 21, 13, 10
+    x = torch.from_numpy(O.synthetic((N, C, H, Wd), 9, 0)).cuda()
+    w = torch.from_numpy(O.synthetic((K, C, 3, 3), 9, 1)).cuda()
+    op = W.layer_op(ts, cfg, N, C, H, Wd, K, 1)
+    V = op.input_transform(x)
+    V2 = torch.empty_like(V)
+    xh = x.permute(0, 2, 3, 1).contiguous()
+    lib = _native.lib()
+    _native.check(lib.wino_input_transform_nhwc(op.plan.handle, ctypes.byref(op.shape), D.ptr(xh), D.ptr(V2),
+                                                D.stream_handle()), "input_transform_nhwc")
+    assert torch.equal(V.view(torch.int32), V2.view(torch.int32))
+    M = op.contract(op.filter_transform(w), V)
+    y = op.output_transform(M)
+    y2 = torch.empty((N, op.layout.Ho, op.layout.Wo, K), device="cuda")
+    _native.check(lib.wino_output_transform_nhwc(op.plan.handle, ctypes.byref(op.shape), D.ptr(M), D.ptr(y2),
+                                                 D.stream_handle()), "output_transform_nhwc")
+    assert torch.equal(y.view(torch.int32), y2.permute(0, 3, 1, 2).contiguous().view(torch.int32))
     with pytest.raises(ValueError):
-        W.conv2d_layer(ts, x, w, W.ConvConfig(*mode), pad=1, layout="CHWN")
+        W.conv2d_layer(ts, x.cpu().numpy(), w.cpu().numpy(), cfg, pad=1, layout="CHWN")
+    tc = W.layer_op(ts, W.ConvConfig(), N, C, H, Wd, K, 1, "tc_bf16")
+    rc = lib.wino_input_transform_nhwc(tc.plan.handle, ctypes.byref(tc.shape), D.ptr(xh), D.ptr(V2), D.stream_handle())
+    assert rc != 0 and b"FP32-pipe" in lib.wino_last_error()
+    # tensor-core modes still accept layout="NHWC" (device permute around the NCHW kernels)
+    yt = W.conv2d_layer(ts, xh, w, W.ConvConfig(), pad=1, contraction="tc_fp16", layout="NHWC")
+    yn = W.conv2d_layer(ts, x, w, W.ConvConfig(), pad=1, contraction="tc_fp16")
+    assert torch.equal(yt.permute(0, 3, 1, 2).contiguous().view(torch.int32), yn.view(torch.int32))
 
 
 @pytest.mark.parametrize("by", ["batch", "filters"])
