@@ -561,11 +561,14 @@ def run_vgg(args):
         # still in L2 (the deferred write-back a per-kernel capture would miss)
         clean = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
         clean.sum()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()  # ncu --profile-from-start off: only this forward is captured
         cur = x
         for i in range(len(st.ops)):
             cur = st.layer_forward(i, cur, after_kernel=lambda: clean.sum())
         clean.sum()
         torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
         return
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph):
@@ -731,6 +734,17 @@ def traffic_of(kernel, config, contraction):
         return None
 
 
+def vgg_traffic(kernel="wino_contract"):
+    """Measured DRAM bytes per launch of `kernel` over one VGG-16 forward, deferred L2
+    write-back included (profiles/traffic_vgg16.json from tools/traffic.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic_vgg16.json")) as fh:
+            rows = [r for r in json.load(fh)["launches"] if r["kernel"] == kernel]
+        return float(np.mean([r["traffic"] for r in rows])) if rows else None
+    except Exception:
+        return None
+
+
 def vgg_roof(args, ach, peak, share):
     if args.contraction.startswith("tc_"):
         mp = measured_peaks()
@@ -740,7 +754,9 @@ def vgg_roof(args, ach, peak, share):
     pk = max(peak["ffma_tflops"], peak.get("ffma2_tflops", 0.0))
     xceil = max(peak["fmul_fadd_tflops"], peak.get("fmul_fadd_packed_tflops", 0.0))
     return {"kernel": "wino_contract (13 layers)", "bound": "fp32", "bound_note": "FP32 CUDA-core pipe (neither HBM nor tensor cores): the reference rounds every product and sum separately, which tensor-core accumulation cannot reproduce", "achieved": ach, "peak": pk,
-            "unit": "TFLOP/s", "frac": ach / pk, "traffic": None,
+            "unit": "TFLOP/s", "frac": ach / pk, "traffic": vgg_traffic() if args.contraction == "exact" else None,
+            "traffic_note": "mean DRAM bytes per contraction launch over the 13 layers at batch 256, incl. the "
+                            "deferred L2 write-back (profiles/traffic_vgg16.json, tools/traffic.py)",
             "peak_source": "measured in this run: libwino wino_peak_probe, max of FFMA and packed FFMA2",
             "exact_ceiling_tflops": xceil, "frac_of_exact_ceiling": ach / xceil, "share_of_step": share}
 

@@ -144,8 +144,10 @@ int wino_layer_layout_query(const wino_plan* plan, const wino_layer_shape* s,
  * U's blocking ([P][Kp/bm][Cp][bm]) follows the contraction tile the plan picks
  * for the WHOLE shape, batch size N included (wino_layer_layout_query: bm, Cp,
  * Kp).  A U computed for one shape may be reused with wino_contract for another
- * shape only if both layout queries report the same (bm, Cp, Kp); wino_contract
- * cannot detect a mismatch from the pointer.  HostPipeline keeps one U per
+ * shape only if both layout queries report the same (bm, Cp, Kp).  The library
+ * remembers, per device pointer, the blocking its transforms last wrote there,
+ * and wino_contract returns WINO_EINVAL for a U recorded with another blocking
+ * (a pointer it never wrote is taken on trust).  HostPipeline keeps one U per
  * blocking for this reason. */
 int wino_filter_transform(wino_plan* plan, const wino_layer_shape* s, const void* w,
                           void* U, void* stream);

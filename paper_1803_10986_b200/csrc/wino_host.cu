@@ -592,6 +592,42 @@ int layout_of(const wino_plan* p, const wino_layer_shape* s, wino_layer_layout* 
     return WINO_OK;
 }
 
+// ---- U layout registry.  U is blocked [P][Kp/bm][Cp][bm] for the contraction tile the plan
+// picks for the WHOLE layer shape (batch size included), and a caller-owned device pointer
+// carries no layout.  The transforms record, per (device, U pointer), the blocking they
+// wrote; wino_contract rejects a U recorded with a different blocking instead of silently
+// reading it with the wrong one (e.g. a U computed once for the weights and reused at
+// another batch size).  Pointers the library never wrote are not checked.
+struct ULayout {
+    long long bm, Cp, Kp;
+    int P;
+};
+static std::mutex g_u_mu;
+static std::map<std::pair<int, const void*>, ULayout> g_u_layouts;
+
+void u_layout_record(const void* U, const wino_layer_layout& L) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(g_u_mu);
+    if (g_u_layouts.size() > 4096) g_u_layouts.clear();  // bounded: stale entries only cost a missed check
+    g_u_layouts[{dev, U}] = ULayout{L.bm, L.Cp, L.Kp, L.P};
+}
+
+int u_layout_check(const void* U, const wino_layer_layout& L, const char* what) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(g_u_mu);
+    auto it = g_u_layouts.find({dev, U});
+    if (it == g_u_layouts.end()) return WINO_OK;
+    const ULayout& r = it->second;
+    if (r.bm == L.bm && r.Cp == L.Cp && r.Kp == L.Kp && r.P == L.P) return WINO_OK;
+    return wino::fail(WINO_EINVAL, std::string(what) + ": U was transformed with blocking (bm " + std::to_string(r.bm) +
+                                       ", Cp " + std::to_string(r.Cp) + ", Kp " + std::to_string(r.Kp) +
+                                       ") but this layer shape contracts with (bm " + std::to_string(L.bm) + ", Cp " +
+                                       std::to_string(L.Cp) + ", Kp " + std::to_string(L.Kp) +
+                                       "): transform the filters again for this shape (wino_layer_layout_query)");
+}
+
 inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
 // K1 / K4 block size (must match codegen.cpp): 128 tiles, halved while the
@@ -864,6 +900,7 @@ int wino_filter_transform(wino_plan* plan, const wino_layer_shape* s, const void
     CUfunction f;
     int K = s->K, C = s->C;
     long long Kp = L.Kp, Cp = L.Cp;
+    u_layout_record(U, L);
     if (plan->mode >= WINO_CONTRACT_TC_BF16 && (k1_gather() || plan->fused()) && Cp / 8 <= 65535) {
         if ((rc = plan->layer_mod(plan->pick(s))->function("wino_filter_tcg", &f))) return rc;
         void* args[] = {(void*)&w, &U, &K, &C, &Kp, &Cp};
@@ -884,6 +921,7 @@ int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, c
     int rc = layout_of(plan, s, &L);
     if (rc) return rc;
     if ((uintptr_t)V & 15) return wino::fail(WINO_EINVAL, "transforms: V must be 16-byte aligned");
+    u_layout_record(U, L);
     CUfunction f;
     int C = s->C, H = s->H, W = s->W, pad = s->pad, th = L.th, tw = L.tw, K = s->K;
     long long T = L.T, Tp = L.Tp, Cp = L.Cp, Kp = L.Kp;
@@ -982,6 +1020,7 @@ int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, con
     if (rc) return rc;
     if (((uintptr_t)U | (uintptr_t)V | (uintptr_t)M) & 15)
         return wino::fail(WINO_EINVAL, "contract: U, V, M must be 16-byte aligned");
+    if ((rc = u_layout_check(U, L, "contract"))) return rc;
     if (plan->fused())
         return wino::fail(WINO_EINVAL, "contract: fused tensor-core plan has no M; use wino_contract_output");
     if (plan->mode >= WINO_CONTRACT_TC_BF16)
@@ -1171,6 +1210,7 @@ int wino_contract_output_smallc(wino_plan* plan, const wino_layer_shape* s, cons
     if (mode < 0 || mode > 2) return wino::fail(WINO_EINVAL, "contract_output_smallc: mode must be 0, 1 or 2");
     if (mode == 2 && (plan->m & 1)) return wino::fail(WINO_EUNSUPPORTED, "contract_output_smallc: pooling needs an even m");
     if (((uintptr_t)U | (uintptr_t)V) & 15) return wino::fail(WINO_EINVAL, "contract_output_smallc: U, V must be 16-byte aligned");
+    if ((rc = u_layout_check(U, L, "contract_output_smallc"))) return rc;
     if (s->N == 0) return WINO_OK;
     const std::string kname = "wino_smallc_c" + std::to_string(s->C) + (plan->chsum == WINO_SUM_PAIRWISE ? "p" : "l");
     CUfunction f;

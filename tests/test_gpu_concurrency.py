@@ -88,3 +88,33 @@ def test_pipeline_chunks_with_different_blockings():
     pipe(xh, wh, yh)
     torch.cuda.synchronize()
     assert np.array_equal(yh.numpy().view(np.uint32), want.view(np.uint32))
+
+
+def test_contract_rejects_a_u_blocked_for_another_shape():
+    """A U transformed for one batch size must not be contracted under a shape whose
+    contraction tile (hence U blocking) differs: wino_contract fails loudly."""
+    import ctypes
+    from paper_1803_10986_b200 import _native
+    from paper_1803_10986_b200 import device as D
+    ts = W.build_transforms(3, 2, W.parse_points("0,1,-1,inf"))
+    C, H, K = 128, 28, 128
+    big = W.layer_op(ts, W.ConvConfig(), 8, C, H, H, K, 1)
+    small = W.layer_op(ts, W.ConvConfig(), 4, C, H, H, K, 1)
+    assert (big.layout.bm, big.layout.Cp, big.layout.Kp) != (small.layout.bm, small.layout.Cp, small.layout.Kp)
+    w = torch.from_numpy(O.synthetic((K, C, 3, 3), 2, 1)).cuda()
+    x = torch.from_numpy(O.synthetic((4, C, H, H), 2, 0)).cuda()
+    U = big.filter_transform(w)            # blocked for the 8-image shape
+    V = small.input_transform(x)
+    M = torch.empty((small.layout.P, small.layout.Kp, small.layout.Tp), device="cuda")
+    lib = _native.lib()
+    rc = lib.wino_contract(small.plan.handle, ctypes.byref(small.shape), D.ptr(U), D.ptr(V), D.ptr(M),
+                           D.stream_handle())
+    assert rc != 0 and b"blocking" in lib.wino_last_error()
+    # transformed again for the shape it is used with: accepted, and the layer is right
+    _native.check(lib.wino_filter_transform(small.plan.handle, ctypes.byref(small.shape), D.ptr(w), D.ptr(U),
+                                            D.stream_handle()))
+    _native.check(lib.wino_contract(small.plan.handle, ctypes.byref(small.shape), D.ptr(U), D.ptr(V), D.ptr(M),
+                                    D.stream_handle()))
+    y = small.output_transform(M)
+    want = W.conv2d_layer(ts, x, w, W.ConvConfig(), pad=1)
+    assert torch.equal(y.view(torch.int32), want.view(torch.int32))

@@ -2,7 +2,7 @@
 
 Capture (GPU box, one GPU):
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --cache-control none --clock-control none \\
-      --csv --log-file gpurun_out/traffic.csv python bench.py --traffic
+      --profile-from-start off --csv --log-file gpurun_out/traffic.csv python bench.py --traffic
 bench.py --traffic runs one VGG-16 forward with an L2 eviction (a read of a clean
 256 MiB buffer) after every libwino kernel.  With --cache-control none nothing else
 flushes L2, so the eviction's DRAM writes are exactly the dirty lines the preceding

@@ -67,6 +67,21 @@ def k4_perm():
 
 
 k4p = t(k4_perm)
+yn = torch.empty_like(y)
+full = t(lambda: op(x, w, out=yn))
+fullh = t(lambda: op.call_nhwc(xh, w, out=yh))
+assert torch.equal(yn.view(torch.int32), yh.permute(0, 3, 1, 2).contiguous().view(torch.int32))
+
+
+def full_perm():
+    op(xh.permute(0, 3, 1, 2).contiguous(), w, out=yn)
+    yh.copy_(yn.permute(0, 2, 3, 1))
+
+
+fullp = t(full_perm)
+tf = op.direct_flops / 1e6
+print(f"  whole layer (K2 K1 K3 K4): NCHW {full:.1f} us ({tf / full:.1f} TFLOP/s)  NHWC native {fullh:.1f} us "
+      f"({tf / fullh:.1f} TFLOP/s)  NHWC via permutes {fullp:.1f} us ({tf / fullp:.1f} TFLOP/s)", flush=True)
 b1 = x.numel() * 4 + L.v_bytes
 b4 = L.m_bytes + y.numel() * 4
 print(f"N={N} C={C} K={K} H={H} m={m}:  K1 NCHW {k1:.1f} us ({b1 / k1 / 1e6:.2f} TB/s)  NHWC native {k1h:.1f} us "
