@@ -630,6 +630,38 @@ def run_vgg(args):
             c_ms += t_c
             other_ms += t_x + t_o
             c_flops += op_.contraction_flops
+    else:
+        # tensor-core modes: K1+K2, K3t, K4, then ReLU / pool as its own kernel
+        import ctypes
+        lib_, D_ = _native.lib(), __import__("paper_1803_10986_b200.device", fromlist=["x"])
+        sh_ = D_.stream_handle()
+        for i, op_ in enumerate(st.ops):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            C, K, h, w_, pool = st.shapes[i]
+            L = op_.layout
+            U_, V_, M_ = st._uvm(L)
+            sref = ctypes.byref(op_.shape)
+            y_ = st.conv_out[i]
+            ev[0].record()
+            _native.check(lib_.wino_transforms(op_.plan.handle, sref, D_.ptr(cur), D_.ptr(st.weights[i]),
+                                               ctypes.c_void_p(U_), ctypes.c_void_p(V_), sh_))
+            ev[1].record()
+            _native.check(lib_.wino_contract(op_.plan.handle, sref, ctypes.c_void_p(U_), ctypes.c_void_p(V_),
+                                             ctypes.c_void_p(M_), sh_))
+            ev[2].record()
+            _native.check(lib_.wino_output_transform(op_.plan.handle, sref, ctypes.c_void_p(M_), D_.ptr(y_), sh_))
+            _native.check(lib_.wino_relu_pool(0, op_.N * K, L.Ho, L.Wo, 1 if pool else 0, D_.ptr(y_),
+                                              D_.ptr(st.act[i]), sh_))
+            ev[3].record()
+            torch.cuda.synchronize()
+            t_x, t_c, t_o = (ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]))
+            per_layer.append({"layer": i + 1, "C": C, "K": K, "H": h, "transforms_ms": t_x, "contract_ms": t_c,
+                              "contract_tflops": op_.contraction_flops / (t_c * 1e-3) / 1e12,
+                              "output_act_ms": t_o})
+            c_ms += t_c
+            other_ms += t_x + t_o
+            c_flops += op_.contraction_flops
+            cur = st.act[i]
     peak = measure_peaks(_native.lib(), _native, torch)
     ach = c_flops / (c_ms * 1e-3) / 1e12 if c_ms else 0.0
 
@@ -725,13 +757,11 @@ def measured_peaks():
 
 
 def traffic_of(kernel, config, contraction):
-    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
-    --set full capture summary (profiles/traffic.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            return json.load(fh).get(f"{config}/{contraction}/{kernel}")
-    except Exception:
-        return None
+    """Measured DRAM bytes per launch of `kernel` for a single-layer config.  Only the vgg16
+    workload has a committed capture that includes the deferred L2 write-back
+    (profiles/traffic_vgg16.json, vgg_traffic); a per-kernel --set full capture of these
+    small layers misses most of the writes (they are still dirty in L2), so: None."""
+    return None
 
 
 def vgg_traffic(kernel="wino_contract"):

@@ -109,6 +109,31 @@ class Emitter {
         return out;
     }
 
+    // 2D, one output row at a time: row i of the left pass is evaluated on every column
+    // (the same rounded products and sums as apply2d, but products are not shared between
+    // the rows of the left pass), then the right pass of that row, then `sink(i, values)`.
+    // Only one row of the intermediate is live at a time, so the inputs can stay in their
+    // narrow storage type (mixed precision: 64 f32 registers instead of 64 f64 values).
+    template <class Sink>
+    void apply2d_rowwise(const MatProg& mp, const std::vector<std::vector<std::string>>& data, Sink sink) {
+        const int R = mp.rows, K = mp.cols;
+        const int ncol = (int)data[0].size();
+        for (int i = 0; i < R; ++i) {
+            os_ << "  {\n";
+            std::vector<std::string> left(ncol);
+            for (int b = 0; b < ncol; ++b) {
+                std::vector<std::string> col(K);
+                for (int a = 0; a < K; ++a) col[a] = data[a][b];
+                products_.clear();
+                left[b] = row(mp.row[i], col);
+            }
+            products_.clear();
+            sink(i, apply(mp, left));
+            os_ << "  }\n";
+            products_.clear();
+        }
+    }
+
   private:
     std::string fresh() { return "t" + std::to_string(ctr_++); }
     std::string mul(const std::string& a, const std::string& b) const {
@@ -151,7 +176,14 @@ std::string header(const GenTypes& ty) {
        << "typedef " << tname(ty.compute_double) << " ct_t;\n"
        << "typedef " << tname(ty.uv_double) << " uv_t;\n"
        << "typedef " << tname(ty.y_double) << " y_t;\n"
-       << kIdivSmall;
+       << kIdivSmall
+       // f32 -> f64 at the point of use: volatile, so the compiler does not hoist one widened
+       // copy of every input and keep all of them live (row-wise mixed-precision transforms)
+       << "static __device__ __forceinline__ double wino_widen(float v) {\n"
+          "  double d;\n"
+          "  asm volatile(\"cvt.f64.f32 %0, %1;\" : \"=d\"(d) : \"f\"(v));\n"
+          "  return d;\n"
+          "}\n\n";
     return os.str();
 }
 
@@ -350,11 +382,16 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
        << "    for (int p = 0; p < " << P << "; ++p) op[p * plane] = (uv_t)(-0.0);\n"
           "    continue;\n"
           "  }\n";
+    // mixed precision (f32 tensors, f64 transforms): keep the window in its 64 f32 registers and
+    // evaluate one output row at a time (Emitter::apply2d_rowwise) instead of holding alpha^2
+    // f64 intermediates (166 registers, 16% occupancy at alpha = 8); same products, same sums
+    const bool rowwise = ty.compute_double && !ty.in_double && n >= 6 && tuning("k1rowwise") != "0";
+    const char* wt = rowwise ? "in_t" : "ct_t";
     std::vector<std::vector<std::string>> d(n, std::vector<std::string>(n));
     for (int a = 0; a < n; ++a)
         for (int b = 0; b < n; ++b) {
             d[a][b] = "x" + std::to_string(a) + "_" + std::to_string(b);
-            os << "  ct_t " << d[a][b] << ";\n";
+            os << "  " << wt << " " << d[a][b] << ";\n";
         }
     if (m % 2 == 0 && !ty.in_double) {
         // even m: every window starts at the same parity (w0 = m*tj - pad), so with an
@@ -372,7 +409,7 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
                     os << "    const float2 f" << a << "_" << q << " = __ldg(rp + " << a << " * W2 + " << q << ");\n";
                 for (int b = 0; b < n; ++b) {
                     const int e = b + sh;
-                    os << "    " << d[a][b] << " = (ct_t)f" << a << "_" << e / 2 << (e % 2 ? ".y" : ".x") << ";\n";
+                    os << "    " << d[a][b] << " = (" << wt << ")f" << a << "_" << e / 2 << (e % 2 ? ".y" : ".x") << ";\n";
                 }
             }
             os << "  }\n";
@@ -384,7 +421,7 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
     os << "    const in_t* rp = src + h0 * W + w0;\n";
     for (int a = 0; a < n; ++a)
         for (int b = 0; b < n; ++b)
-            os << "    " << d[a][b] << " = (ct_t)__ldg(rp + " << a << " * W + " << b << ");\n";
+            os << "    " << d[a][b] << " = (" << wt << ")__ldg(rp + " << a << " * W + " << b << ");\n";
     os << "  } else {\n";
     for (int a = 0; a < n; ++a)
         os << "    const bool r" << a << " = (unsigned)(h0 + " << a << ") < (unsigned)H;\n";
@@ -392,23 +429,39 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
         os << "    const bool c" << b << " = (unsigned)(w0 + " << b << ") < (unsigned)W;\n";
     for (int a = 0; a < n; ++a)
         for (int b = 0; b < n; ++b)
-            os << "    " << d[a][b] << " = (r" << a << " && c" << b << ") ? (ct_t)__ldg(src + (h0 + " << a
-               << ") * W + (w0 + " << b << ")) : (ct_t)0;\n";
+            os << "    " << d[a][b] << " = (r" << a << " && c" << b << ") ? (" << wt << ")__ldg(src + (h0 + " << a
+               << ") * W + (w0 + " << b << ")) : (" << wt << ")0;\n";
     os << "  }\n";
     Emitter em(os, ty.compute_double, ctr);
-    auto v = em.apply2d(BT, d);
-    for (int i = 0; i < n; ++i)
-        for (int j = 0; j < n; ++j)
-            os << "  op[" << (i * n + j) << " * plane] = " << store_cvt(ty.compute_double, ty.uv_double, v[i][j])
-               << ";\n";
+    if (rowwise) {
+        std::vector<std::vector<std::string>> dw(n, std::vector<std::string>(n));
+        for (int a = 0; a < n; ++a)
+            for (int b = 0; b < n; ++b) dw[a][b] = "wino_widen(" + d[a][b] + ")";
+        em.apply2d_rowwise(BT, dw, [&](int i, const std::vector<std::string>& row) {
+            for (int j = 0; j < n; ++j)
+                os << "  op[" << (i * n + j) << " * plane] = " << store_cvt(ty.compute_double, ty.uv_double, row[j])
+                   << ";\n";
+        });
+    } else {
+        auto v = em.apply2d(BT, d);
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j)
+                os << "  op[" << (i * n + j) << " * plane] = " << store_cvt(ty.compute_double, ty.uv_double, v[i][j])
+                   << ";\n";
+    }
     os << "  }\n}\n\n";
-    os << "extern \"C\" __global__ void __launch_bounds__(" << TB << ") wino_input_gather(\n"
+    // register cap through the minimum-blocks launch bound: 384 threads per SM (<= 168 registers:
+    // no spills; cfg3 mixed K1 79.9 -> 51.1 us, against 69.8 / 131.8 us at 512 / 640 threads, which
+    // spill); tuning key k1rowwise = 2..6 selects another bound (0: row-wise off)
+    const int rw_blocks = std::atoi(tuning("k1rowwise").c_str()) >= 2 ? std::atoi(tuning("k1rowwise").c_str()) : 3;
+    const std::string lb = rowwise ? std::to_string(TB) + ", " + std::to_string(rw_blocks * 128 / TB) : std::to_string(TB);
+    os << "extern \"C\" __global__ void __launch_bounds__(" << lb << ") wino_input_gather(\n"
           "    const in_t* __restrict__ x, uv_t* __restrict__ V, int C, int H, int W, int pad, int th,\n"
           "    int tw, long long T, long long Tp, long long Cp, int Wl, float rtw, float rth) {\n"
        << "  input_gather_body(x, V, C, H, W, pad, th, tw, T, Tp, Cp, rtw, rth, blockIdx.y * " << TB
        << ", blockIdx.x);\n"
        << "}\n\n"
-       << "extern \"C\" __global__ void __launch_bounds__(" << TB << ") wino_transforms_gather(\n"
+       << "extern \"C\" __global__ void __launch_bounds__(" << lb << ") wino_transforms_gather(\n"
           "    const in_t* __restrict__ x, uv_t* __restrict__ V, int C, int H, int W, int pad, int th,\n"
           "    int tw, long long T, long long Tp, long long Cp, int n_tb,\n"
           "    const in_t* __restrict__ w, uv_t* __restrict__ U, int K, long long Kp, int Wl, float rtw, float rth) {\n"
@@ -434,7 +487,11 @@ static void emit_output_gather(std::ostringstream& os, int r, int m, const MatPr
                                int& ctr, const char* mt = "uv_t") {
     const int n = r + m - 1;
     const char* PT = ty.y_double ? "double2" : "float2";
-    os << "extern \"C\" __global__ void __launch_bounds__(" << TB << ") wino_output_gather(\n"
+    const bool rowwise = ty.compute_double && !ty.uv_double && std::string(mt) == "uv_t" && n >= 6 &&
+                         tuning("k4rowwise") != "0";
+    const int rw_blocks = std::atoi(tuning("k4rowwise").c_str()) >= 2 ? std::atoi(tuning("k4rowwise").c_str()) : 3;  // cfg3 mixed K4 65.8 -> 47.2 us at 2..4 blocks, 61.5 at 5 (spills)
+    os << "extern \"C\" __global__ void __launch_bounds__(" << TB << (rowwise ? ", " + std::to_string(rw_blocks) : std::string())
+       << ") wino_output_gather(\n"
           "    const " << mt << "* __restrict__ Mm, y_t* __restrict__ y, int K, int Ho, int Wo, int th, int tw,\n"
           "    long long T, long long Tp, long long Kp, float rtw, float rth) {\n"
        << "  const int t0 = blockIdx.x * " << TB << ";\n"
@@ -455,38 +512,55 @@ static void emit_output_gather(std::ostringstream& os, int r, int m, const MatPr
        << "  const bool full = y0 + " << m << " <= Ho && x0 + " << m << " <= Wo;\n"
        << "#pragma unroll 1\n"
        << "  for (int k = k0; k < k0 + " << gather_kpt() << " && k < K; ++k, src += Tp, dst += HoWo) {\n";
+    // mixed precision (f32 M, f64 transform): keep the alpha^2 values in f32 registers and
+    // evaluate one output row at a time (see emit_input_gather)
     std::vector<std::vector<std::string>> mm(n, std::vector<std::string>(n));
     for (int a = 0; a < n; ++a)
         for (int b = 0; b < n; ++b) {
             mm[a][b] = "m" + std::to_string(a) + "_" + std::to_string(b);
-            os << "  const ct_t " << mm[a][b] << " = (ct_t)__ldg(src + " << (a * n + b) << " * plane);\n";
+            if (rowwise)
+                os << "  const " << mt << " " << mm[a][b] << " = __ldg(src + " << (a * n + b) << " * plane);\n";
+            else
+                os << "  const ct_t " << mm[a][b] << " = (ct_t)__ldg(src + " << (a * n + b) << " * plane);\n";
         }
     Emitter em(os, ty.compute_double, ctr);
-    auto yv = em.apply2d(AT, mm);
-    auto val = [&](int a, int b) { return store_cvt(ty.compute_double, ty.y_double, yv[a][b]); };
-    os << "  if (full) {\n";
-    if (m % 2 == 0) {
-        os << "    if ((Wo & 1) == 0) {\n";
-        for (int a = 0; a < m; ++a)
+    // stores of output row a (values already in the y type)
+    auto store_row = [&](int a, const std::vector<std::string>& v) {
+        os << "  if (full) {\n";
+        if (m % 2 == 0) {
+            os << "    if ((Wo & 1) == 0) {\n";
             for (int b = 0; b < m; b += 2)
                 os << "      *reinterpret_cast<" << PT << "*>(dst + " << a << " * Wo + " << b << ") = make_" << PT
-                   << "(" << val(a, b) << ", " << val(a, b + 1) << ");\n";
-        os << "    } else {\n";
-        for (int a = 0; a < m; ++a)
-            for (int b = 0; b < m; ++b) os << "      dst[" << a << " * Wo + " << b << "] = " << val(a, b) << ";\n";
-        os << "    }\n";
-    } else {
-        for (int a = 0; a < m; ++a)
-            for (int b = 0; b < m; ++b) os << "    dst[" << a << " * Wo + " << b << "] = " << val(a, b) << ";\n";
-    }
-    os << "  } else {\n";
-    for (int a = 0; a < m; ++a) {
-        os << "    if (y0 + " << a << " < Ho) {\n";
+                   << "(" << v[b] << ", " << v[b + 1] << ");\n";
+            os << "    } else {\n";
+            for (int b = 0; b < m; ++b) os << "      dst[" << a << " * Wo + " << b << "] = " << v[b] << ";\n";
+            os << "    }\n";
+        } else {
+            for (int b = 0; b < m; ++b) os << "    dst[" << a << " * Wo + " << b << "] = " << v[b] << ";\n";
+        }
+        os << "  } else if (y0 + " << a << " < Ho) {\n";
         for (int b = 0; b < m; ++b)
-            os << "      if (x0 + " << b << " < Wo) dst[" << a << " * Wo + " << b << "] = " << val(a, b) << ";\n";
-        os << "    }\n";
+            os << "    if (x0 + " << b << " < Wo) dst[" << a << " * Wo + " << b << "] = " << v[b] << ";\n";
+        os << "  }\n";
+    };
+    if (rowwise) {
+        std::vector<std::vector<std::string>> mw(n, std::vector<std::string>(n));
+        for (int a = 0; a < n; ++a)
+            for (int b = 0; b < n; ++b) mw[a][b] = "wino_widen(" + mm[a][b] + ")";
+        em.apply2d_rowwise(AT, mw, [&](int a, const std::vector<std::string>& row) {
+            std::vector<std::string> v(m);
+            for (int b = 0; b < m; ++b) v[b] = store_cvt(ty.compute_double, ty.y_double, row[b]);
+            store_row(a, v);
+        });
+    } else {
+        auto yv = em.apply2d(AT, mm);
+        for (int a = 0; a < m; ++a) {
+            std::vector<std::string> v(m);
+            for (int b = 0; b < m; ++b) v[b] = store_cvt(ty.compute_double, ty.y_double, yv[a][b]);
+            store_row(a, v);
+        }
     }
-    os << "  }\n  }\n}\n\n";
+    os << "  }\n}\n\n";
 }
 
 // K4 with the activation fused (conv stacks, BASELINE config 5): the same
