@@ -510,6 +510,7 @@ static void emit_output_gather(std::ostringstream& os, int r, int m, const MatPr
        << "  const " << mt << "* src = Mm + (long long)k0 * Tp + t;\n"
        << "  y_t* dst = y + (((long long)(img0 + di) * K + k0) * Ho + y0) * Wo + x0;\n"
        << "  const bool full = y0 + " << m << " <= Ho && x0 + " << m << " <= Wo;\n"
+       << "  const bool pair_ok = (Wo & 1) == 0 && (reinterpret_cast<size_t>(y) & (2 * sizeof(y_t) - 1)) == 0;\n"
        << "#pragma unroll 1\n"
        << "  for (int k = k0; k < k0 + " << gather_kpt() << " && k < K; ++k, src += Tp, dst += HoWo) {\n";
     // mixed precision (f32 M, f64 transform): keep the alpha^2 values in f32 registers and
@@ -526,21 +527,20 @@ static void emit_output_gather(std::ostringstream& os, int r, int m, const MatPr
     Emitter em(os, ty.compute_double, ctr);
     // stores of output row a (values already in the y type)
     auto store_row = [&](int a, const std::vector<std::string>& v) {
-        os << "  if (full) {\n";
         if (m % 2 == 0) {
-            os << "    if ((Wo & 1) == 0) {\n";
+            // x0 = m * tj and Wo even: a pair of columns is valid or clipped as a whole, so every
+            // tile (edge tiles too) stores 8/16-byte pairs -- half the L2 store requests
+            os << "  if (pair_ok) {\n"
+               << "    if (full || y0 + " << a << " < Ho) {\n";
             for (int b = 0; b < m; b += 2)
-                os << "      *reinterpret_cast<" << PT << "*>(dst + " << a << " * Wo + " << b << ") = make_" << PT
-                   << "(" << v[b] << ", " << v[b + 1] << ");\n";
-            os << "    } else {\n";
-            for (int b = 0; b < m; ++b) os << "      dst[" << a << " * Wo + " << b << "] = " << v[b] << ";\n";
-            os << "    }\n";
-        } else {
-            for (int b = 0; b < m; ++b) os << "    dst[" << a << " * Wo + " << b << "] = " << v[b] << ";\n";
+                os << "      if (full || x0 + " << b << " < Wo) *reinterpret_cast<" << PT << "*>(dst + " << a
+                   << " * Wo + " << b << ") = make_" << PT << "(" << v[b] << ", " << v[b + 1] << ");\n";
+            os << "    }\n"
+               << "  } else\n";
         }
-        os << "  } else if (y0 + " << a << " < Ho) {\n";
+        os << "  if (full || y0 + " << a << " < Ho) {\n";
         for (int b = 0; b < m; ++b)
-            os << "    if (x0 + " << b << " < Wo) dst[" << a << " * Wo + " << b << "] = " << v[b] << ";\n";
+            os << "    if (full || x0 + " << b << " < Wo) dst[" << a << " * Wo + " << b << "] = " << v[b] << ";\n";
         os << "  }\n";
     };
     if (rowwise) {
@@ -600,6 +600,21 @@ static void emit_output_gather_act(std::ostringstream& os, int r, int m, const M
     os << "  const int y0 = ti * " << m << ", x0 = tj * " << m << ";\n"
           "  if (!pool) {\n"
           "    float* dst = act + (((long long)(img0 + di) * K + k) * Ho + y0) * Wo + x0;\n";
+    if (m % 2 == 0) {
+        // whole tiles of an even-width output: 8-byte stores (x0 = m * tj is even), half as many
+        // store requests -- the un-pooled 56 / 28 / 14-pixel layers are bound by the L2's
+        // request rate for 4-byte partial-sector writes, not by bytes
+        os << "    // x0 and Wo even: a pair of columns is valid or clipped as a whole\n"
+              "    if ((Wo & 1) == 0 && (reinterpret_cast<size_t>(act) & 7) == 0) {\n";
+        for (int a = 0; a < m; ++a) {
+            os << "      if (y0 + " << a << " < Ho) {\n";
+            for (int b = 0; b < m; b += 2)
+                os << "        if (x0 + " << b << " < Wo) *reinterpret_cast<float2*>(dst + " << a << " * Wo + " << b
+                   << ") = make_float2(wino_relu(" << val(a, b) << "), wino_relu(" << val(a, b + 1) << "));\n";
+            os << "      }\n";
+        }
+        os << "      return;\n    }\n";
+    }
     for (int a = 0; a < m; ++a) {
         os << "    if (y0 + " << a << " < Ho) {\n";
         for (int b = 0; b < m; ++b)
