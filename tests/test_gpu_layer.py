@@ -129,6 +129,34 @@ def test_layer_validation_errors():
         W.conv2d_layer(ts, np.zeros((1, 2, 2, 2), np.float32), np.zeros((1, 2, 3, 3), np.float32), pad=0)
 
 
+def test_layer_with_4_byte_aligned_tensors():
+    """x and y that are only 4-byte aligned (views one element into a buffer): the 8-byte paired
+    loads / stores of K1 and K4 must fall back to scalar accesses, same bits."""
+    ts = W.build_transforms(3, 6, W.parse_points("0,-1,1,1/2,-1/2,2,-2,inf"))
+    cfg = W.ConvConfig("fp32", "huffman", "pairwise")
+    N, C, K, H = 2, 5, 6, 16                      # even width: the paired paths apply when aligned
+    x = torch.from_numpy(O.synthetic((N, C, H, H), 11, 0)).cuda()
+    w = torch.from_numpy(O.synthetic((K, C, 3, 3), 11, 1)).cuda()
+    op = W.layer_op(ts, cfg, N, C, H, H, K, 1)
+    want = op(x, w)
+    xb = torch.empty(x.numel() + 1, device="cuda")
+    xo = xb[1:].view(x.shape)
+    xo.copy_(x)
+    yb = torch.empty(want.numel() + 1, device="cuda")
+    yo = yb[1:].view(want.shape)
+    assert xo.data_ptr() % 8 == 4 and yo.data_ptr() % 8 == 4
+    got = op(xo, w, out=yo)
+    assert torch.equal(got.view(torch.int32), want.view(torch.int32))
+    from paper_1803_10986_b200.stack import ConvStack
+    st = ConvStack(ts, cfg, [(C, K, False)], N, H)
+    st.set_weights([w.cpu().numpy()])
+    a_ref = st.forward(x).clone()
+    ab = torch.empty(a_ref.numel() + 1, device="cuda")
+    st.act[0] = ab[1:].view(a_ref.shape)
+    assert st.act[0].data_ptr() % 8 == 4
+    assert torch.equal(st.forward(x).view(torch.int32), a_ref.view(torch.int32))
+
+
 NHWC_CASES = [
     # r, m, points, N, C, K, H, W, pad  (odd C / K around the 16-channel block, partial edge tiles, pad 0 / 2)
     (3, 4, "0,1,-1,1/2,-1/2,inf", 2, 9, 5, 14, 11, 1),
