@@ -152,6 +152,19 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+def cpu_model():
+    """CPU model string of the host (state the core count and the CPU model)."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.lower().startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or platform.machine()
+
+
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -170,7 +183,7 @@ def run_reference(args, cfg):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32" if cfg[10] == "fp32" else "f32/f64",
             "data": "synthetic (seeded Philox U[-1,1] inputs, He-normal filters)",
             "config": config_dict(args, cfg),
-            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": procs, "kind": "port",
+            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": procs, "cpu_model": cpu_model(), "kind": "port",
                              "sample": f"full batch of {x.shape[0]} images per step, oracle/wino_oracle.py "
                                        f"layer_conv2d (numpy restatement of the reference) over {procs} processes"},
             "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -435,7 +448,7 @@ def run_gpu(args, cfg):
             procs = min(host_cores(), xs.shape[0])
             t = cpu_layer_time(cfg, xs, w_np, procs)
             fl = direct_flops(cfg) * xs.shape[0] / N
-            line["cpu_baseline"] = {"value": fl / t / 1e12, "unit": "TFLOP/s", "cores": procs, "kind": "port",
+            line["cpu_baseline"] = {"value": fl / t / 1e12, "unit": "TFLOP/s", "cores": procs, "cpu_model": cpu_model(), "kind": "port",
                                     "sample": f"{xs.shape[0]} of {N} images of the same layer, oracle/wino_oracle.py "
                                               f"layer_conv2d over {procs} processes, {t:.2f} s"}
         print(json.dumps(line), flush=True)
@@ -515,7 +528,7 @@ def run_reference_vgg(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Philox U[-1,1] 224x224x3 images, He-normal filters)",
             "config": vgg_config(args, args.vgg_batch, 1),
-            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": procs, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": procs, "cpu_model": cpu_model(), "kind": "port", "sample": sample},
             "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -723,14 +736,14 @@ def run_vgg(args):
             xs = x_np[: args.cpu_vgg_images]
             t_all, outs, act = vgg_cpu_forward(xs, ws_np, procs)
             fl = vgg_direct_flops(xs.shape[0])
-            line["cpu_baseline"] = {"value": fl / t_all / 1e12, "unit": "TFLOP/s", "cores": procs, "kind": "port",
+            line["cpu_baseline"] = {"value": fl / t_all / 1e12, "unit": "TFLOP/s", "cores": procs, "cpu_model": cpu_model(), "kind": "port",
                                     "sample": f"{xs.shape[0]} of {n} images through all 13 layers "
                                               f"(oracle/stack_pool.py over {procs} processes), {t_all:.2f} s"}
             if args.cpu_1core_images > 0:
                 x1 = x_np[: args.cpu_1core_images]
                 t1, _, _ = vgg_cpu_forward(x1, ws_np, 1)
                 line["cpu_baseline_1core"] = {
-                    "value": vgg_direct_flops(x1.shape[0]) / t1 / 1e12, "unit": "TFLOP/s", "cores": 1,
+                    "value": vgg_direct_flops(x1.shape[0]) / t1 / 1e12, "unit": "TFLOP/s", "cores": 1, "cpu_model": cpu_model(),
                     "kind": "port", "sample": f"{x1.shape[0]} image(s) through all 13 layers, one process "
                                               f"(numpy ufuncs are single-threaded), {t1:.2f} s"}
             same = [bool(outs[i].tobytes() == conv_first[i].tobytes()) for i in range(len(outs))]
