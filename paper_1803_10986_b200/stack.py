@@ -219,8 +219,19 @@ class StackPipeline:
     tensors.  Weights stay resident on the device (set_weights once)."""
 
     def __init__(self, ts, cfg: ConvConfig, layers, N, H, W=None, chunks=4, pad=1, contraction="exact"):
-        chunks = max(1, min(int(chunks), N))
-        self.bounds = [(i * N // chunks, (i + 1) * N // chunks) for i in range(chunks)]
+        if isinstance(chunks, (list, tuple)):
+            # explicit image counts (scaled to N if they do not add up): a small first chunk starts
+            # the compute stream early, a small last chunk shortens the exposed D2H tail
+            sizes_ = [max(1, int(round(c * N / sum(chunks)))) for c in chunks]
+            sizes_[-1] = N - sum(sizes_[:-1])
+            if min(sizes_) < 1:  # batch too small for this split: equal chunks
+                k = max(1, min(len(chunks), N))
+                sizes_ = [(i + 1) * N // k - i * N // k for i in range(k)]
+            edges = np.cumsum([0] + sizes_)
+            self.bounds = [(int(a), int(b)) for a, b in zip(edges[:-1], edges[1:])]
+        else:
+            chunks = max(1, min(int(chunks), N))
+            self.bounds = [(i * N // chunks, (i + 1) * N // chunks) for i in range(chunks)]
         sizes = sorted({b - a for a, b in self.bounds})
         self.stacks = {n: ConvStack(ts, cfg, layers, n, H, W, pad, contraction) for n in sizes}
         first = self.stacks[sizes[0]]

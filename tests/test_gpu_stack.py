@@ -136,3 +136,30 @@ def test_smallc_fused_kernel_matches_unfused(cs):
                                                               _native.as_ptr(got), mode, s))
                 torch.cuda.synchronize()
                 assert torch.equal(got.view(torch.int32), want.view(torch.int32)), (m, C, cs, mode)
+
+
+@pytest.mark.parametrize("chunks", [1, 3, [1, 3, 1], [32, 192, 32], [4, 4, 4, 4, 4, 4, 4]],
+                         ids=lambda c: "chunks=" + str(c).replace(" ", ""))
+def test_stack_pipeline_host_buffers_bitwise(chunks):
+    """StackPipeline (pinned host images in, final activation out, copies overlapped over image
+    chunks of equal or explicit sizes) equals the one-shot device forward, bit for bit."""
+    from paper_1803_10986_b200.stack import ConvStack, StackPipeline, he_normal_weights
+    layers = [(3, 8, True), (8, 12, False), (12, 9, True)]
+    ts = W.build_transforms(3, 6, W.parse_points(P8))
+    cfg = W.ConvConfig("fp32", "huffman", "pairwise")
+    N, H = 5, 26
+    x = np.stack([O.synthetic((3, H, H), 8, i) for i in range(N)])
+    ws = he_normal_weights(layers, 3, seed=5)
+    st = ConvStack(ts, cfg, layers, N, H)
+    st.set_weights(ws)
+    want = st.forward(torch.from_numpy(x).cuda()).cpu()
+    pipe = StackPipeline(ts, cfg, layers, N, H, chunks=chunks)
+    assert pipe.bounds[0][0] == 0 and pipe.bounds[-1][1] == N
+    assert all(b > a for a, b in pipe.bounds) and all(p[1] == q[0] for p, q in zip(pipe.bounds, pipe.bounds[1:]))
+    pipe.set_weights(ws)
+    xh = torch.from_numpy(x).pin_memory()
+    yh = torch.empty(pipe.out_shape, dtype=torch.float32).pin_memory()
+    for _ in range(2):  # the second call reuses every buffer and event
+        pipe(xh, yh)
+        torch.cuda.synchronize()
+        assert torch.equal(yh.view(torch.int32), want.view(torch.int32))
