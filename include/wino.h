@@ -183,6 +183,19 @@ int wino_smallc_supported(wino_plan* plan, const wino_layer_shape* s);
 int wino_contract_output_smallc(wino_plan* plan, const wino_layer_shape* s, const void* U, const void* V,
                                 void* out, int mode, void* stream);
 
+/* K2 + K1, then K3 + K4 (+ activation) in ONE exact kernel for alpha^2 <= 16 (F(2x2,3x3),
+ * F(2x2,2x2), ...; fp32 plans, exact or ffma contraction): a CTA contracts all alpha^2
+ * points of a 64-filter x 64-tile block and parks the accumulators in tensor memory
+ * (each thread's private TMEM columns), then runs the output transform from there, so M
+ * never exists in shared or global memory -- engine.py:415-423 composed per (filter,
+ * tile) as engine.py:426-429.  mode 0: y, 1: ReLU, 2: ReLU + 2x2 max-pool (even m).
+ * Bitwise equal to wino_conv2d (+ wino_relu_pool).  The workspace holds U and V only
+ * (wino_fused_workspace bytes, 256-byte aligned). */
+int wino_fused_supported(wino_plan* plan, const wino_layer_shape* s);
+int wino_fused_workspace(wino_plan* plan, const wino_layer_shape* s, size_t* bytes);
+int wino_conv2d_fused(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w,
+                      void* out, int mode, void* workspace, size_t workspace_bytes, void* stream);
+
 /* K2 -> K1 -> K3 -> K4 with a caller-provided workspace of
  * layout.workspace_bytes bytes (256-byte aligned). */
 int wino_conv2d(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w,

@@ -68,6 +68,10 @@ SIGNATURES = [
     ("wino_output_transform_nhwc", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p]),
     ("wino_conv2d_nhwc", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                           c_void_p]),
+    ("wino_fused_supported", c_int, [c_void_p, POINTER(LayerShape)]),
+    ("wino_fused_workspace", c_int, [c_void_p, POINTER(LayerShape), POINTER(c_size_t)]),
+    ("wino_conv2d_fused", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_int, c_void_p,
+                           c_size_t, c_void_p]),
     ("wino_conv2d", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                             c_void_p]),
     ("wino_tile_hadamard2d", c_int, [c_void_p, c_int64, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -1047,6 +1047,67 @@ std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, 
     return os.str();
 }
 
+// Output transform of ONE (filter k, tile t) pair from its alpha^2 point sums in registers
+// (mr[a * n + b], raw fp32 bits), for the fused exact contraction (contract_template.cuh
+// WINO_FUSE_P): (A^T M) A in the plan's order, crop, and the NCHW store -- omode 0: y,
+// 1: ReLU, 2: ReLU of the 2x2 max-pool (even m; same expressions as wino_output_gather_act).
+// fp32 plans only.  The text is prepended to the contraction template.
+std::string gen_fused_out_source(int r, int m, const MatProg& AT) {
+    const int n = r + m - 1;
+    std::ostringstream os;
+    int ctr = 0;
+    os << "static __device__ __forceinline__ float wino_relu(float v) { return v > 0.f ? v : 0.f; }\n"
+          "static __device__ __forceinline__ void wino_fused_out(const unsigned* mr, int k, int t,\n"
+          "    float* __restrict__ out, int K, int Ho, int Wo, int th, int tw, int omode) {\n";
+    std::vector<std::vector<std::string>> mm(n, std::vector<std::string>(n));
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+            mm[a][b] = "m" + std::to_string(a) + "_" + std::to_string(b);
+            os << "  const float " << mm[a][b] << " = __uint_as_float(mr[" << (a * n + b) << "]);\n";
+        }
+    os << "  const int g = t / tw, tj = t - g * tw;\n"
+          "  const int img = g / th, ti = g - img * th;\n"
+       << "  const int y0 = ti * " << m << ", x0 = tj * " << m << ";\n";
+    Emitter em(os, false, ctr);
+    auto yv = em.apply2d(AT, mm);
+    os << "  if (omode < 2) {\n"
+          "    float* dst = out + (((long long)img * K + k) * Ho + y0) * Wo + x0;\n";
+    if (m % 2 == 0) {
+        os << "    if ((Wo & 1) == 0 && (reinterpret_cast<size_t>(out) & 7) == 0) {\n";
+        for (int a = 0; a < m; ++a) {
+            os << "      if (y0 + " << a << " < Ho) {\n";
+            for (int b = 0; b < m; b += 2)
+                os << "        if (x0 + " << b << " < Wo) *reinterpret_cast<float2*>(dst + " << a << " * Wo + " << b
+                   << ") = omode ? make_float2(wino_relu(" << yv[a][b] << "), wino_relu(" << yv[a][b + 1]
+                   << ")) : make_float2(" << yv[a][b] << ", " << yv[a][b + 1] << ");\n";
+            os << "      }\n";
+        }
+        os << "      return;\n    }\n";
+    }
+    for (int a = 0; a < m; ++a) {
+        os << "    if (y0 + " << a << " < Ho) {\n";
+        for (int b = 0; b < m; ++b)
+            os << "      if (x0 + " << b << " < Wo) dst[" << a << " * Wo + " << b << "] = omode ? wino_relu(" << yv[a][b]
+               << ") : " << yv[a][b] << ";\n";
+        os << "    }\n";
+    }
+    os << "    return;\n  }\n";
+    if (m % 2 == 0) {
+        os << "  const int Hp = Ho >> 1, Wp = Wo >> 1, py0 = y0 >> 1, px0 = x0 >> 1;\n"
+              "  float* dst = out + (((long long)img * K + k) * Hp + py0) * Wp + px0;\n";
+        for (int a = 0; a < m / 2; ++a) {
+            os << "  if (py0 + " << a << " < Hp) {\n";
+            for (int b = 0; b < m / 2; ++b)
+                os << "    if (px0 + " << b << " < Wp) dst[" << a << " * Wp + " << b << "] = wino_relu(fmaxf(fmaxf("
+                   << yv[2 * a][2 * b] << ", " << yv[2 * a][2 * b + 1] << "), fmaxf(" << yv[2 * a + 1][2 * b] << ", "
+                   << yv[2 * a + 1][2 * b + 1] << ")));\n";
+            os << "  }\n";
+        }
+    }
+    os << "}\n\n";
+    return os.str();
+}
+
 std::string gen_tile_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
                             const GenTypes& ty) {
     const int n = r + m - 1, P = n * n;

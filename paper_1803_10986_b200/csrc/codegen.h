@@ -48,6 +48,9 @@ std::string gen_layer_source_tc(int r, int m, const MatProg& G, const MatProg& B
                                 const GenTypes& ty, bool fp16, int fused_nk = 0);
 std::string gen_tile_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
                             const GenTypes& ty);
+// wino_fused_out(): output transform of one (filter, tile) pair from registers, for the fused
+// exact contraction (contract_template.cuh WINO_FUSE_P); fp32 plans
+std::string gen_fused_out_source(int r, int m, const MatProg& AT);
 
 // Gather transforms: channels per K1 thread / output channels per K4 thread (the
 // tile index math is amortised over them).  Must divide every channel padding

@@ -48,6 +48,18 @@
 #ifndef WINO_PACK
 #define WINO_PACK 0
 #endif
+#ifndef WINO_FUSE_P
+// > 0: fused exact K3 + K4 (+ activation).  One CTA contracts all WINO_FUSE_P = alpha^2 points
+// of a (filter block, tile block) pair, one after the other, and parks every finished
+// accumulator in tensor memory: with the 32x32b access shape a thread reaches only its own
+// TMEM lane, so its 512 / (warps per lane quarter) columns are a private scratchpad that holds
+// its TM x TN microtile for every point, [pair][point]-major.  After the last point each thread
+// reads back the alpha^2 point sums of one (filter, tile) pair with a single tcgen05.ld and runs
+// the generated output transform (wino_fused_out, prepended by the host) -- M never exists in
+// shared or global memory.  Needs alpha^2 <= 16 with the 4 x 4 microtile and 8 consumer warps
+// (16 pairs x 16 points = 256 columns per thread).
+#define WINO_FUSE_P 0
+#endif
 #ifndef WINO_WN
 #define WINO_WN 0  // > 0: warp-tiled thread map, WINO_WN lanes along t x 32/WINO_WN lanes along k
 #endif
@@ -174,9 +186,38 @@ static __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsi
 #define WINO_REGS __launch_bounds__(NTHR + (WINO_NOPROD ? 0 : 32))
 #endif
 
+#if WINO_FUSE_P
+#define WINO_FUSE_PS 16  // TMEM columns per (filter, tile) pair: alpha^2 rounded up to an x16 load
+static_assert(WINO_FUSE_P <= WINO_FUSE_PS && WINO_TM * WINO_TN * WINO_FUSE_PS * (NCW / 4) <= 512 && NCW % 4 == 0 &&
+                  !WINO_DT_IS_DOUBLE && !WINO_NOPROD,
+              "fused output: alpha^2 x microtile must fit the thread's TMEM columns");
+static __device__ __forceinline__ void tmem_st1(unsigned taddr, unsigned v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
+}
+static __device__ __forceinline__ void tmem_ld16(unsigned taddr, unsigned* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, "
+        "[%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+#endif
+
+// (one textual kernel definition with textually balanced braces: the host wraps every kernel
+// body in an #if by brace matching, wino_host.cu wrap_kernels)
+#if WINO_FUSE_P
+#define WINO_FUSE_PARAMS , float *__restrict__ Y, int K, int Ho, int Wo, int th, int tw, long long T, int omode
+#else
+#define WINO_FUSE_PARAMS
+#endif
 extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, const DT* __restrict__ V,
                                                   DT* __restrict__ M, long long Kp, long long Tp, long long Cp,
-                                                  int n_tiles, u64 nz2) {
+                                                  int n_tiles, u64 nz2 WINO_FUSE_PARAMS) {
+#if WINO_FUSE_P
+    __shared__ unsigned tmem_slot;
+#endif
     extern __shared__ __align__(128) unsigned char smem_raw[];
     DT* sU = reinterpret_cast<DT*>(smem_raw);      // [STAGES][BK][BM]
     DT* sV = sU + WINO_STAGES * WINO_BK * BM;      // [STAGES][BK][BN]
@@ -222,18 +263,47 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
         for (int gg = 0; gg < WINO_STAGES; ++gg) issue(gg);
 #endif
     }
+#if WINO_FUSE_P
+    if (warp == 0) {  // all 512 TMEM columns: one CTA per SM
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                     "r"(512u)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+#endif
     __syncthreads();
+#if WINO_FUSE_P
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const unsigned tmem = tmem_slot;
+#endif
 
     if (!WINO_NOPROD && warp == NCW) {
         // ------------------------------------------------ producer warp
         if (lane == 0) {
             int g = 0;  // global stage counter across this CTA's tiles
+#if WINO_FUSE_P
+            // fused: a CTA takes whole (kb, tb) groups and walks their points in order
 #pragma unroll 1
-            for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+            for (int gi = blockIdx.x * WINO_FUSE_P; gi < n_tiles; gi += gridDim.x * WINO_FUSE_P)
+#pragma unroll 1
+            for (int tile = gi; tile < gi + WINO_FUSE_P; ++tile)
+#else
+#pragma unroll 1
+            for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x)
+#endif
+            {
+#if WINO_FUSE_P
+                const long long p = tile % WINO_FUSE_P;
+                const int grp = tile / WINO_FUSE_P;
+                const int tb = grp % n_tb;
+                const int kb = grp / n_tb;
+#else
                 const int tb = tile % n_tb;
                 const int rest = tile / n_tb;
                 const int kb = rest % n_kb;
                 const long long p = rest / n_kb;
+#endif
                 const DT* gU = U + (p * Kp + (long long)kb * BM) * Cp;
                 const DT* gV = V + (p * Tp + (long long)tb * BN) * Cp;
 #pragma unroll 1
@@ -269,12 +339,31 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
 #endif
     int g = 0;
 
+#if WINO_FUSE_P
+    const unsigned tcol0 = tmem + ((unsigned)((warp & 3) * 32) << 16) + (unsigned)((warp >> 2) * (WINO_TM * WINO_TN * WINO_FUSE_PS));
 #pragma unroll 1
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    for (int gi = blockIdx.x * WINO_FUSE_P; gi < n_tiles; gi += gridDim.x * WINO_FUSE_P)
+#endif
+    {  // fused: one (filter block, tile block) group; otherwise a plain block
+#if WINO_FUSE_P
+    const int grp = gi / WINO_FUSE_P;
+    const int tb = grp % n_tb;
+    const int kb = grp / n_tb;
+#pragma unroll 1
+    for (int pp = 0; pp < WINO_FUSE_P; ++pp)
+#else
+#pragma unroll 1
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x)
+#endif
+    {
+#if WINO_FUSE_P
+        const long long p = pp;
+#else
         const int tb = tile % n_tb;
         const int rest = tile / n_tb;
         const int kb = rest % n_kb;
         const long long p = rest / n_kb;
+#endif
 
 #if WINO_SUM == 0
         acc_t acc[WINO_TM][NJ];
@@ -485,6 +574,23 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
         }
 #endif
 
+#if WINO_FUSE_P
+        // park this point's microtile in the thread's TMEM columns, [pair][point]-major
+        static_assert(GM == 1 && GN == 1, "fused output: one 16-byte vector per microtile side");
+#pragma unroll
+        for (int i = 0; i < WINO_TM; ++i)
+#pragma unroll
+            for (int jj = 0; jj < WINO_TN; ++jj) {
+#if WINO_PACK
+                float lo, hi;
+                asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc[i][jj >> 1]));
+                const float val = (jj & 1) ? hi : lo;
+#else
+                const float val = acc[i][jj];
+#endif
+                tmem_st1(tcol0 + (unsigned)((i * WINO_TN + jj) * WINO_FUSE_PS) + (unsigned)pp, __float_as_uint(val));
+            }
+#else
         DT* gM = M + (p * Kp + (long long)kb * BM) * Tp + (long long)tb * BN;
 #pragma unroll
         for (int q = 0; q < GM; ++q)
@@ -511,5 +617,28 @@ extern "C" __global__ void WINO_REGS wino_contract(const DT* __restrict__ U, con
                     *reinterpret_cast<vec_t*>(gM + row * Tp + h * (WINO_THN * VW) + tn * VW) = w4;
                 }
             }
+#endif
+    }  // tiles (fused: points of the group)
+#if WINO_FUSE_P
+        // all points of this (filter block, tile block) are parked: output transform per pair
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+#pragma unroll 1
+        for (int q = 0; q < WINO_TM * WINO_TN; ++q) {
+            unsigned mr[WINO_FUSE_PS];
+            tmem_ld16(tcol0 + (unsigned)(q * WINO_FUSE_PS), mr);
+            const int k = kb * BM + tm * VW + q / WINO_TN;
+            const long long t = (long long)tb * BN + tn * VW + q % WINO_TN;
+            if (k < K && t < T) wino_fused_out(mr, k, (int)t, Y, K, Ho, Wo, th, tw, omode);
+        }
+#endif
+    }  // groups (fused)
+#if WINO_FUSE_P
+    // every consumer warp is done with tensor memory before warp 0 frees it
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(NTHR) : "memory");
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u) : "memory");
     }
+#endif
 }

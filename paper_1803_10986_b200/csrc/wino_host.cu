@@ -393,6 +393,16 @@ struct GemmCfg {
 
 }  // namespace wino
 
+// The fused exact path (wino_conv2d_fused) runs the regular transforms with the tile config
+// of its own contraction: while a ForceCand guard is alive on this thread, wino_plan::pick()
+// returns that candidate instead of choosing by shape.
+static thread_local int g_force_cand = -1;
+struct ForceCand {
+    int prev;
+    explicit ForceCand(int ci) : prev(g_force_cand) { g_force_cand = ci; }
+    ~ForceCand() { g_force_cand = prev; }
+};
+
 // ------------------------------------------------------------------ plan
 struct wino_plan {
     int r, m, n, precision, chsum, mode;
@@ -402,6 +412,7 @@ struct wino_plan {
     wino::GenTypes ty;
     wino::GemmCfg gemm;                 // cands[0]
     std::vector<wino::GemmCfg> cands;   // contraction tile configs a layer shape picks from
+    int fused_ci = -1;                  // candidate of the fused exact K3 + K4 kernel (never picked by shape)
     wino::Module layer, tile;           // layer: transforms blocked for cands[0]
     std::mutex mu;
     std::map<int, std::unique_ptr<wino::Module>> contract;  // key: counter levels * 16 + candidate
@@ -465,6 +476,7 @@ struct wino_plan {
     // device answers); ties keep the earlier candidate.
     static long long rup(long long v, long long q) { return (v + q - 1) / q * q; }
     int pick(const wino_layer_shape* s) const {
+        if (g_force_cand >= 0 && g_force_cand < (int)cands.size()) return g_force_cand;
         if (cands.size() < 2) return 0;
         const int Ho = s->H + 2 * s->pad - r + 1, Wo = s->W + 2 * s->pad - r + 1;
         const long long T = (long long)s->N * ((Ho + m - 1) / m) * ((Wo + m - 1) / m);
@@ -472,6 +484,7 @@ struct wino_plan {
         int best = 0;
         double best_cost = 0;
         for (size_t i = 0; i < cands.size(); ++i) {
+            if ((int)i == fused_ci) continue;
             const long long bm = cands[i].bm(), bn = cands[i].bn();
             const long long tiles = (long long)n * n * ((s->K + bm - 1) / bm) * (((T > 0 ? T : 1) + bn - 1) / bn);
             // measured per-flop speed of the 4x8 / 4x4 microtiles vs 8x8: 0.91 / 0.92 (cfg2, cfg3)
@@ -502,7 +515,7 @@ struct wino_plan {
 
     int sum_mode() const { return (mode == WINO_CONTRACT_FFMA ? 2 : 0) + (chsum == WINO_SUM_PAIRWISE ? 1 : 0); }
 
-    wino::Module* contract_module(long long Cp, int ci = 0) {
+    wino::Module* contract_module(long long Cp, int ci = 0, bool fused_out = false) {
         const wino::GemmCfg& gemm = cands.empty() ? this->gemm : cands[ci];
         int levels = 1;
         const long long Q = Cp / gemm.bk;  // pairwise: the dynamic counter runs over stages
@@ -511,7 +524,7 @@ struct wino_plan {
         bool slots_smem = false;
         gemm.smem_bytes(levels, ty.uv_double ? 8 : 4, &slots_smem);
         std::lock_guard<std::mutex> g(mu);
-        const int key = levels * 16 + ci;
+        const int key = levels * 16 + ci + (fused_out ? 1 << 20 : 0);
         auto it = contract.find(key);
         if (it != contract.end()) return it->second.get();
         auto mod = std::make_unique<wino::Module>();
@@ -524,11 +537,13 @@ struct wino_plan {
            << (levels > 0 ? levels : 1) << "\n#define WINO_MAXREG " << gemm.maxreg << "\n#define WINO_KU " << (gemm.ku > 0 ? gemm.ku : gemm.bk) << "\n#define WINO_NOPROD " << gemm.noprod
            << "\n#define WINO_PACK " << (gemm.pack && !dbl ? 1 : 0) << "\n#define WINO_WN " << gemm.wn << "\n#define WINO_SLOTS_SMEM " << slots_smem << "\n"
            << (!wino::tuning("dbuf").empty() ? "#define WINO_DBUF " + wino::tuning("dbuf") + "\n" : std::string())
-           << ""
+           << (fused_out ? "#define WINO_FUSE_P " + std::to_string(n * n) + "\n" + wino::gen_fused_out_source(r, m, AT)
+                         : std::string())
            << wino::kContractTemplate;
         mod->source = os.str();
-        mod->name = "wino_contract_s" + std::to_string(sum_mode()) + "_L" + std::to_string(levels) + "_c" +
-                    std::to_string(ci) + ".cu";
+        mod->name = std::string(fused_out ? "wino_contract_fused_r" + std::to_string(r) + "m" + std::to_string(m) + "_s"
+                                          : "wino_contract_s") +
+                    std::to_string(sum_mode()) + "_L" + std::to_string(levels) + "_c" + std::to_string(ci) + ".cu";
         wino::Module* raw = mod.get();
         contract[key] = std::move(mod);
         return raw;
@@ -810,6 +825,15 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
         // C not a multiple of 64: 32-channel stages pad less
         p->cands.push_back({4, 4, 16, 16, 32, 3, 168, 8, 0, 1});
     }
+    if (!env_gemm && contract_mode < WINO_CONTRACT_TC_BF16 && precision == WINO_FP32 && n * n <= 16) {
+        // fused exact K3 + K4 (wino_conv2d_fused): 64 x 64 tile, 8 consumer warps x 4x4 microtile,
+        // alpha^2 x 16 accumulators per thread parked in tensor memory (contract_template.cuh)
+        p->fused_ci = (int)p->cands.size();
+        if (channel_sum == WINO_SUM_PAIRWISE)
+            p->cands.push_back({4, 4, 16, 16, 64, 2, 168, 8, 0, 1});
+        else
+            p->cands.push_back({4, 4, 16, 16, 16, 4, 0, 16, 0, 1});
+    }
     const std::string tag = "r" + std::to_string(r) + "m" + std::to_string(m) + "p" + std::to_string(precision);
     p->layer.name = "wino_layer_" + tag + ".cu";
     p->layer.source = contract_mode >= WINO_CONTRACT_TC_BF16
@@ -842,10 +866,14 @@ int wino_plan_source(const wino_plan* plan, int which, char* buf, size_t cap, si
 }
 
 int wino_plan_cubin(wino_plan* plan, int which, int channels, void* buf, size_t cap, size_t* len) {
-    if (!plan || which < 0 || which > 2) return wino::fail(WINO_EINVAL, "plan_cubin: bad arguments");
+    if (!plan || which < 0 || which > 3) return wino::fail(WINO_EINVAL, "plan_cubin: bad arguments");
+    if (which == 3 && plan->fused_ci < 0) return wino::fail(WINO_EUNSUPPORTED, "plan_cubin: no fused exact kernel for this plan");
     wino::Module* mod = which == 0 ? &plan->layer
                         : which == 1 ? &plan->tile
-                                     : plan->contract_module(round_up(channels > 0 ? channels : 1, plan->gemm.bk));
+                        : which == 2 ? plan->contract_module(round_up(channels > 0 ? channels : 1, plan->gemm.bk))
+                                     : plan->contract_module(round_up(channels > 0 ? channels : 1,
+                                                                      plan->cands[plan->fused_ci].bk),
+                                                             plan->fused_ci, true);
     const wino::Compiled* bin = nullptr;
     int rc = mod->ensure_compiled("*", &bin);
     if (rc) return rc;
@@ -1189,6 +1217,76 @@ int wino_conv2d_nhwc(wino_plan* plan, const wino_layer_shape* s, const void* x, 
     if ((rc = wino_input_transform_nhwc(plan, s, x, V, stream))) return rc;
     if ((rc = wino_contract(plan, s, U, V, M, stream))) return rc;
     return wino_output_transform_nhwc(plan, s, M, y, stream);
+}
+
+int wino_fused_supported(wino_plan* plan, const wino_layer_shape* s) {
+    wino_layer_layout L;
+    if (!plan || !s || plan->fused_ci < 0) return 0;
+    ForceCand guard(plan->fused_ci);
+    if (layout_of(plan, s, &L)) return 0;
+    const long long groups = (L.Kp / L.bm) * (L.Tp / L.bn);
+    return groups > 0 && groups * L.P < (1LL << 30);
+}
+
+int wino_fused_workspace(wino_plan* plan, const wino_layer_shape* s, size_t* bytes) {
+    if (!bytes) return wino::fail(WINO_EINVAL, "fused_workspace: null bytes");
+    if (!wino_fused_supported(plan, s))
+        return wino::fail(WINO_EUNSUPPORTED, "fused: needs an fp32 plan with an FP32-pipe contraction and alpha^2 <= 16");
+    ForceCand guard(plan->fused_ci);
+    wino_layer_layout L;
+    int rc = layout_of(plan, s, &L);
+    if (rc) return rc;
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    *bytes = al(L.u_bytes) + al(L.v_bytes);
+    return WINO_OK;
+}
+
+int wino_conv2d_fused(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w, void* out, int mode,
+                      void* workspace, size_t workspace_bytes, void* stream) {
+    if (!wino_fused_supported(plan, s))
+        return wino::fail(WINO_EUNSUPPORTED, "conv2d_fused: needs an fp32 plan with an FP32-pipe contraction and alpha^2 <= 16");
+    if (mode < 0 || mode > 2) return wino::fail(WINO_EINVAL, "conv2d_fused: mode must be 0 (y), 1 (ReLU) or 2 (ReLU + 2x2 max-pool)");
+    if (mode == 2 && (plan->m & 1)) return wino::fail(WINO_EUNSUPPORTED, "conv2d_fused: pooling needs an even m");
+    ForceCand guard(plan->fused_ci);  // transforms and layout follow the fused kernel's 64 x 64 blocking
+    wino_layer_layout L;
+    int rc = layout_of(plan, s, &L);
+    if (rc) return rc;
+    if (s->N == 0) return WINO_OK;
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    if (!workspace || workspace_bytes < al(L.u_bytes) + al(L.v_bytes) || ((uintptr_t)workspace & 255))
+        return wino::fail(WINO_EINVAL, "conv2d_fused: workspace missing, too small or not 256-byte aligned");
+    char* U = (char*)workspace;
+    char* V = U + al(L.u_bytes);
+    if ((rc = wino_transforms(plan, s, x, w, U, V, stream))) return rc;
+    const int ci = plan->fused_ci;
+    const wino::GemmCfg& g = plan->cands[ci];
+    wino::Module* mod = plan->contract_module(L.Cp, ci, true);
+    CUfunction f;
+    if ((rc = mod->function("wino_contract", &f))) return rc;
+    long long Kp = L.Kp, Tp = L.Tp, Cp = L.Cp, T = L.T;
+    const long long groups = (Kp / g.bm()) * (Tp / g.bn());
+    int n_tiles = (int)(groups * L.P);
+    int levels = 1;
+    while ((1LL << levels) <= Cp / g.bk) ++levels;
+    if (plan->chsum != WINO_SUM_PAIRWISE) levels = 0;
+    bool slots_smem = false;
+    unsigned smem = (unsigned)g.smem_bytes(levels, 4, &slots_smem);
+    // the CTA owns all 512 TMEM columns of its SM: ask for more than half of the shared memory so
+    // that no second CTA of this kernel can become co-resident (and block in tcgen05.alloc)
+    if (smem < 120 * 1024) smem = 120 * 1024;
+    CUresult cr = wino::driver().FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
+    if (cr != CUDA_SUCCESS) return wino::fail(WINO_ECUDA, "conv2d_fused: set smem: " + wino::cu_err(cr));
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long grid = std::min<long long>(groups, sms > 0 ? sms : 148);
+    unsigned long long nz2 = 0x8000000080000000ull;
+    void* M = nullptr;
+    int K = s->K, Ho = L.Ho, Wo = L.Wo, th = L.th, tw = L.tw;
+    const void* Uc = U;
+    const void* Vc = V;
+    void* args[] = {(void*)&Uc, (void*)&Vc, &M, &Kp, &Tp, &Cp, &n_tiles, &nz2, &out, &K, &Ho, &Wo, &th, &tw, &T, &mode};
+    return wino::launch(f, dim3((unsigned)grid, 1, 1), dim3(g.block()), smem, stream, args, "conv2d_fused");
 }
 
 int wino_smallc_supported(wino_plan* plan, const wino_layer_shape* s) {

@@ -113,6 +113,29 @@ class LayerOp:
                                                      D.ptr(out), D.ptr(ws), ws.numel(), s), "conv2d_nhwc")
         return out
 
+    @property
+    def fused_exact_supported(self) -> bool:
+        """alpha^2 <= 16, fp32, FP32-pipe contraction: K3 + K4 can run as one exact kernel."""
+        return bool(_native.lib().wino_fused_supported(self.plan.handle, ctypes.byref(self.shape)))
+
+    def call_fused(self, x, w, mode=0, out=None, stream=None):
+        """K2 + K1, then the contraction and the output transform (+ ReLU / ReLU + 2x2 max-pool
+        for mode 1 / 2) in ONE exact kernel: the alpha^2 accumulators of every (filter, tile)
+        pair are parked in tensor memory, M never goes to HBM (wino_conv2d_fused).  Same bits
+        as __call__ (followed by relu / max-pool)."""
+        lib = _native.lib()
+        need = ctypes.c_size_t(0)
+        _native.check(lib.wino_fused_workspace(self.plan.handle, ctypes.byref(self.shape), ctypes.byref(need)),
+                      "fused_workspace")
+        N, K, Ho, Wo = self.out_shape
+        if out is None:
+            out = D.empty((N, K, Ho // 2, Wo // 2) if mode == 2 else self.out_shape, self.out_dtype)
+        s = D.stream_handle() if stream is None else stream
+        ws = _workspace(need.value, s)
+        _native.check(lib.wino_conv2d_fused(self.plan.handle, ctypes.byref(self.shape), D.ptr(x), D.ptr(w), D.ptr(out),
+                                            mode, D.ptr(ws), ws.numel(), s), "conv2d_fused")
+        return out
+
     # -- individual stages (tests, profiling) --------------------------------
     @property
     def tensor_core(self) -> bool:
