@@ -537,7 +537,8 @@ struct wino_plan {
            << (levels > 0 ? levels : 1) << "\n#define WINO_MAXREG " << gemm.maxreg << "\n#define WINO_KU " << (gemm.ku > 0 ? gemm.ku : gemm.bk) << "\n#define WINO_NOPROD " << gemm.noprod
            << "\n#define WINO_PACK " << (gemm.pack && !dbl ? 1 : 0) << "\n#define WINO_WN " << gemm.wn << "\n#define WINO_SLOTS_SMEM " << slots_smem << "\n"
            << (!wino::tuning("dbuf").empty() ? "#define WINO_DBUF " + wino::tuning("dbuf") + "\n" : std::string())
-           << (fused_out ? "#define WINO_FUSE_P " + std::to_string(n * n) + "\n" + wino::gen_fused_out_source(r, m, AT)
+           << (fused_out ? std::string(wino::tuning("dbuf").empty() ? "#define WINO_DBUF 1\n" : "") + "#define WINO_FUSE_P " +
+                               std::to_string(n * n) + "\n" + wino::gen_fused_out_source(r, m, AT)
                          : std::string())
            << wino::kContractTemplate;
         mod->source = os.str();
@@ -829,10 +830,9 @@ int wino_plan_create(int r, int m, int precision, int channel_sum, int contract_
         // fused exact K3 + K4 (wino_conv2d_fused): 64 x 64 tile, 8 consumer warps x 4x4 microtile,
         // alpha^2 x 16 accumulators per thread parked in tensor memory (contract_template.cuh)
         p->fused_ci = (int)p->cands.size();
-        if (channel_sum == WINO_SUM_PAIRWISE)
-            p->cands.push_back({4, 4, 16, 16, 64, 2, 168, 8, 0, 1});
-        else
-            p->cands.push_back({4, 4, 16, 16, 16, 4, 0, 16, 0, 1});
+        // (the linear sum uses the pairwise kernel's pipeline shape too: 64-channel stages x 2,
+        // 8-step unrolled blocks with the explicit fragment double buffer)
+        p->cands.push_back({4, 4, 16, 16, 64, 2, 168, 8, 0, 1});
     }
     const std::string tag = "r" + std::to_string(r) + "m" + std::to_string(m) + "p" + std::to_string(precision);
     p->layer.name = "wino_layer_" + tag + ".cu";

@@ -356,7 +356,7 @@ def layer_op(ts, cfg, N, C, H, W, K, pad, contraction="exact") -> LayerOp:
 
 
 def conv2d_layer(ts: TransformSet, x, w, cfg: ConvConfig = ConvConfig(), pad: int = 0,
-                 contraction: str = "exact", layout: str = "NCHW"):
+                 contraction: str = "exact", layout: str = "NCHW", fused: bool = False):
     """Winograd F(m x m, r x r) convolution layer (stride 1, zero padding `pad`).
 
     x (N, C, H, W), w (K, C, r, r) -> y (N, K, Ho, Wo): numpy in -> numpy out
@@ -365,7 +365,11 @@ def conv2d_layer(ts: TransformSet, x, w, cfg: ConvConfig = ConvConfig(), pad: in
     layout="NHWC": x (N, H, W, C) -> y (N, Ho, Wo, K) through NHWC-native K1 / K4 kernels
     (wino_conv2d_nhwc; same values as the NCHW path, bit for bit).  Tensor-core
     contraction modes have no NHWC kernels: there the activations are permuted on the
-    device around the NCHW kernels."""
+    device around the NCHW kernels.
+    fused=True (NCHW, fp32, alpha^2 <= 16, FP32-pipe contraction): the contraction and the
+    output transform run as one exact kernel with the accumulators parked in tensor memory
+    (wino_conv2d_fused) -- same bits, no M in HBM; faster than the unfused path on large
+    transform-heavy layers (C <= 128, thousands of 64 x 64 blocks), slower on small ones."""
     if layout not in ("NCHW", "NHWC"):
         raise ValueError("layout must be 'NCHW' or 'NHWC'")
     if layout == "NHWC":
@@ -400,6 +404,10 @@ def conv2d_layer(ts: TransformSet, x, w, cfg: ConvConfig = ConvConfig(), pad: in
     op = layer_op(ts, cfg, N, C, H, W, K, pad, contraction)
     xt, hx = D.to_device(x, op.in_dtype)
     wt, hw = D.to_device(w, op.in_dtype)
+    if fused:
+        if not op.fused_exact_supported:
+            raise ValueError("fused=True needs an fp32 plan, an FP32-pipe contraction and alpha^2 <= 16")
+        return D.finish(op.call_fused(xt, wt), hx or hw)
     return D.finish(op(xt, wt), hx or hw)
 
 
