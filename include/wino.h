@@ -122,7 +122,8 @@ void wino_plan_destroy(wino_plan* plan);
  * transforms) -- for inspection and the SASS gate. */
 int wino_plan_source(const wino_plan* plan, int which, char* buf, size_t cap, size_t* len);
 /* cubin of a generated module (0 = layer transforms, 1 = tile transforms,
- * 2 = contraction kernel for a C-channel layer); CPU-only OK. */
+ * 2 = contraction kernel for a C-channel layer, 3 = the fused exact contraction +
+ * output-transform kernel of wino_conv2d_fused, alpha^2 <= 16 only); CPU-only OK. */
 int wino_plan_cubin(wino_plan* plan, int which, int channels, void* buf, size_t cap, size_t* len);
 
 /* Compile, concurrently on host threads, the generated kernels a layer shape

@@ -108,6 +108,22 @@ def test_sass_gate_exact_kernels_have_no_fma(built, prec, cs, pack, gemm_tuning)
         assert "FFMA2" not in contract
 
 
+@pytest.mark.parametrize("cs", ["linear", "pairwise"])
+def test_sass_gate_fused_exact_kernel(built, cs):
+    """The fused exact K3 + K4 kernel (wino_conv2d_fused): separately rounded products and sums
+    like the unfused contraction, accumulators parked in tensor memory (STTM / LDTM), operands
+    through bulk copies, and no M store (its only global stores are the outputs)."""
+    plan = _plan(3, 2, "0,1,-1,inf", "fp32", cs)
+    sass = _sass(plan.cubin(3, 128))
+    assert not _fused_ops(sass)
+    assert "FFMA2" in sass and "FADD2" in sass and "UBLKCP" in sass
+    assert re.search(r"\bSTTM\b", sass) and re.search(r"\bLDTM\b", sass)   # tcgen05.st / tcgen05.ld
+    assert "STG.E.128" not in sass                                          # (the unfused kernel's M stores)
+    big = _plan(3, 4, "0,1,-1,1/2,-1/2,inf", "fp32", cs)                    # alpha = 6: no fused kernel
+    with pytest.raises(RuntimeError):
+        big.cubin(3, 128)
+
+
 def test_sass_gate_rejects_fused_sums():
     assert _fused_ops("FFMA R1, R2, R3, R4 ;")
     assert _fused_ops("FFMA2 R16, R25.F32, R32.F32x2.HI_LO, R8.F32x2.HI_LO ;")
