@@ -895,6 +895,174 @@ static void emit_smallc(std::ostringstream& os, int r, int m, const MatProg& AT,
     os << "\n";
 }
 
+// K3 + K4 (+ ReLU, + 2x2 max-pool) in one kernel for C <= 4 (an RGB first layer: VGG-16
+// layer 1 moves 6 GB of M out to HBM and back in for 3 products per point).  Second design
+// (the first, emit_smallc, spilled and was shared-memory bound):
+//   * a CTA owns the bn tiles of one V block and all filters: U as sU[p][k/2][c][k%2] and the
+//     block's V rows as sV[p][c][tile] are staged once with coalesced loads;
+//   * a warp is 32 consecutive tiles (conflict-free V loads, the store pattern of the
+//     gather K4) times one filter PAIR, so each V value loaded feeds two filters and the
+//     filter operands are two broadcast loads per point: 2.5 shared-memory wavefronts per
+//     (point, filter) against ~18 FP32-pipe cycles;
+//   * channel sums are produced one column of the alpha x alpha point grid at a time and
+//     consumed at once by the left pass of (A^T M) A, so the live set is the 2 x m x alpha
+//     left-pass results, not 2 x alpha^2 sums;
+//   * the channel sum is the contraction kernel's value bit for bit: the plan's linear order
+//     ((-0 + z0) + z1 ... == (z0 + z1) ...), or the halving tree of the padded 8-channel stage
+//     with its -0 leaves pruned (x + -0 == x exactly).
+// KG warps-of-pairs per tile warp (tuning key "sc2_kg", default 3): threads = bn * KG.
+inline int smallc2_kg() {
+    static const int v = std::atoi(tuning("sc2_kg").c_str());
+    return v >= 1 && v <= 8 ? v : 3;
+}
+
+static void emit_smallc2(std::ostringstream& os, int r, int m, const MatProg& AT, int bn, int& ctr) {
+    const int n = r + m - 1, P = n * n, KG = smallc2_kg();
+    if (bn % 32 || bn * KG > 1024) return;
+    os << "template <int C, int PW>\n"
+          "static __device__ __forceinline__ float sc2_dot(float u0, float u1, float u2, float u3, float v0, float v1,\n"
+          "                                                float v2, float v3) {\n"
+          "  const float z0 = __fmul_rn(u0, v0);\n"
+          "  if constexpr (C == 1) return z0;\n"
+          "  const float z1 = __fmul_rn(u1, v1);\n"
+          "  if constexpr (C == 2) return __fadd_rn(z0, z1);\n"
+          "  const float z2 = __fmul_rn(u2, v2);\n"
+          "  if constexpr (C == 3) return __fadd_rn(__fadd_rn(z0, z1), z2);\n"
+          "  const float z3 = __fmul_rn(u3, v3);\n"
+          "  if constexpr (PW) return __fadd_rn(__fadd_rn(z0, z1), __fadd_rn(z2, z3));\n"
+          "  return __fadd_rn(__fadd_rn(__fadd_rn(z0, z1), z2), z3);\n"
+          "}\n";
+    // store of one (tile, filter) result, y[a][b] in registers
+    os << "static __device__ __forceinline__ void sc2_store(float* __restrict__ out, int mode, long long plane, int Ho,\n"
+          "    int Wo, int y0, int x0";
+    for (int a = 0; a < m; ++a)
+        for (int b = 0; b < m; ++b) os << ", float y" << a << "_" << b;
+    os << ") {\n"
+          "  if (mode < 2) {\n"
+          "    float* dst = out + (plane * Ho + y0) * Wo + x0;\n";
+    auto val = [&](int a, int b) { return "y" + std::to_string(a) + "_" + std::to_string(b); };
+    if (m % 2 == 0) {
+        os << "    if ((Wo & 1) == 0 && (reinterpret_cast<size_t>(out) & 7) == 0) {\n";
+        for (int a = 0; a < m; ++a) {
+            os << "      if (y0 + " << a << " < Ho) {\n";
+            for (int b = 0; b < m; b += 2)
+                os << "        if (x0 + " << b << " < Wo) *reinterpret_cast<float2*>(dst + " << a << " * Wo + " << b
+                   << ") = mode ? make_float2(wino_relu(" << val(a, b) << "), wino_relu(" << val(a, b + 1)
+                   << ")) : make_float2(" << val(a, b) << ", " << val(a, b + 1) << ");\n";
+            os << "      }\n";
+        }
+        os << "      return;\n    }\n";
+    }
+    for (int a = 0; a < m; ++a) {
+        os << "    if (y0 + " << a << " < Ho) {\n";
+        for (int b = 0; b < m; ++b)
+            os << "      if (x0 + " << b << " < Wo) dst[" << a << " * Wo + " << b << "] = mode ? wino_relu(" << val(a, b)
+               << ") : " << val(a, b) << ";\n";
+        os << "    }\n";
+    }
+    os << "    return;\n  }\n";
+    if (m % 2 == 0) {
+        os << "  const int Hp = Ho >> 1, Wp = Wo >> 1, py0 = y0 >> 1, px0 = x0 >> 1;\n"
+              "  float* dst = out + (plane * Hp + py0) * Wp + px0;\n";
+        for (int a = 0; a < m / 2; ++a) {
+            os << "  if (py0 + " << a << " < Hp) {\n";
+            for (int b = 0; b < m / 2; ++b)
+                os << "    if (px0 + " << b << " < Wp) dst[" << a << " * Wp + " << b << "] = wino_relu(fmaxf(fmaxf("
+                   << val(2 * a, 2 * b) << ", " << val(2 * a, 2 * b + 1) << "), fmaxf(" << val(2 * a + 1, 2 * b) << ", "
+                   << val(2 * a + 1, 2 * b + 1) << ")));\n";
+            os << "  }\n";
+        }
+    }
+    os << "}\n";
+    os << "template <int C, int PW>\n"
+          "static __device__ __forceinline__ void sc2_body(const float* __restrict__ U, const float* __restrict__ V,\n"
+          "    float* __restrict__ out, int K, int Ho, int Wo, int th, int tw, long long T, long long Tp, long long Kp,\n"
+          "    long long Cp, int bm, int mode) {\n"
+       << "  constexpr int P = " << P << ", BN = " << bn << ", NT = " << bn * KG << ", KG = " << KG << ";\n"
+          "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
+          "  float* sU = reinterpret_cast<float*>(smem_raw);   // [P][Kp / 2][4 channels][2 filters]\n"
+          "  float* sV = sU + (long long)P * Kp * 4;           // [P][C][BN]\n"
+          "  const long long plu = Cp * Kp, plv = Cp * Tp;\n"
+          "  const int kp2 = (int)(Kp >> 1);\n"
+          "  for (int i = threadIdx.x; i < P * 4 * (int)Kp; i += NT) {\n"
+          "    const int k = i % (int)Kp, pc = i / (int)Kp, c = pc & 3, p = pc >> 2;\n"
+          "    const float u = c < C ? __ldg(U + p * plu + (long long)(k / bm) * Cp * bm + (long long)c * bm + (k % bm)) : 0.f;\n"
+          "    sU[((long long)(p * kp2 + (k >> 1)) * 4 + c) * 2 + (k & 1)] = u;\n"
+          "  }\n"
+          "  {\n"
+          "    const float* vb = V + (long long)blockIdx.x * Cp * BN;\n"
+          "    for (int i = threadIdx.x; i < P * C * (BN / 4); i += NT) {\n"
+          "      const int q = i % (BN / 4), pc = i / (BN / 4), c = pc % C, p = pc / C;\n"
+          "      reinterpret_cast<float4*>(sV + pc * BN)[q] =\n"
+          "          __ldg(reinterpret_cast<const float4*>(vb + p * plv + (long long)c * BN) + q);\n"
+          "    }\n"
+          "  }\n"
+          "  __syncthreads();\n"
+          "  const int tl = threadIdx.x % BN, kg = threadIdx.x / BN;\n"
+          "  const long long t = (long long)blockIdx.x * BN + tl;\n"
+          "  if (t >= T) return;\n"
+          "  const int per = th * tw;\n"
+          "  const int img = (int)(t / per), rem = (int)(t - (long long)img * per);\n"
+          "  const int ti = rem / tw, tj = rem - ti * tw;\n"
+       << "  const int y0 = ti * " << m << ", x0 = tj * " << m << ";\n"
+          "  const float* vp = sV + tl;\n"
+          "  const int us = kp2 * 8;  // floats between the points of one filter pair\n"
+          "#pragma unroll 1\n"
+          "  for (int kp = kg; 2 * kp < K; kp += KG) {\n"
+          "    const float* up = sU + kp * 8;\n";
+    Emitter em(os, false, ctr);
+    std::vector<std::vector<std::string>> leftA(AT.rows, std::vector<std::string>(n)), leftB = leftA;
+    for (int b = 0; b < n; ++b) {
+        std::vector<std::string> colA(n), colB(n);
+        for (int a = 0; a < n; ++a) {
+            const int p = a * n + b;
+            const std::string s = std::to_string(a) + "_" + std::to_string(b);
+            colA[a] = "ma" + s;
+            colB[a] = "mb" + s;
+            os << "    const float4 ua" << s << " = *reinterpret_cast<const float4*>(up + " << p << " * us);\n"
+               << "    float4 ub" << s << " = make_float4(0.f, 0.f, 0.f, 0.f);\n"
+               << "    if constexpr (C > 2) ub" << s << " = *reinterpret_cast<const float4*>(up + " << p << " * us + 4);\n"
+               << "    const float va" << s << " = vp[" << p << " * C * BN];\n"
+               << "    const float vb" << s << " = C > 1 ? vp[(" << p << " * C + 1) * BN] : 0.f;\n"
+               << "    const float vc" << s << " = C > 2 ? vp[(" << p << " * C + 2) * BN] : 0.f;\n"
+               << "    const float vd" << s << " = C > 3 ? vp[(" << p << " * C + 3) * BN] : 0.f;\n"
+               << "    const float " << colA[a] << " = sc2_dot<C, PW>(ua" << s << ".x, ua" << s << ".z, ub" << s << ".x, ub"
+               << s << ".z, va" << s << ", vb" << s << ", vc" << s << ", vd" << s << ");\n"
+               << "    const float " << colB[a] << " = sc2_dot<C, PW>(ua" << s << ".y, ua" << s << ".w, ub" << s << ".y, ub"
+               << s << ".w, va" << s << ", vb" << s << ", vc" << s << ", vd" << s << ");\n";
+            // keep the shared-memory loads of later points behind the sums of these (ptxas would hoist
+            // all 64 points' operands and spill)
+            if ((a + 1) % 4 == 0) os << "    asm volatile(\"\" ::: \"memory\");\n";
+        }
+        auto ra = em.apply(AT, colA);
+        auto rb = em.apply(AT, colB);
+        for (int i = 0; i < AT.rows; ++i) {
+            leftA[i][b] = ra[i];
+            leftB[i][b] = rb[i];
+        }
+    }
+    for (int half = 0; half < 2; ++half) {
+        auto& left = half ? leftB : leftA;
+        std::vector<std::vector<std::string>> yv(AT.rows);
+        for (int i = 0; i < AT.rows; ++i) yv[i] = em.apply(AT, left[i]);
+        os << "    " << (half ? "if (2 * kp + 1 < K) " : "") << "sc2_store(out, mode, (long long)img * K + 2 * kp + " << half
+           << ", Ho, Wo, y0, x0";
+        for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; ++b) os << ", " << yv[a][b];
+        os << ");\n";
+    }
+    os << "  }\n}\n";
+    for (int C = 1; C <= 4; ++C)
+        for (int pw = 0; pw < 2; ++pw)
+            os << "extern \"C\" __global__ void __launch_bounds__(" << bn * KG << ", 1) wino_smallc2_c" << C
+               << (pw ? "p" : "l")
+               << "(\n    const float* __restrict__ U, const float* __restrict__ V, float* __restrict__ out, int K,\n"
+                  "    int Ho, int Wo, int th, int tw, long long T, long long Tp, long long Kp, long long Cp, int bm,\n"
+                  "    int mode) {\n"
+               << "  sc2_body<" << C << ", " << pw << ">(U, V, out, K, Ho, Wo, th, tw, T, Tp, Kp, Cp, bm, mode);\n}\n";
+    os << "\n";
+}
+
 std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
                              const GenTypes& ty, int bm, int bn) {
     const int n = r + m - 1, P = n * n;
@@ -1042,7 +1210,10 @@ std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, 
         emit_output_gather(os, r, m, AT, ty, 128, ctr);
         if (!ty.y_double) emit_output_gather_act(os, r, m, AT, ty, 128, ctr);
         emit_nhwc(os, r, m, BT, AT, ty, bn, ctr);
-        if (!ty.compute_double && !ty.uv_double && !ty.y_double) emit_smallc(os, r, m, AT, ty, ctr);
+        if (!ty.compute_double && !ty.uv_double && !ty.y_double) {
+            emit_smallc(os, r, m, AT, ty, ctr);
+            emit_smallc2(os, r, m, AT, bn, ctr);
+        }
     }
     return os.str();
 }

@@ -722,7 +722,7 @@ const char* wino_last_error(void) { return wino::g_last_error.c_str(); }
 
 int wino_tuning_set(const char* key, const char* value) {
     static const char* const keys[] = {"gemm", "dbuf", "k1", "k1order", "k4", "k1tc", "tile_interp",
-                                       "cpt", "kpt", "tcf_nk", "tcf_dbg", "tc_epi", "k1rowwise", "k4rowwise"};
+                                       "cpt", "kpt", "tcf_nk", "tcf_dbg", "tc_epi", "k1rowwise", "k4rowwise", "sc2_kg"};
     if (!key) return wino::fail(WINO_EINVAL, "tuning_set: null key");
     bool known = false;
     for (const char* k : keys) known = known || std::strcmp(k, key) == 0;
@@ -882,6 +882,23 @@ int wino_plan_cubin(wino_plan* plan, int which, int channels, void* buf, size_t 
     return WINO_OK;
 }
 
+// codegen.cpp emit_smallc2 (C <= 4): CTA = the bn tiles of one V block x all filters, threads = bn * KG
+static int smallc2_kg() {
+    const int v = std::atoi(wino::tuning("sc2_kg").c_str());
+    return v >= 1 && v <= 8 ? v : 3;
+}
+static size_t smallc2_smem(const wino_layer_layout& L, int C) {
+    return ((size_t)L.P * L.Kp * 4 + (size_t)L.P * C * L.bn) * 4;  // sU[P][Kp/2][4][2] + sV[P][C][bn]
+}
+static bool smallc2_ok(const wino_layer_layout& L, int C) {
+    return C <= 4 && L.bn % 32 == 0 && L.bn * smallc2_kg() <= 1024 && L.Kp % 2 == 0 && smallc2_smem(L, C) <= 232448;
+}
+
+static bool smallc_v2(wino_plan* plan, const wino_layer_shape* s) {
+    wino_layer_layout L;
+    return !layout_of(plan, s, &L) && smallc2_ok(L, s->C);
+}
+
 int wino_plan_prepare(wino_plan* plan, const wino_layer_shape* s, int flags) {
     wino_layer_layout L;
     int rc = layout_of(plan, s, &L);
@@ -903,7 +920,8 @@ int wino_plan_prepare(wino_plan* plan, const wino_layer_shape* s, int flags) {
     }
     if ((flags & WINO_PREPARE_ACT) && !plan->ty.y_double) work.push_back({lm, "wino_output_gather_act"});
     if ((flags & (WINO_PREPARE_ACT | WINO_PREPARE_CONV)) && wino_smallc_supported(plan, s))
-        work.push_back({lm, "wino_smallc_c" + std::to_string(s->C) + (plan->chsum == WINO_SUM_PAIRWISE ? "p" : "l")});
+        work.push_back({lm, std::string(smallc_v2(plan, s) ? "wino_smallc2_c" : "wino_smallc_c") + std::to_string(s->C) +
+                                (plan->chsum == WINO_SUM_PAIRWISE ? "p" : "l")});
     if (flags & WINO_PREPARE_NHWC) {
         work.push_back({lm, "wino_filter_xform"});
         work.push_back({lm, "wino_input_gather_nhwc"});
@@ -1293,6 +1311,7 @@ int wino_smallc_supported(wino_plan* plan, const wino_layer_shape* s) {
     wino_layer_layout L;
     if (!plan || !s || layout_of(plan, s, &L)) return 0;
     if (plan->mode != WINO_CONTRACT_EXACT || plan->precision != WINO_FP32 || s->C > 8) return 0;
+    if (smallc2_ok(L, s->C)) return 1;
     const long long cw = s->C <= 4 ? 4 : 8;
     const long long tt = s->C <= 4 ? 96 : 32;  // codegen.cpp emit_smallc: SC_TT
     return (L.P * cw + 4) * (L.Kp + tt) * 4 <= 232448 ? 1 : 0;
@@ -1310,14 +1329,28 @@ int wino_contract_output_smallc(wino_plan* plan, const wino_layer_shape* s, cons
     if (((uintptr_t)U | (uintptr_t)V) & 15) return wino::fail(WINO_EINVAL, "contract_output_smallc: U, V must be 16-byte aligned");
     if ((rc = u_layout_check(U, L, "contract_output_smallc"))) return rc;
     if (s->N == 0) return WINO_OK;
-    const std::string kname = "wino_smallc_c" + std::to_string(s->C) + (plan->chsum == WINO_SUM_PAIRWISE ? "p" : "l");
+    const bool v2 = smallc2_ok(L, s->C);
+    const std::string kname = std::string(v2 ? "wino_smallc2_c" : "wino_smallc_c") + std::to_string(s->C) +
+                              (plan->chsum == WINO_SUM_PAIRWISE ? "p" : "l");
     CUfunction f;
     if ((rc = plan->layer_mod(plan->pick(s))->function(kname.c_str(), &f))) return rc;
+    int K = s->K, Ho = L.Ho, Wo = L.Wo, th = L.th, tw = L.tw, bm = L.bm, bn = L.bn;
+    long long T = L.T, Tp = L.Tp, Kp = L.Kp, Cp = L.Cp;
+    if (v2) {
+        const unsigned smem = (unsigned)smallc2_smem(L, s->C);
+        const long long nb = (T + bn - 1) / bn;
+        if (nb > (1LL << 30)) return wino::fail(WINO_EUNSUPPORTED, "contract_output_smallc: too many tiles");
+        if (smem > 48 * 1024) {
+            CUresult cr = wino::driver().FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
+            if (cr != CUDA_SUCCESS) return wino::fail(WINO_ECUDA, "contract_output_smallc: set smem: " + wino::cu_err(cr));
+        }
+        void* args[] = {(void*)&U, (void*)&V, &out, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp, &Cp, &bm, &mode};
+        return wino::launch(f, dim3((unsigned)nb), dim3((unsigned)(bn * smallc2_kg())), smem, stream, args,
+                            "contract_output_smallc");
+    }
     const long long cw = s->C <= 4 ? 4 : 8;
     const long long tt = s->C <= 4 ? 96 : 32;  // tiles per block (SC_TT); threads = 4 * tt
     const unsigned smem = (unsigned)((L.P * cw + 4) * (L.Kp + tt) * 4);  // codegen.cpp emit_smallc: [Kp + TT][P*CW + 4]
-    int K = s->K, Ho = L.Ho, Wo = L.Wo, th = L.th, tw = L.tw, bm = L.bm, bn = L.bn;
-    long long T = L.T, Tp = L.Tp, Kp = L.Kp, Cp = L.Cp;
     float rtw = 1.0f / tw, rth = 1.0f / th;
     const long long nb = (T + tt - 1) / tt;
     if (nb > (1LL << 30)) return wino::fail(WINO_EUNSUPPORTED, "contract_output_smallc: too many tiles");
