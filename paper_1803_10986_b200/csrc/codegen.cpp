@@ -910,15 +910,17 @@ static void emit_smallc(std::ostringstream& os, int r, int m, const MatProg& AT,
 //   * the channel sum is the contraction kernel's value bit for bit: the plan's linear order
 //     ((-0 + z0) + z1 ... == (z0 + z1) ...), or the halving tree of the padded 8-channel stage
 //     with its -0 leaves pruned (x + -0 == x exactly).
-// KG warps-of-pairs per tile warp (tuning key "sc2_kg", default 3): threads = bn * KG.
+// KG warps-of-pairs per tile warp (tuning key "sc2_kg", default 2: 256 threads, no spills at
+// 236 registers; 3 spills at the 168-register cap): threads = bn * KG.
 inline int smallc2_kg() {
     static const int v = std::atoi(tuning("sc2_kg").c_str());
-    return v >= 1 && v <= 8 ? v : 3;
+    return v >= 1 && v <= 8 ? v : 2;
 }
 
-static void emit_smallc2(std::ostringstream& os, int r, int m, const MatProg& AT, int bn, int& ctr) {
+static void emit_smallc2(std::ostringstream& os, int r, int m, const MatProg& AT, int bm, int bn, int& ctr) {
     const int n = r + m - 1, P = n * n, KG = smallc2_kg();
-    if (bn % 32 || bn * KG > 1024) return;
+    if (bn % 32 || bm % 4 || bn * KG > 1024) return;
+    const bool even = m % 2 == 0;
     os << "template <int C, int PW>\n"
           "static __device__ __forceinline__ float sc2_dot(float u0, float u1, float u2, float u3, float v0, float v1,\n"
           "                                                float v2, float v3) {\n"
@@ -932,107 +934,169 @@ static void emit_smallc2(std::ostringstream& os, int r, int m, const MatProg& AT
           "  if constexpr (PW) return __fadd_rn(__fadd_rn(z0, z1), __fadd_rn(z2, z3));\n"
           "  return __fadd_rn(__fadd_rn(__fadd_rn(z0, z1), z2), z3);\n"
           "}\n";
-    // store of one (tile, filter) result, y[a][b] in registers
-    os << "static __device__ __forceinline__ void sc2_store(float* __restrict__ out, int mode, long long plane, int Ho,\n"
-          "    int Wo, int y0, int x0";
+    auto val = [&](int a, int b) { return "y" + std::to_string(a) + "_" + std::to_string(b); };
+    // Store of one (tile, filter) result y[a][b] (registers).  MODE 0: y, 1: ReLU, 2: ReLU of the 2x2
+    // max-pool.  MODE 0 / 1 with an even m and an even, 8-byte aligned output row (`coop`): the warp's
+    // 32 tiles are consecutive, so one output row of the warp is (mostly) one contiguous run of
+    // 32 x m floats; each lane parks its m x m values in the warp's shared-memory buffer and the
+    // warp writes every row as m/2 fully coalesced 8-byte stores (lane l writes pair j*32 + l, whose
+    // address and clipping -- soff / sy0 -- were computed once per thread).  Direct stores (8 bytes per
+    // lane, 4 m bytes apart) touch every sector of the run m/2 times, and that request rate, not the
+    // arithmetic, bounded the first version of this kernel.
+    os << "template <int MODE>\n"
+          "static __device__ __forceinline__ void sc2_store(float* __restrict__ out, bool coop, bool live, float2* wbuf,\n"
+          "    int lane, const long long* soff, const int* sy0, int img, int K, int k, int Ho, int Wo, int y0, int x0";
     for (int a = 0; a < m; ++a)
         for (int b = 0; b < m; ++b) os << ", float y" << a << "_" << b;
     os << ") {\n"
-          "  if (mode < 2) {\n"
-          "    float* dst = out + (plane * Ho + y0) * Wo + x0;\n";
-    auto val = [&](int a, int b) { return "y" + std::to_string(a) + "_" + std::to_string(b); };
-    if (m % 2 == 0) {
-        os << "    if ((Wo & 1) == 0 && (reinterpret_cast<size_t>(out) & 7) == 0) {\n";
-        for (int a = 0; a < m; ++a) {
-            os << "      if (y0 + " << a << " < Ho) {\n";
-            for (int b = 0; b < m; b += 2)
-                os << "        if (x0 + " << b << " < Wo) *reinterpret_cast<float2*>(dst + " << a << " * Wo + " << b
-                   << ") = mode ? make_float2(wino_relu(" << val(a, b) << "), wino_relu(" << val(a, b + 1)
-                   << ")) : make_float2(" << val(a, b) << ", " << val(a, b + 1) << ");\n";
-            os << "      }\n";
-        }
+          "  if constexpr (MODE < 2) {\n";
+    if (even) {
+        os << "    if (coop) {\n"
+              "      float* ok = out + (long long)k * Ho * Wo;  // soff carries the image and the tile origin\n"
+              "      __syncwarp();\n";
+        for (int a = 0; a < m; ++a)
+            for (int q = 0; q < m / 2; ++q)
+                os << "      wbuf[(" << a << " * 32 + lane) * " << m / 2 << " + " << q << "] = MODE ? make_float2(wino_relu("
+                   << val(a, 2 * q) << "), wino_relu(" << val(a, 2 * q + 1) << ")) : make_float2(" << val(a, 2 * q) << ", "
+                   << val(a, 2 * q + 1) << ");\n";
+        os << "      __syncwarp();\n";
+        for (int a = 0; a < m; ++a)
+            for (int j = 0; j < m / 2; ++j)
+                os << "      if (sy0[" << j << "] + " << a << " < Ho) *reinterpret_cast<float2*>(ok + soff[" << j << "] + "
+                   << a << " * Wo) = wbuf[" << (a * (m / 2) + j) << " * 32 + lane];\n";
         os << "      return;\n    }\n";
     }
+    os << "    if (!live) return;\n"
+          "    float* dst = out + ((((long long)img * K + k) * Ho + y0) * Wo + x0);\n";
     for (int a = 0; a < m; ++a) {
         os << "    if (y0 + " << a << " < Ho) {\n";
         for (int b = 0; b < m; ++b)
-            os << "      if (x0 + " << b << " < Wo) dst[" << a << " * Wo + " << b << "] = mode ? wino_relu(" << val(a, b)
+            os << "      if (x0 + " << b << " < Wo) dst[" << a << " * Wo + " << b << "] = MODE ? wino_relu(" << val(a, b)
                << ") : " << val(a, b) << ";\n";
         os << "    }\n";
     }
-    os << "    return;\n  }\n";
-    if (m % 2 == 0) {
-        os << "  const int Hp = Ho >> 1, Wp = Wo >> 1, py0 = y0 >> 1, px0 = x0 >> 1;\n"
-              "  float* dst = out + (plane * Hp + py0) * Wp + px0;\n";
+    os << "  } else {\n";
+    if (even) {
+        os << "    if (!live) return;\n"
+              "    const int Hp = Ho >> 1, Wp = Wo >> 1, py0 = y0 >> 1, px0 = x0 >> 1;\n"
+              "    float* dst = out + ((((long long)img * K + k) * Hp + py0) * Wp + px0);\n";
         for (int a = 0; a < m / 2; ++a) {
-            os << "  if (py0 + " << a << " < Hp) {\n";
+            os << "    if (py0 + " << a << " < Hp) {\n";
             for (int b = 0; b < m / 2; ++b)
-                os << "    if (px0 + " << b << " < Wp) dst[" << a << " * Wp + " << b << "] = wino_relu(fmaxf(fmaxf("
+                os << "      if (px0 + " << b << " < Wp) dst[" << a << " * Wp + " << b << "] = wino_relu(fmaxf(fmaxf("
                    << val(2 * a, 2 * b) << ", " << val(2 * a, 2 * b + 1) << "), fmaxf(" << val(2 * a + 1, 2 * b) << ", "
                    << val(2 * a + 1, 2 * b + 1) << ")));\n";
-            os << "  }\n";
+            os << "    }\n";
         }
     }
-    os << "}\n";
-    os << "template <int C, int PW>\n"
+    os << "  }\n}\n";
+    os << "static __device__ __forceinline__ unsigned sc2_s32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }\n"
+          "static __device__ __forceinline__ void sc2_wait(unsigned long long* bar) {\n"
+          "  asm volatile(\"{\\n\\t.reg .pred P1;\\nSC2_WAIT_%=:\\n\\t\"\n"
+          "               \"mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\\n\\t\"\n"
+          "               \"@!P1 bra SC2_WAIT_%=;\\n}\\n\" ::\"r\"(sc2_s32(bar)), \"r\"(0u) : \"memory\");\n"
+          "}\n"
+          "static __device__ __forceinline__ void sc2_bulk(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {\n"
+          "  asm volatile(\"cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\"\n"
+          "               ::\"r\"(sc2_s32(dst)), \"l\"(src), \"r\"(bytes), \"r\"(sc2_s32(bar)) : \"memory\");\n"
+          "}\n";
+    os << "template <int C, int PW, int MODE>\n"
           "static __device__ __forceinline__ void sc2_body(const float* __restrict__ U, const float* __restrict__ V,\n"
           "    float* __restrict__ out, int K, int Ho, int Wo, int th, int tw, long long T, long long Tp, long long Kp,\n"
-          "    long long Cp, int bm, int mode) {\n"
-       << "  constexpr int P = " << P << ", BN = " << bn << ", NT = " << bn * KG << ", KG = " << KG << ";\n"
+          "    long long Cp) {\n"
+       << "  constexpr int N1 = " << n << ", P = " << P << ", M = " << m << ", BM = " << bm << ", BN = " << bn
+       << ", KG = " << KG << ", HP = " << (even ? m / 2 : 1) << ";\n"
           "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
-          "  float* sU = reinterpret_cast<float*>(smem_raw);   // [P][Kp / 2][4 channels][2 filters]\n"
-          "  float* sV = sU + (long long)P * Kp * 4;           // [P][C][BN]\n"
+          "  __shared__ __align__(8) unsigned long long bar[N1];  // one per column of the point grid\n"
+          "  const int KB = (int)(Kp / BM);\n"
+          "  float* sU = reinterpret_cast<float*>(smem_raw);   // [P][KB][C][BM]: the first C rows of U's blocks\n"
+          "  float* sV = sU + (long long)P * KB * C * BM;      // [P][C][BN]:     the first C rows of this V block\n"
           "  const long long plu = Cp * Kp, plv = Cp * Tp;\n"
-          "  const int kp2 = (int)(Kp >> 1);\n"
-          "  for (int i = threadIdx.x; i < P * 4 * (int)Kp; i += NT) {\n"
-          "    const int k = i % (int)Kp, pc = i / (int)Kp, c = pc & 3, p = pc >> 2;\n"
-          "    const float u = c < C ? __ldg(U + p * plu + (long long)(k / bm) * Cp * bm + (long long)c * bm + (k % bm)) : 0.f;\n"
-          "    sU[((long long)(p * kp2 + (k >> 1)) * 4 + c) * 2 + (k & 1)] = u;\n"
-          "  }\n"
-          "  {\n"
-          "    const float* vb = V + (long long)blockIdx.x * Cp * BN;\n"
-          "    for (int i = threadIdx.x; i < P * C * (BN / 4); i += NT) {\n"
-          "      const int q = i % (BN / 4), pc = i / (BN / 4), c = pc % C, p = pc / C;\n"
-          "      reinterpret_cast<float4*>(sV + pc * BN)[q] =\n"
-          "          __ldg(reinterpret_cast<const float4*>(vb + p * plv + (long long)c * BN) + q);\n"
-          "    }\n"
+          "  // Staging: one bulk copy per (point, U block) and per point of V, completing on the barrier of\n"
+          "  // the point's column, so the first column's sums start while the rest streams in.\n"
+          "  if (threadIdx.x == 0) {\n"
+          "    for (int b = 0; b < N1; ++b)\n"
+          "      asm volatile(\"mbarrier.init.shared::cta.b64 [%0], %1;\" ::\"r\"(sc2_s32(&bar[b])), \"r\"(1u) : \"memory\");\n"
+          "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n"
           "  }\n"
           "  __syncthreads();\n"
-          "  const int tl = threadIdx.x % BN, kg = threadIdx.x / BN;\n"
+          "  if (threadIdx.x < 32) {\n"
+          "    const float* vb = V + (long long)blockIdx.x * Cp * BN;\n"
+          "    for (int b = 0; b < N1; ++b) {\n"
+          "      if (threadIdx.x == 0)\n"
+          "        asm volatile(\"mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\" ::\"r\"(sc2_s32(&bar[b])),\n"
+          "                     \"r\"((unsigned)(N1 * (KB * C * BM + C * BN) * 4)) : \"memory\");\n"
+          "      __syncwarp();\n"
+          "      for (int j = threadIdx.x; j < N1 * (KB + 1); j += 32) {\n"
+          "        const int a = j / (KB + 1), kb = j - a * (KB + 1), p = a * N1 + b;\n"
+          "        if (kb < KB)\n"
+          "          sc2_bulk(sU + ((long long)p * KB + kb) * C * BM, U + p * plu + (long long)kb * Cp * BM, C * BM * 4, &bar[b]);\n"
+          "        else\n"
+          "          sc2_bulk(sV + p * C * BN, vb + p * plv, C * BN * 4, &bar[b]);\n"
+          "      }\n"
+          "    }\n"
+          "  }\n"
+          "  const int tl = threadIdx.x % BN, kg = threadIdx.x / BN, lane = threadIdx.x & 31;\n"
           "  const long long t = (long long)blockIdx.x * BN + tl;\n"
-          "  if (t >= T) return;\n"
+          "  const bool live = t < T;\n"
           "  const int per = th * tw;\n"
-          "  const int img = (int)(t / per), rem = (int)(t - (long long)img * per);\n"
-          "  const int ti = rem / tw, tj = rem - ti * tw;\n"
-       << "  const int y0 = ti * " << m << ", x0 = tj * " << m << ";\n"
+          "  int y0 = 0, x0 = 0, img = 0;\n"
+          "  if (live) {\n"
+          "    img = (int)(t / per);\n"
+          "    const int rem = (int)(t - (long long)img * per), ti = rem / tw;\n"
+          "    y0 = ti * M;\n"
+          "    x0 = (rem - ti * tw) * M;\n"
+          "  }\n"
+          "  // warp-cooperative row stores (sc2_store): pair j * 32 + lane of a warp row belongs to lane ls\n"
+          "  const bool coop = MODE < 2 && " << (even ? "true" : "false")
+       << " && (Wo & 1) == 0 && (reinterpret_cast<size_t>(out) & 7) == 0;\n"
+          "  float2* wbuf = reinterpret_cast<float2*>(sV + P * C * BN) + (threadIdx.x >> 5) * (M * 32 * HP);\n"
+          "  long long soff[HP];\n"
+          "  int sy0[HP];\n"
+          "#pragma unroll\n"
+          "  for (int j = 0; j < HP; ++j) {\n"
+          "    const int i = j * 32 + lane, ls = i / HP, q = i - ls * HP;\n"
+          "    const long long tt = t - lane + ls;\n"
+          "    soff[j] = 0;\n"
+          "    sy0[j] = Ho;\n"
+          "    if (coop && tt < T) {\n"
+          "      const int im = (int)(tt / per), rem = (int)(tt - (long long)im * per), ti = rem / tw;\n"
+          "      const int xx = (rem - ti * tw) * M + 2 * q;\n"
+          "      soff[j] = ((long long)im * K * Ho + ti * M) * Wo + xx;\n"
+          "      if (xx < Wo) sy0[j] = ti * M;\n"
+          "    }\n"
+          "  }\n"
           "  const float* vp = sV + tl;\n"
-          "  const int us = kp2 * 8;  // floats between the points of one filter pair\n"
+          "  const int us = KB * C * BM;  // floats between the points of one filter\n"
+          "  bool first = true;\n"
           "#pragma unroll 1\n"
           "  for (int kp = kg; 2 * kp < K; kp += KG) {\n"
-          "    const float* up = sU + kp * 8;\n";
+          "    const float* up = sU + ((2 * kp) / BM) * C * BM + ((2 * kp) % BM);\n";
     Emitter em(os, false, ctr);
     std::vector<std::vector<std::string>> leftA(AT.rows, std::vector<std::string>(n)), leftB = leftA;
     for (int b = 0; b < n; ++b) {
         std::vector<std::string> colA(n), colB(n);
+        os << "    if (first) sc2_wait(&bar[" << b << "]);\n";
         for (int a = 0; a < n; ++a) {
             const int p = a * n + b;
             const std::string s = std::to_string(a) + "_" + std::to_string(b);
             colA[a] = "ma" + s;
             colB[a] = "mb" + s;
-            os << "    const float4 ua" << s << " = *reinterpret_cast<const float4*>(up + " << p << " * us);\n"
-               << "    float4 ub" << s << " = make_float4(0.f, 0.f, 0.f, 0.f);\n"
-               << "    if constexpr (C > 2) ub" << s << " = *reinterpret_cast<const float4*>(up + " << p << " * us + 4);\n"
+            os << "    const float2 ua" << s << " = *reinterpret_cast<const float2*>(up + " << p << " * us);\n"
+               << "    const float2 ub" << s << " = C > 1 ? *reinterpret_cast<const float2*>(up + " << p << " * us + BM) : make_float2(0.f, 0.f);\n"
+               << "    const float2 uc" << s << " = C > 2 ? *reinterpret_cast<const float2*>(up + " << p << " * us + 2 * BM) : make_float2(0.f, 0.f);\n"
+               << "    const float2 ud" << s << " = C > 3 ? *reinterpret_cast<const float2*>(up + " << p << " * us + 3 * BM) : make_float2(0.f, 0.f);\n"
                << "    const float va" << s << " = vp[" << p << " * C * BN];\n"
                << "    const float vb" << s << " = C > 1 ? vp[(" << p << " * C + 1) * BN] : 0.f;\n"
                << "    const float vc" << s << " = C > 2 ? vp[(" << p << " * C + 2) * BN] : 0.f;\n"
                << "    const float vd" << s << " = C > 3 ? vp[(" << p << " * C + 3) * BN] : 0.f;\n"
-               << "    const float " << colA[a] << " = sc2_dot<C, PW>(ua" << s << ".x, ua" << s << ".z, ub" << s << ".x, ub"
-               << s << ".z, va" << s << ", vb" << s << ", vc" << s << ", vd" << s << ");\n"
-               << "    const float " << colB[a] << " = sc2_dot<C, PW>(ua" << s << ".y, ua" << s << ".w, ub" << s << ".y, ub"
-               << s << ".w, va" << s << ", vb" << s << ", vc" << s << ", vd" << s << ");\n";
+               << "    const float " << colA[a] << " = sc2_dot<C, PW>(ua" << s << ".x, ub" << s << ".x, uc" << s << ".x, ud"
+               << s << ".x, va" << s << ", vb" << s << ", vc" << s << ", vd" << s << ");\n"
+               << "    const float " << colB[a] << " = sc2_dot<C, PW>(ua" << s << ".y, ub" << s << ".y, uc" << s << ".y, ud"
+               << s << ".y, va" << s << ", vb" << s << ", vc" << s << ", vd" << s << ");\n";
             // keep the shared-memory loads of later points behind the sums of these (ptxas would hoist
             // all 64 points' operands and spill)
-            if ((a + 1) % 4 == 0) os << "    asm volatile(\"\" ::: \"memory\");\n";
+            if ((a + 1) % 2 == 0) os << "    asm volatile(\"\" ::: \"memory\");\n";
         }
         auto ra = em.apply(AT, colA);
         auto rb = em.apply(AT, colB);
@@ -1045,21 +1109,23 @@ static void emit_smallc2(std::ostringstream& os, int r, int m, const MatProg& AT
         auto& left = half ? leftB : leftA;
         std::vector<std::vector<std::string>> yv(AT.rows);
         for (int i = 0; i < AT.rows; ++i) yv[i] = em.apply(AT, left[i]);
-        os << "    " << (half ? "if (2 * kp + 1 < K) " : "") << "sc2_store(out, mode, (long long)img * K + 2 * kp + " << half
+        os << "    " << (half ? "if (2 * kp + 1 < K) " : "")
+           << "sc2_store<MODE>(out, coop, live, wbuf, lane, soff, sy0, img, K, 2 * kp + " << half
            << ", Ho, Wo, y0, x0";
         for (int a = 0; a < m; ++a)
             for (int b = 0; b < m; ++b) os << ", " << yv[a][b];
         os << ");\n";
     }
-    os << "  }\n}\n";
+    os << "    first = false;\n  }\n}\n";
     for (int C = 1; C <= 4; ++C)
         for (int pw = 0; pw < 2; ++pw)
-            os << "extern \"C\" __global__ void __launch_bounds__(" << bn * KG << ", 1) wino_smallc2_c" << C
-               << (pw ? "p" : "l")
-               << "(\n    const float* __restrict__ U, const float* __restrict__ V, float* __restrict__ out, int K,\n"
-                  "    int Ho, int Wo, int th, int tw, long long T, long long Tp, long long Kp, long long Cp, int bm,\n"
-                  "    int mode) {\n"
-               << "  sc2_body<" << C << ", " << pw << ">(U, V, out, K, Ho, Wo, th, tw, T, Tp, Kp, Cp, bm, mode);\n}\n";
+            for (int mode = 0; mode < (even ? 3 : 2); ++mode)
+                os << "extern \"C\" __global__ void __launch_bounds__(" << bn * KG << ", 1) wino_smallc2_c" << C
+                   << (pw ? "p" : "l") << "_m" << mode
+                   << "(\n    const float* __restrict__ U, const float* __restrict__ V, float* __restrict__ out, int K,\n"
+                      "    int Ho, int Wo, int th, int tw, long long T, long long Tp, long long Kp, long long Cp) {\n"
+                   << "  sc2_body<" << C << ", " << pw << ", " << mode
+                   << ">(U, V, out, K, Ho, Wo, th, tw, T, Tp, Kp, Cp);\n}\n";
     os << "\n";
 }
 
@@ -1212,7 +1278,7 @@ std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, 
         emit_nhwc(os, r, m, BT, AT, ty, bn, ctr);
         if (!ty.compute_double && !ty.uv_double && !ty.y_double) {
             emit_smallc(os, r, m, AT, ty, ctr);
-            emit_smallc2(os, r, m, AT, bn, ctr);
+            emit_smallc2(os, r, m, AT, bm, bn, ctr);
         }
     }
     return os.str();

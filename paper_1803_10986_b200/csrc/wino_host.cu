@@ -360,7 +360,10 @@ static int launch(CUfunction f, dim3 grid, dim3 block, unsigned smem, void* stre
     }
     CUresult cr = driver().LaunchKernel(f, grid.x, grid.y, grid.z, block.x, block.y, block.z, smem,
                                         (CUstream)stream, args, nullptr);
-    if (cr != CUDA_SUCCESS) return fail(WINO_ECUDA, std::string(what) + ": " + cu_err(cr));
+    if (cr != CUDA_SUCCESS)
+        return fail(WINO_ECUDA, std::string(what) + ": " + cu_err(cr) + " (grid " + std::to_string(grid.x) + "x" +
+                                    std::to_string(grid.y) + ", block " + std::to_string(block.x) + ", dynamic smem " +
+                                    std::to_string(smem) + ")");
     count_launch();
     return WINO_OK;
 }
@@ -885,18 +888,21 @@ int wino_plan_cubin(wino_plan* plan, int which, int channels, void* buf, size_t 
 // codegen.cpp emit_smallc2 (C <= 4): CTA = the bn tiles of one V block x all filters, threads = bn * KG
 static int smallc2_kg() {
     const int v = std::atoi(wino::tuning("sc2_kg").c_str());
-    return v >= 1 && v <= 8 ? v : 3;
+    return v >= 1 && v <= 8 ? v : 2;
 }
-static size_t smallc2_smem(const wino_layer_layout& L, int C) {
-    return ((size_t)L.P * L.Kp * 4 + (size_t)L.P * C * L.bn) * 4;  // sU[P][Kp/2][4][2] + sV[P][C][bn]
+static size_t smallc2_smem(const wino_layer_layout& L, int C, int m) {
+    // sU[P][Kp/bm][C][bm] + sV[P][C][bn] + (even m) one m x 32 x m/2 float2 store buffer per warp
+    const size_t wbuf = m % 2 == 0 ? (size_t)(L.bn * smallc2_kg() / 32) * m * 32 * (m / 2) * 8 : 0;
+    return ((size_t)L.P * L.Kp * C + (size_t)L.P * C * L.bn) * 4 + wbuf;
 }
-static bool smallc2_ok(const wino_layer_layout& L, int C) {
-    return C <= 4 && L.bn % 32 == 0 && L.bn * smallc2_kg() <= 1024 && L.Kp % 2 == 0 && smallc2_smem(L, C) <= 232448;
+static bool smallc2_ok(const wino_layer_layout& L, int C, int m) {
+    return C <= 4 && L.bn % 32 == 0 && L.bm % 4 == 0 && L.bn * smallc2_kg() <= 1024 &&
+           smallc2_smem(L, C, m) <= 232448 - 1024;
 }
 
 static bool smallc_v2(wino_plan* plan, const wino_layer_shape* s) {
     wino_layer_layout L;
-    return !layout_of(plan, s, &L) && smallc2_ok(L, s->C);
+    return !layout_of(plan, s, &L) && smallc2_ok(L, s->C, plan->m);
 }
 
 int wino_plan_prepare(wino_plan* plan, const wino_layer_shape* s, int flags) {
@@ -919,9 +925,14 @@ int wino_plan_prepare(wino_plan* plan, const wino_layer_shape* s, int flags) {
                                                          : "wino_output_xform"});
     }
     if ((flags & WINO_PREPARE_ACT) && !plan->ty.y_double) work.push_back({lm, "wino_output_gather_act"});
-    if ((flags & (WINO_PREPARE_ACT | WINO_PREPARE_CONV)) && wino_smallc_supported(plan, s))
-        work.push_back({lm, std::string(smallc_v2(plan, s) ? "wino_smallc2_c" : "wino_smallc_c") + std::to_string(s->C) +
-                                (plan->chsum == WINO_SUM_PAIRWISE ? "p" : "l")});
+    if ((flags & WINO_PREPARE_ACT) && wino_smallc_supported(plan, s)) {
+        const std::string suf = std::to_string(s->C) + (plan->chsum == WINO_SUM_PAIRWISE ? "p" : "l");
+        if (smallc_v2(plan, s)) {  // one kernel per store mode; the ReLU-only one is what a first layer uses
+            work.push_back({lm, "wino_smallc2_c" + suf + "_m1"});
+        } else {
+            work.push_back({lm, "wino_smallc_c" + suf});
+        }
+    }
     if (flags & WINO_PREPARE_NHWC) {
         work.push_back({lm, "wino_filter_xform"});
         work.push_back({lm, "wino_input_gather_nhwc"});
@@ -1311,7 +1322,7 @@ int wino_smallc_supported(wino_plan* plan, const wino_layer_shape* s) {
     wino_layer_layout L;
     if (!plan || !s || layout_of(plan, s, &L)) return 0;
     if (plan->mode != WINO_CONTRACT_EXACT || plan->precision != WINO_FP32 || s->C > 8) return 0;
-    if (smallc2_ok(L, s->C)) return 1;
+    if (smallc2_ok(L, s->C, plan->m)) return 2;
     const long long cw = s->C <= 4 ? 4 : 8;
     const long long tt = s->C <= 4 ? 96 : 32;  // codegen.cpp emit_smallc: SC_TT
     return (L.P * cw + 4) * (L.Kp + tt) * 4 <= 232448 ? 1 : 0;
@@ -1329,22 +1340,22 @@ int wino_contract_output_smallc(wino_plan* plan, const wino_layer_shape* s, cons
     if (((uintptr_t)U | (uintptr_t)V) & 15) return wino::fail(WINO_EINVAL, "contract_output_smallc: U, V must be 16-byte aligned");
     if ((rc = u_layout_check(U, L, "contract_output_smallc"))) return rc;
     if (s->N == 0) return WINO_OK;
-    const bool v2 = smallc2_ok(L, s->C);
+    const bool v2 = smallc2_ok(L, s->C, plan->m);
     const std::string kname = std::string(v2 ? "wino_smallc2_c" : "wino_smallc_c") + std::to_string(s->C) +
-                              (plan->chsum == WINO_SUM_PAIRWISE ? "p" : "l");
+                              (plan->chsum == WINO_SUM_PAIRWISE ? "p" : "l") + (v2 ? "_m" + std::to_string(mode) : "");
     CUfunction f;
     if ((rc = plan->layer_mod(plan->pick(s))->function(kname.c_str(), &f))) return rc;
     int K = s->K, Ho = L.Ho, Wo = L.Wo, th = L.th, tw = L.tw, bm = L.bm, bn = L.bn;
     long long T = L.T, Tp = L.Tp, Kp = L.Kp, Cp = L.Cp;
     if (v2) {
-        const unsigned smem = (unsigned)smallc2_smem(L, s->C);
+        const unsigned smem = (unsigned)smallc2_smem(L, s->C, plan->m);
         const long long nb = (T + bn - 1) / bn;
         if (nb > (1LL << 30)) return wino::fail(WINO_EUNSUPPORTED, "contract_output_smallc: too many tiles");
-        if (smem > 48 * 1024) {
+        if (smem + 1024 > 48 * 1024) {  // the kernel also has static shared memory (its mbarriers)
             CUresult cr = wino::driver().FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
             if (cr != CUDA_SUCCESS) return wino::fail(WINO_ECUDA, "contract_output_smallc: set smem: " + wino::cu_err(cr));
         }
-        void* args[] = {(void*)&U, (void*)&V, &out, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp, &Cp, &bm, &mode};
+        void* args[] = {(void*)&U, (void*)&V, &out, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp, &Cp};
         return wino::launch(f, dim3((unsigned)nb), dim3((unsigned)(bn * smallc2_kg())), smem, stream, args,
                             "contract_output_smallc");
     }

@@ -59,10 +59,10 @@ class ConvStack:
             if pool:
                 h, w = h // 2, w // 2
         self.out_hw = (h, w)
-        # small-C layers (VGG-16 layer 1) can run K3 + K4 + activation in one kernel (M never
-        # stored, wino_contract_output_smallc); off by default: at VGG layer 1 it is still
-        # slower than K3 + K4act (3.45 vs 2.84 ms, register-spill / latency bound)
-        self.use_smallc(False)
+        # small-C layers (VGG-16 layer 1, C = 3) run K3 + K4 + activation in one kernel (M -- 6 GB
+        # at batch 256 -- never stored, wino_contract_output_smallc) where the fast variant applies
+        # (wino_smallc_supported == 2: 1.63 vs 2.73 ms at VGG layer 1)
+        self.use_smallc(True, fast_only=True)
         ws = max(op.layout.workspace_bytes for op in self.ops)
         self.workspace = D.torch.empty(ws, dtype=D.torch.uint8, device="cuda")
         self._conv_out = None  # pre-activation outputs, allocated on first keep_conv_out forward
@@ -72,10 +72,12 @@ class ConvStack:
             self.act.append(D.empty((N, K, Ho // 2, Wo // 2) if pool else (N, K, Ho, Wo), np.float32))
         self.weights = None
 
-    def use_smallc(self, on: bool = True):
-        """Route qualifying small-C layers through the fused K3 + K4 + activation kernel."""
-        self.smallc = [on and not op.tensor_core and
-                       bool(_native.lib().wino_smallc_supported(op.plan.handle, ctypes.byref(op.shape)))
+    def use_smallc(self, on: bool = True, fast_only: bool = False):
+        """Route qualifying small-C layers through the fused K3 + K4 + activation kernel
+        (fast_only: only where libwino reports the faster-than-unfused variant)."""
+        lib = _native.lib()
+        self.smallc = [on and not op.tensor_core and self.fused_act and
+                       lib.wino_smallc_supported(op.plan.handle, ctypes.byref(op.shape)) >= (2 if fast_only else 1)
                        for op in self.ops]
         return self
 
