@@ -349,12 +349,57 @@ static void emit_output_kernel(std::ostringstream& os, int r, int m, const MatPr
 static void emit_input_gather(std::ostringstream& os, int r, int m, const MatProg& BT, const GenTypes& ty, int bn,
                               int TB, int& ctr) {
     const int n = r + m - 1, P = n * n;
-    os << "static __device__ __forceinline__ void input_gather_body(const in_t* __restrict__ x, uv_t* __restrict__ V,\n"
+    // ST: the image planes this block's tiles read (consecutive images of channels c0 .. c0 + CPT - 1,
+    // each a contiguous H x W run of x) are first copied to shared memory with one cp.async.bulk
+    // per plane (completion on an mbarrier: no staging loop, no registers), and the windows are
+    // gathered from there -- for small images, where a warp's 32 tiles span several tile rows and
+    // every window load from global memory touches 7-13 L1 lines.
+    os << "template <bool ST> static __device__ __forceinline__ in_t k1_ld(const in_t* p) {\n"
+          "  if constexpr (ST) return *p; else return __ldg(p);\n}\n"
+          "template <bool ST> static __device__ __forceinline__ float2 k1_ld2(const float2* p) {\n"
+          "  if constexpr (ST) return *p; else return __ldg(p);\n}\n"
+          "template <bool ST>\n"
+          "static __device__ __forceinline__ void input_gather_body(const in_t* __restrict__ x, uv_t* __restrict__ V,\n"
           "    int C, int H, int W, int pad, int th, int tw, long long T, long long Tp, long long Cp,\n"
           "    float rtw, float rth, int t0, int cb) {\n"
           "  const long long plane = Cp * Tp;\n"
           "  const long long tt = (long long)t0 + threadIdx.x;\n"
        << "  const int c0 = cb * " << gather_cpt(P) << ";\n"
+       << "  extern __shared__ __align__(16) unsigned char k1_smem[];\n"
+          "  __shared__ __align__(8) unsigned long long k1_bar;\n"
+          "  int img_lo = 0;\n"
+          "  if constexpr (ST) {\n"
+          "    if (c0 < C && t0 < T) {  // block-uniform\n"
+          "      const int per = th * tw, HWi = H * W;\n"
+          "      img_lo = t0 / per;\n"
+       << "      const long long tl = (T < (long long)t0 + " << TB << " ? T : (long long)t0 + " << TB << ") - 1;\n"
+       << "      const int nc = C - c0 < " << gather_cpt(P) << " ? C - c0 : " << gather_cpt(P) << ";\n"
+          "      const int ncp = ((int)(tl / per) - img_lo + 1) * nc;\n"
+          "      const unsigned bar = (unsigned)__cvta_generic_to_shared(&k1_bar);\n"
+          "      if (threadIdx.x == 0) {\n"
+          "        asm volatile(\"mbarrier.init.shared::cta.b64 [%0], %1;\" ::\"r\"(bar), \"r\"(1u) : \"memory\");\n"
+          "        asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n"
+          "      }\n"
+          "      __syncthreads();\n"
+          "      if (threadIdx.x < 32) {\n"
+          "        if (threadIdx.x == 0)\n"
+          "          asm volatile(\"mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\" ::\"r\"(bar),\n"
+          "                       \"r\"((unsigned)(ncp * HWi * (int)sizeof(in_t))) : \"memory\");\n"
+          "        __syncwarp();\n"
+          "        for (int j = threadIdx.x; j < ncp; j += 32) {\n"
+          "          const int ii = j / nc, cc = j - ii * nc;\n"
+       << "          const in_t* gp = x + ((long long)(img_lo + ii) * C + c0 + cc) * HWi;\n"
+       << "          in_t* sp = reinterpret_cast<in_t*>(k1_smem) + (long long)(ii * " << gather_cpt(P) << " + cc) * HWi;\n"
+          "          asm volatile(\"cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\"\n"
+          "                       ::\"r\"((unsigned)__cvta_generic_to_shared(sp)), \"l\"(gp),\n"
+          "                         \"r\"((unsigned)(HWi * (int)sizeof(in_t))), \"r\"(bar) : \"memory\");\n"
+          "        }\n"
+          "      }\n"
+          "      asm volatile(\"{\\n\\t.reg .pred P1;\\nK1_WAIT_%=:\\n\\t\"\n"
+          "                   \"mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\\n\\t\"\n"
+          "                   \"@!P1 bra K1_WAIT_%=;\\n}\\n\" ::\"r\"(bar), \"r\"(0u) : \"memory\");\n"
+          "    }\n"
+          "  }\n"
        << "  if (tt >= Tp) return;\n"
        << "  uv_t* op = V + ((tt / " << bn << ") * Cp + c0) * " << bn << " + (tt % " << bn << ");\n"
        << "  if (tt >= T || c0 >= C) {\n"
@@ -373,7 +418,9 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
           "  const int ti = ti0 + k - di * th;\n"
        << "  const int h0 = ti * " << m << " - pad, w0 = tj * " << m << " - pad;\n"
        << "  const long long HW = (long long)H * W;\n"
-       << "  const in_t* src = x + ((long long)(img0 + di) * C + c0) * HW;\n"
+       << "  const in_t* src = ST ? reinterpret_cast<const in_t*>(k1_smem) + (long long)(img0 + di - img_lo) * "
+       << gather_cpt(P) << " * HW\n"
+          "                       : x + ((long long)(img0 + di) * C + c0) * HW;\n"
        << "  const bool interior = h0 >= 0 && w0 >= 0 && h0 + " << n << " <= H && w0 + " << n << " <= W;\n"
        << (gather_cpt(P) > 1 && P <= 16 ? "#pragma unroll\n" : "#pragma unroll 1\n")
        << "  for (int cc = 0; cc < " << gather_cpt(P) << "; ++cc, src += HW, op += " << bn << ") {\n"
@@ -406,7 +453,7 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
                << "    const int W2 = W >> 1;\n";
             for (int a = 0; a < n; ++a) {
                 for (int q = 0; q < nl; ++q)
-                    os << "    const float2 f" << a << "_" << q << " = __ldg(rp + " << a << " * W2 + " << q << ");\n";
+                    os << "    const float2 f" << a << "_" << q << " = k1_ld2<ST>(rp + " << a << " * W2 + " << q << ");\n";
                 for (int b = 0; b < n; ++b) {
                     const int e = b + sh;
                     os << "    " << d[a][b] << " = (" << wt << ")f" << a << "_" << e / 2 << (e % 2 ? ".y" : ".x") << ";\n";
@@ -421,7 +468,7 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
     os << "    const in_t* rp = src + h0 * W + w0;\n";
     for (int a = 0; a < n; ++a)
         for (int b = 0; b < n; ++b)
-            os << "    " << d[a][b] << " = (" << wt << ")__ldg(rp + " << a << " * W + " << b << ");\n";
+            os << "    " << d[a][b] << " = (" << wt << ")k1_ld<ST>(rp + " << a << " * W + " << b << ");\n";
     os << "  } else {\n";
     for (int a = 0; a < n; ++a)
         os << "    const bool r" << a << " = (unsigned)(h0 + " << a << ") < (unsigned)H;\n";
@@ -429,7 +476,7 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
         os << "    const bool c" << b << " = (unsigned)(w0 + " << b << ") < (unsigned)W;\n";
     for (int a = 0; a < n; ++a)
         for (int b = 0; b < n; ++b)
-            os << "    " << d[a][b] << " = (r" << a << " && c" << b << ") ? (" << wt << ")__ldg(src + (h0 + " << a
+            os << "    " << d[a][b] << " = (r" << a << " && c" << b << ") ? (" << wt << ")k1_ld<ST>(src + (h0 + " << a
                << ") * W + (w0 + " << b << ")) : (" << wt << ")0;\n";
     os << "  }\n";
     Emitter em(os, ty.compute_double, ctr);
@@ -455,25 +502,28 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
     // spill); tuning key k1rowwise = 2..6 selects another bound (0: row-wise off)
     const int rw_blocks = std::atoi(tuning("k1rowwise").c_str()) >= 2 ? std::atoi(tuning("k1rowwise").c_str()) : 3;
     const std::string lb = rowwise ? std::to_string(TB) + ", " + std::to_string(rw_blocks * 128 / TB) : std::to_string(TB);
-    os << "extern \"C\" __global__ void __launch_bounds__(" << lb << ") wino_input_gather(\n"
-          "    const in_t* __restrict__ x, uv_t* __restrict__ V, int C, int H, int W, int pad, int th,\n"
-          "    int tw, long long T, long long Tp, long long Cp, int Wl, float rtw, float rth) {\n"
-       << "  input_gather_body(x, V, C, H, W, pad, th, tw, T, Tp, Cp, rtw, rth, blockIdx.y * " << TB
-       << ", blockIdx.x);\n"
-       << "}\n\n"
-       << "extern \"C\" __global__ void __launch_bounds__(" << lb << ") wino_transforms_gather(\n"
-          "    const in_t* __restrict__ x, uv_t* __restrict__ V, int C, int H, int W, int pad, int th,\n"
-          "    int tw, long long T, long long Tp, long long Cp, int n_tb,\n"
-          "    const in_t* __restrict__ w, uv_t* __restrict__ U, int K, long long Kp, int Wl, float rtw, float rth) {\n"
-          "  if ((int)blockIdx.y < n_tb) {\n"
-       << "    input_gather_body(x, V, C, H, W, pad, th, tw, T, Tp, Cp, rtw, rth, blockIdx.y * " << TB
-       << ", blockIdx.x);\n"
-       << "  } else {\n"
-       << "    for (int cc = 0; cc < " << gather_cpt(P) << "; ++cc)\n"
-       << "      filter_body(w, U, K, C, Kp, Cp, (blockIdx.y - n_tb) * " << TB << " + threadIdx.x, blockIdx.x * "
-       << gather_cpt(P) << " + cc);\n"
-          "  }\n"
-          "}\n\n";
+    for (int st = 0; st < 2; ++st) {
+        const std::string sfx = st ? "_st" : "", tp = st ? "<true>" : "<false>";
+        os << "extern \"C\" __global__ void __launch_bounds__(" << lb << ") wino_input_gather" << sfx << "(\n"
+              "    const in_t* __restrict__ x, uv_t* __restrict__ V, int C, int H, int W, int pad, int th,\n"
+              "    int tw, long long T, long long Tp, long long Cp, int Wl, float rtw, float rth) {\n"
+           << "  input_gather_body" << tp << "(x, V, C, H, W, pad, th, tw, T, Tp, Cp, rtw, rth, blockIdx.y * " << TB
+           << ", blockIdx.x);\n"
+           << "}\n\n"
+           << "extern \"C\" __global__ void __launch_bounds__(" << lb << ") wino_transforms_gather" << sfx << "(\n"
+              "    const in_t* __restrict__ x, uv_t* __restrict__ V, int C, int H, int W, int pad, int th,\n"
+              "    int tw, long long T, long long Tp, long long Cp, int n_tb,\n"
+              "    const in_t* __restrict__ w, uv_t* __restrict__ U, int K, long long Kp, int Wl, float rtw, float rth) {\n"
+              "  if ((int)blockIdx.y < n_tb) {\n"
+           << "    input_gather_body" << tp << "(x, V, C, H, W, pad, th, tw, T, Tp, Cp, rtw, rth, blockIdx.y * " << TB
+           << ", blockIdx.x);\n"
+           << "  } else {\n"
+           << "    for (int cc = 0; cc < " << gather_cpt(P) << "; ++cc)\n"
+           << "      filter_body(w, U, K, C, Kp, Cp, (blockIdx.y - n_tb) * " << TB << " + threadIdx.x, blockIdx.x * "
+           << gather_cpt(P) << " + cc);\n"
+              "  }\n"
+              "}\n\n";
+    }
 }
 
 // K4, gather form: thread = (tile t, output channel k).  Its P values

@@ -716,6 +716,24 @@ bool k1_gather() {
     return v;
 }
 
+// K1 from shared-memory copies of the image planes (codegen.cpp input_gather_body<true>): f32 inputs,
+// planes of a multiple of 16 bytes, and the planes a 128-tile block can touch must fit (several
+// blocks per SM).  On by default where it applies (VGG-16 batch 256: 14 x 14 layers 119.5 -> 103.2 us,
+// 28 x 28 289 -> 245 us, 56 x 56 494 -> 455 us; single small layers unchanged); tuning key "k1" =
+// "gather" turns it off, "bulk<KB>" changes the shared-memory cap.
+bool k1_staged(const wino_plan* p, const wino_layer_shape* s, const wino_layer_layout& L, const void* x, int tb,
+               unsigned* smem) {
+    const std::string e = wino::tuning("k1");
+    if (e == "gather" || e == "tile" || p->ty.in_double) return false;
+    const long long hw = (long long)s->H * s->W, per = (long long)L.th * L.tw;
+    if (hw % 4 || ((uintptr_t)x & 15) || per <= 0) return false;
+    const long long planes = ((tb - 1) / per + 2) * wino::gather_cpt(L.P);
+    const long long bytes = planes * hw * 4;
+    *smem = (unsigned)bytes;
+    const long long cap = e.rfind("bulk", 0) == 0 && e.size() > 4 ? std::atoll(e.c_str() + 4) * 1024 : 96 * 1024;
+    return bytes <= cap;  // "bulk<KB>" overrides the cap (sweeps)
+}
+
 }  // namespace
 
 // ================================================================== C-ABI
@@ -1013,12 +1031,16 @@ int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, c
     }
     if (!tc && k1_gather() && (long long)n_tb + n_kb <= 65535 && Cp <= 65535) {
         CUfunction fg;
-        if ((rc = plan->layer_mod(plan->pick(s))->function("wino_transforms_gather", &fg))) return rc;
+        unsigned st_smem = 0;
+        const bool st = k1_staged(plan, s, L, x, tb, &st_smem);
+        if ((rc = plan->layer_mod(plan->pick(s))->function(st ? "wino_transforms_gather_st" : "wino_transforms_gather",
+                                                           &fg)))
+            return rc;
         float rtw = 1.0f / tw, rth = 1.0f / th;
         void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &n_tb, (void*)&w, &U, &K, &Kp,
                         &Wl, &rtw, &rth};
-        return wino::launch(fg, dim3((unsigned)(Cp / wino::gather_cpt(L.P)), (unsigned)(n_tb + n_kb)), dim3(tb), 0,
-                            stream, args, "transforms");
+        return wino::launch(fg, dim3((unsigned)(Cp / wino::gather_cpt(L.P)), (unsigned)(n_tb + n_kb)), dim3(tb),
+                            st ? st_smem : 0, stream, args, "transforms");
     }
     if (plan->fused()) return wino::fail(WINO_EUNSUPPORTED, "transforms: grid too large for the fused layout");
     void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &n_tb, (void*)&w, &U, &K, &Kp, &n_kb, &cfast};
@@ -1038,11 +1060,14 @@ int wino_input_transform(wino_plan* plan, const wino_layer_shape* s, const void*
         const int tb = xform_block(plan, &smem);
         int Wl = 0, n_tb = (int)cdiv(Tp, tb);
         if (n_tb <= 65535 && Cp <= 65535) {
-            if ((rc = plan->layer_mod(plan->pick(s))->function("wino_input_gather", &f))) return rc;
+            unsigned st_smem = 0;
+            const bool st = k1_staged(plan, s, L, x, tb, &st_smem);
+            if ((rc = plan->layer_mod(plan->pick(s))->function(st ? "wino_input_gather_st" : "wino_input_gather", &f)))
+                return rc;
             float rtw = 1.0f / tw, rth = 1.0f / th;
             void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &Wl, &rtw, &rth};
-            return wino::launch(f, dim3((unsigned)(Cp / wino::gather_cpt(L.P)), (unsigned)n_tb), dim3(tb), 0, stream,
-                                args, "input_transform");
+            return wino::launch(f, dim3((unsigned)(Cp / wino::gather_cpt(L.P)), (unsigned)n_tb), dim3(tb),
+                                st ? st_smem : 0, stream, args, "input_transform");
         }
     }
     if (plan->mode >= WINO_CONTRACT_TC_BF16 && (k1_gather() || plan->fused()) && Cp / 8 <= 65535 && L.P <= 16 &&

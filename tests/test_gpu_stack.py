@@ -113,8 +113,10 @@ def test_smallc_fused_kernel_matches_unfused(cs):
     s = torch.cuda.current_stream().cuda_stream
     for m, pts in ((6, P8), (4, "0,1,-1,1/2,-1/2,inf"), (3, "0,1,-1,2,-2")):
         ts = W.build_transforms(3, m, W.parse_points(pts))
-        for C in range(1, 9):
-            N, K, H, Wd = 2, 7 + C, 17 + C, 23
+        # odd output width (scalar stores), then an even one (the C <= 4 kernel's warp-cooperative row
+        # stores: partial edge tiles, warps spanning tile rows and images, two U blocks for K = 70)
+        for C, (N, K, H, Wd) in [(C, (2, 7 + C, 17 + C, 23)) for C in range(1, 9)] + \
+                                [(C, (5, 70 if C == 2 else 9 + C, 20, 26)) for C in range(1, 5)]:
             op = W.layer_op(ts, W.ConvConfig("fp32", "huffman", cs), N, C, H, Wd, K, 1)
             assert lib.wino_smallc_supported(op.plan.handle, ctypes.byref(op.shape))
             x = torch.from_numpy(O.synthetic((N, C, H, Wd), 12, C)).cuda()
@@ -135,7 +137,7 @@ def test_smallc_fused_kernel_matches_unfused(cs):
                                                               _native.as_ptr(U), _native.as_ptr(V),
                                                               _native.as_ptr(got), mode, s))
                 torch.cuda.synchronize()
-                assert torch.equal(got.view(torch.int32), want.view(torch.int32)), (m, C, cs, mode)
+                assert torch.equal(got.view(torch.int32), want.view(torch.int32)), (m, C, K, H, Wd, cs, mode)
 
 
 @pytest.mark.parametrize("chunks", [1, 3, [1, 3, 1], [32, 192, 32], [4, 4, 4, 4, 4, 4, 4]],
