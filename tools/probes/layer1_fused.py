@@ -1,6 +1,6 @@
 """VGG-16 layer 1 (N x 3 x 224 x 224 -> 64 filters, F(6x6,3x3), pairwise): K3 + K4act (M through HBM)
 vs the fused small-C kernel (wino_contract_output_smallc).  Bitwise check + CUDA-event timing.
-usage: python tools/probes/layer1_fused.py [N] [sc2_kg]"""
+usage: [WINO_SC2_KG=k] python tools/probes/layer1_fused.py [N]"""
 import ctypes
 import sys
 
@@ -11,9 +11,10 @@ sys.path.insert(0, ".")
 import paper_1803_10986_b200 as W
 from paper_1803_10986_b200 import _native
 
+sys.path.insert(0, "tools")
+import tuning_env  # noqa: E402,F401  (WINO_SC2_KG -> libwino tuning key)
+
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 256
-if len(sys.argv) > 2:
-    _native.check(_native.lib().wino_tuning_set(b"sc2_kg", sys.argv[2].encode()))
 P8 = "0,-1,1,1/2,-1/2,2,-2,inf"
 ts = W.build_transforms(3, 6, W.parse_points(P8))
 lib = _native.lib()
