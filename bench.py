@@ -633,9 +633,14 @@ def run_vgg(args):
             L = op_.layout
             t_x, t_c, t_o = (ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]))
             P, T = L.P, L.T
-            b_x = 4 * n * C * h * w_ + 4 * P * C * T + 4 * K * C * 9 + 4 * P * C * K  # x read, V + U written
+            fused_prev, fused_next = i > 0 and st.fuse_next[i - 1], st.fuse_next[i]
+            # x read, V + U written (K2 only when the previous layer's K4 already wrote this layer's V)
+            b_x = (0 if fused_prev else 4 * n * C * h * w_ + 4 * P * C * T) + 4 * K * C * 9 + 4 * P * C * K
             out_el = n * K * (L.Ho // 2) * (L.Wo // 2) if pool else n * K * L.Ho * L.Wo
             b_o = 4 * P * K * T + 4 * out_el                                             # M read, act written
+            if fused_next:  # K4 + act + K1 of the next layer: M read, the next layer's V written
+                L2 = st.ops[i + 1].layout
+                b_o = 4 * P * K * T + 4 * L2.P * K * L2.T
             if st.smallc[i]:
                 # K3 + K4 + activation in one kernel (small C): M never exists; bytes = V read + act written
                 b_f = 4 * P * C * T + 4 * P * C * K + 4 * out_el
@@ -650,7 +655,8 @@ def run_vgg(args):
             per_layer.append({"layer": i + 1, "C": C, "K": K, "H": h, "tile_bm_bn": [L.bm, L.bn],
                               "transforms_ms": t_x, "transforms_frac_hbm": b_x / (t_x * 1e-3) / 1e9 / hbm,
                               "contract_ms": t_c, "contract_tflops": op_.contraction_flops / (t_c * 1e-3) / 1e12,
-                              "output_act_ms": t_o, "output_act_frac_hbm": b_o / (t_o * 1e-3) / 1e9 / hbm})
+                              "output_act_ms": t_o, "output_act_frac_hbm": b_o / (t_o * 1e-3) / 1e9 / hbm,
+                              "v_written_by_previous_k4": bool(fused_prev), "k4_fused_with_next_k1": bool(fused_next)})
             c_ms += t_c
             other_ms += t_x + t_o
             c_flops += op_.contraction_flops

@@ -135,6 +135,7 @@ int wino_plan_cubin(wino_plan* plan, int which, int channels, void* buf, size_t 
 #define WINO_PREPARE_ACT 2    /* K4 with ReLU / max-pool (wino_output_transform_act) */
 #define WINO_PREPARE_STAGES 4 /* wino_filter_transform / wino_input_transform alone */
 #define WINO_PREPARE_NHWC 8   /* K2, K1, K3, K4 of wino_conv2d_nhwc */
+#define WINO_PREPARE_K4K1 16  /* s as the second layer of wino_output_input_transform (+ K2 alone) */
 int wino_plan_prepare(wino_plan* plan, const wino_layer_shape* s, int flags);
 
 /* ---- layer-level Winograd convolution (new entry point; the reference
@@ -171,6 +172,18 @@ int wino_output_transform(wino_plan* plan, const wino_layer_shape* s, const void
  * values as wino_output_transform followed by wino_relu_pool, y never stored. */
 int wino_output_transform_act(wino_plan* plan, const wino_layer_shape* s, const void* M,
                               void* act, int pool, void* stream);
+/* K4 of layer s + activation + K1 of the next layer s2 in ONE kernel (conv stacks; fp32 plans
+ * with an FP32 contraction): a block owns whole (image, channel) planes of the activation
+ * between the layers, runs layer s's output transform + ReLU (+ 2x2 max-pool, pool = 1) into
+ * shared memory and layer s2's input transform from there, so the activation is never written
+ * to or read from HBM -- engine.py:418-423 then engine.py:410,412 per tile.  V2 gets exactly
+ * what wino_output_transform_act followed by wino_input_transform(s2) would write (same
+ * rounded operations).  Needs s2 = (N, K, Ho[/2], Wo[/2]) of s, unpadded channels in s2's
+ * layout (Cp == C) and PL planes in shared memory; wino_output_input_supported() says so. */
+int wino_output_input_supported(wino_plan* plan, const wino_layer_shape* s, int pool,
+                                const wino_layer_shape* s2);
+int wino_output_input_transform(wino_plan* plan, const wino_layer_shape* s, const void* M, int pool,
+                                const wino_layer_shape* s2, void* V2, void* stream);
 /* K3 + K4 fused (TCF modes only): y = A^T (sum_c U_p[c] V_p[c]) A straight
  * from the tensor-memory accumulators -- engine.py:415-423 */
 int wino_contract_output(wino_plan* plan, const wino_layer_shape* s, const void* U, const void* V,

@@ -43,7 +43,7 @@ class LayerLayout(ctypes.Structure):
                 ("workspace_bytes", c_size_t)]
 
 
-PREPARE_CONV, PREPARE_ACT, PREPARE_STAGES, PREPARE_NHWC = 1, 2, 4, 8  # wino_plan_prepare flags (include/wino.h)
+PREPARE_CONV, PREPARE_ACT, PREPARE_STAGES, PREPARE_NHWC, PREPARE_K4K1 = 1, 2, 4, 8, 16  # wino_plan_prepare flags (include/wino.h)
 
 # (name, restype, argtypes) of every exported symbol, in include/wino.h order
 SIGNATURES = [
@@ -60,6 +60,9 @@ SIGNATURES = [
     ("wino_contract", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_void_p]),
     ("wino_output_transform", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p]),
     ("wino_output_transform_act", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_int, c_void_p]),
+    ("wino_output_input_supported", c_int, [c_void_p, POINTER(LayerShape), c_int, POINTER(LayerShape)]),
+    ("wino_output_input_transform", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_int, POINTER(LayerShape),
+                                            c_void_p, c_void_p]),
     ("wino_smallc_supported", c_int, [c_void_p, POINTER(LayerShape)]),
     ("wino_contract_output_smallc", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_int,
                                             c_void_p]),

@@ -1179,6 +1179,104 @@ static void emit_smallc2(std::ostringstream& os, int r, int m, const MatProg& AT
     os << "\n";
 }
 
+// K4 of layer i fused with K1 of layer i + 1 (conv stacks, fp32): a block owns PL whole (image,
+// channel) planes of the activation between the two layers.  Phase 1 is the gather output transform
+// of layer i (thread = tile: alpha^2 coalesced M loads, (A^T M) A, ReLU, optional 2x2 max-pool --
+// the expressions of wino_output_gather_act) written to the planes in shared memory; phase 2 is
+// the gather input transform of layer i + 1 (thread = tile: window from shared memory with the
+// zero padding, (B^T d) B, V stores coalesced across tiles -- the expressions of
+// input_gather_body).  The activation never goes to HBM: per (tile, channel) the pair moves
+// alpha^2 + alpha^2 values instead of alpha^2 + m^2 and m^2 + alpha^2.  Planes are whole, so
+// there is no halo between blocks.  Same rounded operations, hence the same bits, as the two
+// kernels it replaces.  The kernel lives in the module of layer i + 1 (V blocking bn).
+static void emit_k4k1(std::ostringstream& os, int r, int m, const MatProg& BT, const MatProg& AT, int bn, int& ctr) {
+    const int n = r + m - 1, P = n * n;
+    // Block order: KS consecutive filters innermost, then the plane groups, so the blocks resident at
+    // one time read KS long contiguous runs of M (consecutive tiles of one filter) and write V in
+    // runs of KS consecutive channels (2 KB for KS = 8) -- with the filter as the slow grid axis every
+    // 256-byte V row landed 128 KB from the next one.
+    os << "extern \"C\" __global__ void __launch_bounds__(128) wino_k4k1(\n"
+          "    const float* __restrict__ Mm, float* __restrict__ V, int N, int PL, int pool, int K, int G, int KS,\n"
+          "    int Ho, int Wo, int th, int tw, long long Tp, long long Kp,\n"
+          "    int H2, int W2, int pad2, int th2, int tw2, long long T2, long long Tp2, long long Cp2) {\n"
+          "  extern __shared__ __align__(16) float k41_plane[];  // [PL][H2][W2]\n"
+          "  const int kk = blockIdx.x % KS, rest = blockIdx.x / KS, grp = rest % G;\n"
+          "  const int k = (rest / G) * KS + kk, n0 = grp * PL;\n"
+          "  if (k >= K) return;\n"
+          "  const int np = N - n0 < PL ? N - n0 : PL;\n"
+          "  const int per1 = th * tw, per2 = th2 * tw2, HW2 = H2 * W2;\n"
+          "  const long long mplane = Kp * Tp;\n"
+          "#pragma unroll 1\n"
+          "  for (int q = threadIdx.x; q < np * per1; q += 128) {\n"
+          "    const int pl = q / per1, rem = q - pl * per1, ti = rem / tw, tj = rem - ti * tw;\n"
+          "    const float* src = Mm + (long long)k * Tp + (long long)n0 * per1 + q;\n";
+    std::vector<std::vector<std::string>> mm(n, std::vector<std::string>(n));
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+            mm[a][b] = "m" + std::to_string(a) + "_" + std::to_string(b);
+            os << "    const float " << mm[a][b] << " = __ldg(src + " << (a * n + b) << " * mplane);\n";
+        }
+    {
+        Emitter em(os, false, ctr);
+        auto yv = em.apply2d(AT, mm);
+        os << "    float* dst = k41_plane + pl * HW2;\n"
+           << "    const int y0 = ti * " << m << ", x0 = tj * " << m << ";\n"
+              "    if (!pool) {\n";
+        for (int a = 0; a < m; ++a) {
+            os << "      if (y0 + " << a << " < Ho) {\n";
+            for (int b = 0; b < m; ++b)
+                os << "        if (x0 + " << b << " < Wo) dst[(y0 + " << a << ") * W2 + x0 + " << b << "] = wino_relu("
+                   << yv[a][b] << ");\n";
+            os << "      }\n";
+        }
+        os << "    } else {\n";
+        if (m % 2 == 0) {
+            os << "      const int py0 = y0 >> 1, px0 = x0 >> 1;\n";
+            for (int a = 0; a < m / 2; ++a) {
+                os << "      if (py0 + " << a << " < H2) {\n";
+                for (int b = 0; b < m / 2; ++b)
+                    os << "        if (px0 + " << b << " < W2) dst[(py0 + " << a << ") * W2 + px0 + " << b
+                       << "] = wino_relu(fmaxf(fmaxf(" << yv[2 * a][2 * b] << ", " << yv[2 * a][2 * b + 1] << "), fmaxf("
+                       << yv[2 * a + 1][2 * b] << ", " << yv[2 * a + 1][2 * b + 1] << ")));\n";
+                os << "      }\n";
+            }
+        }
+        os << "    }\n  }\n";
+    }
+    os << "  __syncthreads();\n"
+          "  const long long vplane = Cp2 * Tp2;\n"
+          "#pragma unroll 1\n"
+          "  for (int q = threadIdx.x; q < np * per2; q += 128) {\n"
+          "    const int pl = q / per2, rem = q - pl * per2, ti = rem / tw2, tj = rem - ti * tw2;\n"
+          "    const long long t2 = (long long)n0 * per2 + q;\n"
+       << "    float* op = V + ((t2 / " << bn << ") * Cp2 + k) * " << bn << " + (t2 % " << bn << ");\n"
+       << "    const int h0 = ti * " << m << " - pad2, w0 = tj * " << m << " - pad2;\n"
+          "    const float* sp = k41_plane + pl * HW2;\n";
+    std::vector<std::vector<std::string>> d(n, std::vector<std::string>(n));
+    for (int a = 0; a < n; ++a) os << "    const bool r" << a << " = (unsigned)(h0 + " << a << ") < (unsigned)H2;\n";
+    for (int b = 0; b < n; ++b) os << "    const bool c" << b << " = (unsigned)(w0 + " << b << ") < (unsigned)W2;\n";
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+            d[a][b] = "x" + std::to_string(a) + "_" + std::to_string(b);
+            os << "    const float " << d[a][b] << " = (r" << a << " && c" << b << ") ? sp[(h0 + " << a << ") * W2 + (w0 + "
+               << b << ")] : 0.f;\n";
+        }
+    {
+        Emitter em(os, false, ctr);
+        auto v = em.apply2d(BT, d);
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) os << "    op[" << (i * n + j) << " * vplane] = " << v[i][j] << ";\n";
+    }
+    os << "  }\n"
+          "  // tiles padding T2 up to the contraction's tile: zeros, as K1 writes them\n"
+          "  if (grp == G - 1)\n"
+          "    for (long long tt = T2 + threadIdx.x; tt < Tp2; tt += 128) {\n"
+       << "      float* op = V + ((tt / " << bn << ") * Cp2 + k) * " << bn << " + (tt % " << bn << ");\n"
+       << "      for (int p = 0; p < " << P << "; ++p) op[p * vplane] = 0.f;\n"
+          "    }\n"
+          "}\n\n";
+}
+
 std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, const MatProg& AT,
                              const GenTypes& ty, int bm, int bn) {
     const int n = r + m - 1, P = n * n;
@@ -1329,6 +1427,7 @@ std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, 
         if (!ty.compute_double && !ty.uv_double && !ty.y_double) {
             emit_smallc(os, r, m, AT, ty, ctr);
             emit_smallc2(os, r, m, AT, bm, bn, ctr);
+            emit_k4k1(os, r, m, BT, AT, bn, ctr);
         }
     }
     return os.str();

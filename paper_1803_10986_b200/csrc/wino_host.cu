@@ -743,7 +743,7 @@ const char* wino_last_error(void) { return wino::g_last_error.c_str(); }
 
 int wino_tuning_set(const char* key, const char* value) {
     static const char* const keys[] = {"gemm", "dbuf", "k1", "k1order", "k4", "k1tc", "tile_interp",
-                                       "cpt", "kpt", "tcf_nk", "tcf_dbg", "tc_epi", "k1rowwise", "k4rowwise", "sc2_kg"};
+                                       "cpt", "kpt", "tcf_nk", "tcf_dbg", "tc_epi", "k1rowwise", "k4rowwise", "sc2_kg", "k4k1_ks"};
     if (!key) return wino::fail(WINO_EINVAL, "tuning_set: null key");
     bool known = false;
     for (const char* k : keys) known = known || std::strcmp(k, key) == 0;
@@ -943,6 +943,10 @@ int wino_plan_prepare(wino_plan* plan, const wino_layer_shape* s, int flags) {
                                                          : "wino_output_xform"});
     }
     if ((flags & WINO_PREPARE_ACT) && !plan->ty.y_double) work.push_back({lm, "wino_output_gather_act"});
+    if ((flags & WINO_PREPARE_K4K1) && plan->precision == WINO_FP32 && plan->mode < WINO_CONTRACT_TC_BF16) {
+        work.push_back({lm, "wino_k4k1"});       // as the SECOND layer of wino_output_input_transform
+        work.push_back({lm, "wino_filter_xform"});
+    }
     if ((flags & WINO_PREPARE_ACT) && wino_smallc_supported(plan, s)) {
         const std::string suf = std::to_string(s->C) + (plan->chsum == WINO_SUM_PAIRWISE ? "p" : "l");
         if (smallc_v2(plan, s)) {  // one kernel per store mode; the ReLU-only one is what a first layer uses
@@ -1157,6 +1161,60 @@ int wino_output_transform_act(wino_plan* plan, const wino_layer_shape* s, const 
     float rtw = 1.0f / tw, rth = 1.0f / th;
     void* args[] = {(void*)&M, &act, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp, &rtw, &rth, &pool};
     return wino::launch(f, dim3(cdiv(T, 128), (unsigned)K, 1), dim3(128), 0, stream, args, "output_transform_act");
+}
+
+// K4 of layer `s` + activation + K1 of layer `s2` in one kernel (codegen.cpp emit_k4k1)
+static int k4k1_geometry(wino_plan* plan, const wino_layer_shape* s, int pool, const wino_layer_shape* s2,
+                         wino_layer_layout* L, wino_layer_layout* L2, int* PL, unsigned* smem) {
+    int rc;
+    if (!plan || !s || !s2) return wino::fail(WINO_EINVAL, "output_input_transform: null argument");
+    if ((rc = layout_of(plan, s, L)) || (rc = layout_of(plan, s2, L2))) return rc;
+    if (plan->mode >= WINO_CONTRACT_TC_BF16 || plan->precision != WINO_FP32)
+        return wino::fail(WINO_EUNSUPPORTED, "output_input_transform: fp32 plans with an FP32 contraction only");
+    if (pool != 0 && pool != 1) return wino::fail(WINO_EINVAL, "output_input_transform: pool must be 0 or 1");
+    if (pool && (plan->m & 1)) return wino::fail(WINO_EUNSUPPORTED, "output_input_transform: pooling needs an even m");
+    const int H2 = pool ? L->Ho / 2 : L->Ho, W2 = pool ? L->Wo / 2 : L->Wo;
+    if (s2->N != s->N || s2->C != s->K || s2->H != H2 || s2->W != W2)
+        return wino::fail(WINO_EINVAL, "output_input_transform: the second layer does not take the first one's activation");
+    if (L2->Cp != s2->C)  // padded channels of V are K1's job
+        return wino::fail(WINO_EUNSUPPORTED, "output_input_transform: the second layer's channels are padded");
+    if (s->K > 65535) return wino::fail(WINO_EUNSUPPORTED, "output_input_transform: K > 65535");
+    const long long per1 = (long long)L->th * L->tw, hw2 = (long long)H2 * W2;
+    *PL = (int)std::max(1LL, 128 / per1);
+    const long long bytes = (long long)*PL * hw2 * 4;
+    if (hw2 <= 0 || bytes > 200 * 1024) return wino::fail(WINO_EUNSUPPORTED, "output_input_transform: plane too large for shared memory");
+    *smem = (unsigned)bytes;
+    return WINO_OK;
+}
+
+int wino_output_input_supported(wino_plan* plan, const wino_layer_shape* s, int pool, const wino_layer_shape* s2) {
+    wino_layer_layout L, L2;
+    int PL;
+    unsigned smem;
+    return k4k1_geometry(plan, s, pool, s2, &L, &L2, &PL, &smem) == WINO_OK ? 1 : 0;
+}
+
+int wino_output_input_transform(wino_plan* plan, const wino_layer_shape* s, const void* M, int pool,
+                                const wino_layer_shape* s2, void* V2, void* stream) {
+    wino_layer_layout L, L2;
+    int PL, rc;
+    unsigned smem;
+    if ((rc = k4k1_geometry(plan, s, pool, s2, &L, &L2, &PL, &smem))) return rc;
+    if ((uintptr_t)V2 & 15) return wino::fail(WINO_EINVAL, "output_input_transform: V must be 16-byte aligned");
+    if (s->N == 0) return WINO_OK;
+    CUfunction f;
+    if ((rc = plan->layer_mod(plan->pick(s2))->function("wino_k4k1", &f))) return rc;
+    int N = s->N, Ho = L.Ho, Wo = L.Wo, th = L.th, tw = L.tw, H2 = s2->H, W2 = s2->W, pad2 = s2->pad, th2 = L2.th,
+        tw2 = L2.tw;
+    long long Tp = L.Tp, Kp = L.Kp, T2 = L2.T, Tp2 = L2.Tp, Cp2 = L2.Cp;
+    int K = s->K, G = (int)cdiv(N, PL), KS = 8;
+    const std::string ks = wino::tuning("k4k1_ks");
+    if (!ks.empty() && std::atoi(ks.c_str()) > 0) KS = std::atoi(ks.c_str());
+    const long long blocks = (long long)G * cdiv(K, KS) * KS;
+    if (blocks >= (1LL << 31)) return wino::fail(WINO_EUNSUPPORTED, "output_input_transform: grid too large");
+    void* args[] = {(void*)&M, &V2, &N, &PL, &pool, &K, &G, &KS, &Ho, &Wo, &th, &tw, &Tp, &Kp,
+                    &H2, &W2, &pad2, &th2, &tw2, &T2, &Tp2, &Cp2};
+    return wino::launch(f, dim3((unsigned)blocks, 1, 1), dim3(128), smem, stream, args, "output_input_transform");
 }
 
 int wino_output_transform(wino_plan* plan, const wino_layer_shape* s, const void* M, void* y, void* stream) {

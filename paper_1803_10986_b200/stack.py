@@ -62,9 +62,18 @@ class ConvStack:
         # small-C layers (VGG-16 layer 1, C = 3) run K3 + K4 + activation in one kernel (M -- 6 GB
         # at batch 256 -- never stored, wino_contract_output_smallc) where the fast variant applies
         # (wino_smallc_supported == 2: 1.63 vs 2.73 ms at VGG layer 1)
+        self._fuse_on = False
         self.use_smallc(True, fast_only=True)
         ws = max(op.layout.workspace_bytes for op in self.ops)
         self.workspace = D.torch.empty(ws, dtype=D.torch.uint8, device="cuda")
+        # K4 of layer i + activation + K1 of layer i + 1 can run as one kernel (the activation between
+        # them never goes to HBM, wino_output_input_transform; layer i + 1's V is written while layer
+        # i's M is read, so layers then alternate between two workspaces).  Off by default: bitwise
+        # equal, but at VGG-16 batch 256 only the 28 x 28 and 14 x 14 un-pooled pairs gain (1.03-1.07x);
+        # the large planes lose (0.65-0.94x: one 128-thread block walks a whole plane in two
+        # serial phases) and the forward is 67.3 vs 65.6 ms (profiles/r2_smallc2.md)
+        self._workspace2 = None
+        self.use_fuse_next(False)
         self._conv_out = None  # pre-activation outputs, allocated on first keep_conv_out forward
         self.act = []
         for op, (C, K, h, w, pool) in zip(self.ops, self.shapes):
@@ -79,6 +88,25 @@ class ConvStack:
         self.smallc = [on and not op.tensor_core and self.fused_act and
                        lib.wino_smallc_supported(op.plan.handle, ctypes.byref(op.shape)) >= (2 if fast_only else 1)
                        for op in self.ops]
+        if hasattr(self, "fuse_next"):
+            self.use_fuse_next(self._fuse_on)
+        return self
+
+    def use_fuse_next(self, on: bool = True):
+        """Fuse K4 + activation of layer i with K1 of layer i + 1 where supported."""
+        lib = _native.lib()
+        self._fuse_on = on
+        self.fuse_next = []
+        for i, op in enumerate(self.ops):
+            ok = on and self.fused_act and i + 1 < len(self.ops) and not self.smallc[i] and bool(
+                lib.wino_output_input_supported(op.plan.handle, ctypes.byref(op.shape), 1 if self.shapes[i][4] else 0,
+                                                ctypes.byref(self.ops[i + 1].shape)))
+            self.fuse_next.append(ok)
+        for i, ok in enumerate(self.fuse_next):
+            if ok:
+                self.ops[i + 1].prepare(_native.PREPARE_K4K1)
+        if any(self.fuse_next) and self._workspace2 is None:
+            self._workspace2 = D.torch.empty(self.workspace.numel(), dtype=D.torch.uint8, device="cuda")
         return self
 
     @property
@@ -118,14 +146,19 @@ class ConvStack:
             return 4 * len(self.ops)
         return sum(2 if sc else 3 for sc in self.smallc)
 
-    def _uvm(self, L):
+    def _uvm(self, L, i=0):
         al = lambda v: (v + 255) // 256 * 256
-        U = self.workspace.data_ptr()
+        ws = self._workspace2 if (i & 1) and self._workspace2 is not None else self.workspace
+        U = ws.data_ptr()
         V = U + al(L.u_bytes)
         return U, V, V + al(L.v_bytes)
 
     def layer_forward(self, i, cur, stream=None, events=None, after_kernel=None):
         """Layer i on activation `cur` (fused path): K1+K2, K3, K4+ReLU(+pool) -> self.act[i].
+        Where fuse_next[i - 1] holds, layer i's V was already written by the previous layer's
+        K4+K1 kernel (only K2 runs here and `cur` is not read); where fuse_next[i] holds, the
+        last kernel is K4 + activation + K1 of layer i + 1 and the return value is None (the
+        activation only ever exists in shared memory).
         events: optional 4 CUDA events recorded before K1+K2, before K3, before K4, after K4.
         after_kernel: optional callable issued after each of the three kernels (profiling)."""
         hook = after_kernel if after_kernel is not None else (lambda: None)
@@ -134,11 +167,15 @@ class ConvStack:
         op = self.ops[i]
         pool = self.shapes[i][4]
         sh = ctypes.byref(op.shape)
-        U, V, M = self._uvm(op.layout)
+        U, V, M = self._uvm(op.layout, i)
         if events is not None:
             events[0].record()
-        _native.check(lib.wino_transforms(op.plan.handle, sh, D.ptr(cur), D.ptr(self.weights[i]),
-                                          ctypes.c_void_p(U), ctypes.c_void_p(V), s), f"layer {i + 1} K1/K2")
+        if i > 0 and self.fuse_next[i - 1]:
+            _native.check(lib.wino_filter_transform(op.plan.handle, sh, D.ptr(self.weights[i]), ctypes.c_void_p(U), s),
+                          f"layer {i + 1} K2")
+        else:
+            _native.check(lib.wino_transforms(op.plan.handle, sh, D.ptr(cur), D.ptr(self.weights[i]),
+                                              ctypes.c_void_p(U), ctypes.c_void_p(V), s), f"layer {i + 1} K1/K2")
         hook()
         if events is not None:
             events[1].record()
@@ -156,6 +193,16 @@ class ConvStack:
         hook()
         if events is not None:
             events[2].record()
+        if self.fuse_next[i]:  # K4 + ReLU (+ pool) + K1 of the next layer: writes the next layer's V
+            nxt = self.ops[i + 1]
+            _, V2, _ = self._uvm(nxt.layout, i + 1)
+            _native.check(lib.wino_output_input_transform(op.plan.handle, sh, ctypes.c_void_p(M), 1 if pool else 0,
+                                                          ctypes.byref(nxt.shape), ctypes.c_void_p(V2), s),
+                          f"layer {i + 1} K4+act+K1")
+            hook()
+            if events is not None:
+                events[3].record()
+            return None
         _native.check(lib.wino_output_transform_act(op.plan.handle, sh, ctypes.c_void_p(M),
                                                     D.ptr(self.act[i]), 1 if pool else 0, s),
                       f"layer {i + 1} K4+act")

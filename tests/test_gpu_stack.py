@@ -31,6 +31,10 @@ def test_small_vgg_like_stack_bitwise():
     assert st.smallc[0] and not any(st.smallc[1:])
     assert G.same_bits(st.forward(xt).cpu().numpy(), ref)
     st.use_smallc(False)
+    st.use_fuse_next(True)                                   # K4 + act + K1 of the next layer in one kernel
+    assert any(st.fuse_next)
+    assert G.same_bits(st.forward(xt).cpu().numpy(), ref)
+    st.use_fuse_next(False)
     out2 = st.forward(xt, keep_conv_out=True).cpu().numpy()  # unfused: y stored, wino_relu_pool
     for i, y in enumerate(ref_outs):
         assert G.same_bits(st.conv_out[i].cpu().numpy(), y), i
@@ -165,3 +169,41 @@ def test_stack_pipeline_host_buffers_bitwise(chunks):
         pipe(xh, yh)
         torch.cuda.synchronize()
         assert torch.equal(yh.view(torch.int32), want.view(torch.int32))
+
+
+@pytest.mark.parametrize("cs", ["linear", "pairwise"])
+def test_fused_output_input_transform_matches_k4_then_k1(cs):
+    """wino_output_input_transform (K4 of a layer + ReLU / max-pool + K1 of the next layer in one
+    kernel, the activation only in shared memory) writes the V that wino_output_transform_act
+    followed by wino_input_transform writes, bit for bit: partial edge tiles, odd sizes after
+    pooling, several planes per block, planes spanning several thread rounds, tile padding."""
+    import ctypes
+    from paper_1803_10986_b200 import _native
+    lib = _native.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    for m, pts in ((6, P8), (4, "0,1,-1,1/2,-1/2,inf"), (3, "0,1,-1,2,-2")):
+        ts = W.build_transforms(3, m, W.parse_points(pts))
+        for (N, C, K, H, Wd, K2) in [(3, 5, 16, 20, 26, 9), (7, 8, 64, 14, 14, 16), (2, 3, 32, 70, 52, 8)]:
+            for pool in ((0, 1) if m % 2 == 0 else (0,)):
+                cfg = W.ConvConfig("fp32", "huffman", cs)
+                op = W.layer_op(ts, cfg, N, C, H, Wd, K, 1)
+                Ho, Wo = op.layout.Ho, op.layout.Wo
+                H2, W2 = (Ho // 2, Wo // 2) if pool else (Ho, Wo)
+                nxt = W.layer_op(ts, cfg, N, K, H2, W2, K2, 1)
+                if not lib.wino_output_input_supported(op.plan.handle, ctypes.byref(op.shape), pool,
+                                                       ctypes.byref(nxt.shape)):
+                    assert nxt.layout.Cp != K, (m, N, C, K, H, Wd, pool)   # only padded channels may refuse
+                    continue
+                nxt.prepare(_native.PREPARE_K4K1)
+                x = torch.from_numpy(O.synthetic((N, C, H, Wd), 21, 0)).cuda()
+                w = torch.from_numpy(O.synthetic((K, C, 3, 3), 21, 1)).cuda()
+                M = op.contract(op.filter_transform(w), op.input_transform(x))
+                act = torch.empty((N, K, H2, W2), device="cuda")
+                _native.check(lib.wino_output_transform_act(op.plan.handle, ctypes.byref(op.shape), _native.as_ptr(M),
+                                                            _native.as_ptr(act), pool, s))
+                want = nxt.input_transform(act)
+                got = torch.full_like(want, 7.0)
+                _native.check(lib.wino_output_input_transform(op.plan.handle, ctypes.byref(op.shape), _native.as_ptr(M),
+                                                              pool, ctypes.byref(nxt.shape), _native.as_ptr(got), s))
+                torch.cuda.synchronize()
+                assert torch.equal(got.view(torch.int32), want.view(torch.int32)), (m, cs, N, C, K, H, Wd, pool)
