@@ -21,13 +21,16 @@ done
 # BASELINE configs[2] / configs[3] sweeps: one line per (m, points, order, precision, sum, input) cell
 python bench.py --config sweep_cfg3 --steps 10 --warmup 3 --no-cpu --soak 0.2 > gpurun_out/bench_sweep_cfg3.log 2>&1
 python bench.py --config sweep_cfg4 --steps 10 --warmup 3 --no-cpu --soak 0.2 > gpurun_out/bench_sweep_cfg4.log 2>&1
-# ncu: launch list of the default command, then --set full of one layer's three kernels (layer 9)
+# ncu: launch list of the default command, then --set full of one layer's three kernels (layer 9:
+# 3 warm-up forwards x 38 kernels + 2 of layer 1 + 7 layers x 3), then the fused layer-1 kernel
 python bench.py --ncu --steps 2 --warmup 3 > gpurun_out/b_small.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --ncu --steps 2 --warmup 3 > gpurun_out/ncu1.log 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"wino_contract|wino_transforms|wino_output" -s 141 -c 3 \
+    -k regex:"wino_contract|wino_transforms|wino_output|wino_smallc2" -s 137 -c 3 \
     -o gpurun_out/prof_bench python bench.py --ncu --steps 1 --warmup 3 > gpurun_out/ncu2.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"wino_smallc2" -s 3 -c 1 \
+    -o gpurun_out/prof_smallc2 python bench.py --ncu --steps 1 --warmup 3 > gpurun_out/ncu3.log 2>&1
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --cache-control none --clock-control none \
     --profile-from-start off --csv --log-file gpurun_out/traffic.csv python bench.py --traffic > gpurun_out/traffic_run.log 2>&1
 echo all done
