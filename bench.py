@@ -7,7 +7,8 @@ ReLU, 2x2 max-pools after layers 2/4/7/10), every layer through Winograd
 F(6x6,3x3) with the P8 points {0,-1,1,1/2,-1/2,2,-2,inf}, fp32, Huffman-ordered
 transforms, pairwise channel sums, exact contraction; global batch 256 of
 224x224x3 synthetic U[-1,1] images, He-normal filters (seeded Philox).
-A step = one 13-layer forward (39 libwino kernels, input resident in HBM).
+A step = one 13-layer forward (38 libwino kernels: layer 1 runs K1+K2 and a fused
+K3+K4+ReLU kernel, the other layers K1+K2, K3, K4+ReLU(+pool); input resident in HBM).
 Multi-GPU: one process per GPU (`--gpus N` re-execs under torch.distributed.run
 when no torchrun environment is set), the global batch sharded by images
 (strong scaling); NCCL only reduces timings.  `--impl reference` times the CPU

@@ -300,9 +300,11 @@ int64_t wino_launch_count(void);
 const char* wino_last_error(void);
 /* Tuning hooks for tools/ sweeps and variant tests (the product never sets them):
  * key "gemm" = contraction tile "tm,tn,thm,thn,bk,stages,maxreg[,ku,noprod,pack]"
- * (plans created afterwards), "dbuf", "tcf_nk" (same), "k1" = "tile", "k1order" =
+ * (plans created afterwards), "dbuf", "tcf_nk" (same), "k1" = "tile" | "gather" (K1 from
+ * global memory only) | "bulk<KB>" (shared-memory cap of the bulk-staged K1), "k1order" =
  * "t", "k4" = "staged", "k1tc" = "4x8", "tile_interp" = "0|1", "cpt" / "kpt" =
- * 1|2|4|8, "tcf_dbg", "tc_epi" (read once per process, before the first launch).
+ * 1|2|4|8, "tcf_dbg", "tc_epi", "k1rowwise" / "k4rowwise", "sc2_kg" (filter-pair warp groups
+ * of the small-C fused kernel), "k4k1_ks" (read once per process, before the first launch).
  * value NULL or "" clears the key.  Unknown keys -> WINO_EINVAL. */
 int wino_tuning_set(const char* key, const char* value);
 const char* wino_version(void);

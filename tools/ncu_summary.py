@@ -38,14 +38,14 @@ def launches(path):
         except ValueError:
             pass
     step = [k for k in agg if k.startswith("wino_")]
-    tot = sum(sum(agg[k]) / len(agg[k]) for k in step)
+    tot = sum(sum(agg[k]) for k in step)  # kernels launch a different number of times per step: total time
     print(f"# Launch list ({path}), ncu --metrics gpu__time_duration.sum --clock-control none\n")
     print("cold-cache, serialised per-launch times; compare shares, not absolutes\n")
-    print("| kernel | launches | mean us | share of the 4-kernel step |")
+    print("| kernel | launches | mean us | share of the libwino time (launches x mean) |")
     print("|---|---|---|---|")
     for k, v in agg.items():
         mean = sum(v) / len(v) / 1e3
-        share = f"{100 * mean * 1e3 / tot:.1f}%" if k in step else "-"
+        share = f"{100 * sum(v) / tot:.1f}%" if k in step else "-"
         print(f"| {k} | {len(v)} | {mean:.2f} | {share} |")
 
 
