@@ -17,12 +17,21 @@ struct Ref {
 
 class Emitter {
   public:
-    Emitter(std::ostringstream& os, bool dbl, int& counter) : os_(os), dbl_(dbl), ctr_(counter) {}
+    // packed: every value is an f32x2 pair (two independent problems, e.g. two filters) held in a
+    // 64-bit register; one add.rn.f32x2 / sub.rn.f32x2 per sum and fma.rn.f32x2(c, x, -0) per product
+    // (k2_mul; the -0 pair `nz2` is a kernel parameter so ptxas can neither fold it away nor fuse
+    // the product into the consuming sum -- the contraction kernel's exact packed product)
+    Emitter(std::ostringstream& os, bool dbl, int& counter, bool packed = false)
+        : os_(os), dbl_(dbl), packed_(packed), ctr_(counter) {}
 
-    const char* type() const { return dbl_ ? "double" : "float"; }
+    const char* type() const { return packed_ ? "unsigned long long" : dbl_ ? "double" : "float"; }
 
     std::string lit(double c) const {
         char buf[64];
+        if (packed_) {
+            std::snprintf(buf, sizeof buf, "k2_dup(%af)", c);
+            return buf;
+        }
         if (dbl_)
             std::snprintf(buf, sizeof buf, "(%a)", c);
         else
@@ -35,7 +44,7 @@ class Emitter {
     // +c and -c differ only in sign: fl(-c*x) == -fl(c*x) exactly, and the sign
     // is folded into the consuming add/sub).
     std::string row(const RowProg& p, const std::vector<std::string>& in) {
-        if (p.ops.empty()) return dbl_ ? "0.0" : "0.0f";
+        if (p.ops.empty()) return packed_ ? "0ull" : dbl_ ? "0.0" : "0.0f";
         std::vector<Ref> st;
         for (const wino_op& op : p.ops) {
             if (op.kind == WINO_OP_LEAF) {
@@ -70,7 +79,7 @@ class Emitter {
                 else if (!a.neg && b.neg)
                     e = sub(a.name, b.name);
                 else
-                    e = sub("(-" + a.name + ")", b.name);  // fl(-a + -b) == fl(-a - b)
+                    e = sub(neg(a.name), b.name);  // fl(-a + -b) == fl(-a - b)
                 std::string t = fresh();
                 os_ << "  const " << type() << " " << t << " = " << e << ";\n";
                 st.push_back({t, false});
@@ -79,7 +88,7 @@ class Emitter {
         Ref r = st.back();
         if (!r.neg) return r.name;
         std::string t = fresh();
-        os_ << "  const " << type() << " " << t << " = -" << r.name << ";\n";
+        os_ << "  const " << type() << " " << t << " = " << neg(r.name) << ";\n";
         return t;
     }
 
@@ -136,18 +145,24 @@ class Emitter {
 
   private:
     std::string fresh() { return "t" + std::to_string(ctr_++); }
+    std::string neg(const std::string& a) const {
+        return packed_ ? "(" + a + " ^ 0x8000000080000000ull)" : "(-" + a + ")";
+    }
     std::string mul(const std::string& a, const std::string& b) const {
+        if (packed_) return "k2_mul(" + a + ", " + b + ", nz2)";
         return std::string(dbl_ ? "__dmul_rn(" : "__fmul_rn(") + a + ", " + b + ")";
     }
     std::string add(const std::string& a, const std::string& b) const {
+        if (packed_) return "k2_add(" + a + ", " + b + ")";
         return std::string(dbl_ ? "__dadd_rn(" : "__fadd_rn(") + a + ", " + b + ")";
     }
     std::string sub(const std::string& a, const std::string& b) const {
+        if (packed_) return "k2_sub(" + a + ", " + b + ")";
         return std::string(dbl_ ? "__dsub_rn(" : "__fsub_rn(") + a + ", " + b + ")";
     }
 
     std::ostringstream& os_;
-    bool dbl_;
+    bool dbl_, packed_;
     int& ctr_;
     std::map<std::string, std::string> products_;  // "x*|c|" -> SSA name (per emitter)
 };
@@ -971,18 +986,31 @@ static void emit_smallc2(std::ostringstream& os, int r, int m, const MatProg& AT
     const int n = r + m - 1, P = n * n, KG = smallc2_kg();
     if (bn % 32 || bm % 4 || bn * KG > 1024) return;
     const bool even = m % 2 == 0;
-    os << "template <int C, int PW>\n"
-          "static __device__ __forceinline__ float sc2_dot(float u0, float u1, float u2, float u3, float v0, float v1,\n"
-          "                                                float v2, float v3) {\n"
-          "  const float z0 = __fmul_rn(u0, v0);\n"
+    // packed f32x2 helpers: lane 0 = filter 2kp, lane 1 = filter 2kp + 1 (the same arithmetic on two
+    // independent filters; every product and every sum still rounds once, see Emitter `packed`)
+    os << "typedef unsigned long long k2_t;\n"
+          "static __device__ __forceinline__ k2_t k2_mul(k2_t a, k2_t b, k2_t nz2) {\n"
+          "  k2_t r;\n  asm(\"fma.rn.f32x2 %0, %1, %2, %3;\" : \"=l\"(r) : \"l\"(a), \"l\"(b), \"l\"(nz2));\n  return r;\n}\n"
+          "static __device__ __forceinline__ k2_t k2_add(k2_t a, k2_t b) {\n"
+          "  k2_t r;\n  asm(\"add.rn.f32x2 %0, %1, %2;\" : \"=l\"(r) : \"l\"(a), \"l\"(b));\n  return r;\n}\n"
+          "static __device__ __forceinline__ k2_t k2_sub(k2_t a, k2_t b) {\n"
+          "  k2_t r;\n  asm(\"sub.rn.f32x2 %0, %1, %2;\" : \"=l\"(r) : \"l\"(a), \"l\"(b));\n  return r;\n}\n"
+          "static __device__ __forceinline__ k2_t k2_dup(float a) {\n"
+          "  k2_t r;\n  asm(\"mov.b64 %0, {%1, %1};\" : \"=l\"(r) : \"f\"(a));\n  return r;\n}\n"
+          "static __device__ __forceinline__ float k2_lo(k2_t a) { return __uint_as_float((unsigned)a); }\n"
+          "static __device__ __forceinline__ float k2_hi(k2_t a) { return __uint_as_float((unsigned)(a >> 32)); }\n"
+          "template <int C, int PW>\n"
+          "static __device__ __forceinline__ k2_t sc2_dot(k2_t u0, k2_t u1, k2_t u2, k2_t u3, float v0, float v1,\n"
+          "                                               float v2, float v3, k2_t nz2) {\n"
+          "  const k2_t z0 = k2_mul(u0, k2_dup(v0), nz2);\n"
           "  if constexpr (C == 1) return z0;\n"
-          "  const float z1 = __fmul_rn(u1, v1);\n"
-          "  if constexpr (C == 2) return __fadd_rn(z0, z1);\n"
-          "  const float z2 = __fmul_rn(u2, v2);\n"
-          "  if constexpr (C == 3) return __fadd_rn(__fadd_rn(z0, z1), z2);\n"
-          "  const float z3 = __fmul_rn(u3, v3);\n"
-          "  if constexpr (PW) return __fadd_rn(__fadd_rn(z0, z1), __fadd_rn(z2, z3));\n"
-          "  return __fadd_rn(__fadd_rn(__fadd_rn(z0, z1), z2), z3);\n"
+          "  const k2_t z1 = k2_mul(u1, k2_dup(v1), nz2);\n"
+          "  if constexpr (C == 2) return k2_add(z0, z1);\n"
+          "  const k2_t z2 = k2_mul(u2, k2_dup(v2), nz2);\n"
+          "  if constexpr (C == 3) return k2_add(k2_add(z0, z1), z2);\n"
+          "  const k2_t z3 = k2_mul(u3, k2_dup(v3), nz2);\n"
+          "  if constexpr (PW) return k2_add(k2_add(z0, z1), k2_add(z2, z3));\n"
+          "  return k2_add(k2_add(k2_add(z0, z1), z2), z3);\n"
           "}\n";
     auto val = [&](int a, int b) { return "y" + std::to_string(a) + "_" + std::to_string(b); };
     // Store of one (tile, filter) result y[a][b] (registers).  MODE 0: y, 1: ReLU, 2: ReLU of the 2x2
@@ -1053,7 +1081,7 @@ static void emit_smallc2(std::ostringstream& os, int r, int m, const MatProg& AT
     os << "template <int C, int PW, int MODE>\n"
           "static __device__ __forceinline__ void sc2_body(const float* __restrict__ U, const float* __restrict__ V,\n"
           "    float* __restrict__ out, int K, int Ho, int Wo, int th, int tw, long long T, long long Tp, long long Kp,\n"
-          "    long long Cp) {\n"
+          "    long long Cp, k2_t nz2) {\n"
        << "  constexpr int N1 = " << n << ", P = " << P << ", M = " << m << ", BM = " << bm << ", BN = " << bn
        << ", KG = " << KG << ", HP = " << (even ? m / 2 : 1) << ";\n"
           "  extern __shared__ __align__(16) unsigned char smem_raw[];\n"
@@ -1122,49 +1150,43 @@ static void emit_smallc2(std::ostringstream& os, int r, int m, const MatProg& AT
           "#pragma unroll 1\n"
           "  for (int kp = kg; 2 * kp < K; kp += KG) {\n"
           "    const float* up = sU + ((2 * kp) / BM) * C * BM + ((2 * kp) % BM);\n";
-    Emitter em(os, false, ctr);
-    std::vector<std::vector<std::string>> leftA(AT.rows, std::vector<std::string>(n)), leftB = leftA;
+    Emitter em(os, false, ctr, /*packed=*/true);
+    std::vector<std::vector<std::string>> left(AT.rows, std::vector<std::string>(n));
     for (int b = 0; b < n; ++b) {
-        std::vector<std::string> colA(n), colB(n);
+        std::vector<std::string> col(n);
         os << "    if (first) sc2_wait(&bar[" << b << "]);\n";
         for (int a = 0; a < n; ++a) {
             const int p = a * n + b;
             const std::string s = std::to_string(a) + "_" + std::to_string(b);
-            colA[a] = "ma" + s;
-            colB[a] = "mb" + s;
-            os << "    const float2 ua" << s << " = *reinterpret_cast<const float2*>(up + " << p << " * us);\n"
-               << "    const float2 ub" << s << " = C > 1 ? *reinterpret_cast<const float2*>(up + " << p << " * us + BM) : make_float2(0.f, 0.f);\n"
-               << "    const float2 uc" << s << " = C > 2 ? *reinterpret_cast<const float2*>(up + " << p << " * us + 2 * BM) : make_float2(0.f, 0.f);\n"
-               << "    const float2 ud" << s << " = C > 3 ? *reinterpret_cast<const float2*>(up + " << p << " * us + 3 * BM) : make_float2(0.f, 0.f);\n"
+            col[a] = "mm" + s;
+            os << "    const k2_t ua" << s << " = *reinterpret_cast<const k2_t*>(up + " << p << " * us);\n"
+               << "    const k2_t ub" << s << " = C > 1 ? *reinterpret_cast<const k2_t*>(up + " << p << " * us + BM) : 0ull;\n"
+               << "    const k2_t uc" << s << " = C > 2 ? *reinterpret_cast<const k2_t*>(up + " << p << " * us + 2 * BM) : 0ull;\n"
+               << "    const k2_t ud" << s << " = C > 3 ? *reinterpret_cast<const k2_t*>(up + " << p << " * us + 3 * BM) : 0ull;\n"
                << "    const float va" << s << " = vp[" << p << " * C * BN];\n"
                << "    const float vb" << s << " = C > 1 ? vp[(" << p << " * C + 1) * BN] : 0.f;\n"
                << "    const float vc" << s << " = C > 2 ? vp[(" << p << " * C + 2) * BN] : 0.f;\n"
                << "    const float vd" << s << " = C > 3 ? vp[(" << p << " * C + 3) * BN] : 0.f;\n"
-               << "    const float " << colA[a] << " = sc2_dot<C, PW>(ua" << s << ".x, ub" << s << ".x, uc" << s << ".x, ud"
-               << s << ".x, va" << s << ", vb" << s << ", vc" << s << ", vd" << s << ");\n"
-               << "    const float " << colB[a] << " = sc2_dot<C, PW>(ua" << s << ".y, ub" << s << ".y, uc" << s << ".y, ud"
-               << s << ".y, va" << s << ", vb" << s << ", vc" << s << ", vd" << s << ");\n";
+               << "    const k2_t " << col[a] << " = sc2_dot<C, PW>(ua" << s << ", ub" << s << ", uc" << s << ", ud" << s
+               << ", va" << s << ", vb" << s << ", vc" << s << ", vd" << s << ", nz2);\n";
             // keep the shared-memory loads of later points behind the sums of these (ptxas would hoist
             // all 64 points' operands and spill)
             if ((a + 1) % 2 == 0) os << "    asm volatile(\"\" ::: \"memory\");\n";
         }
-        auto ra = em.apply(AT, colA);
-        auto rb = em.apply(AT, colB);
-        for (int i = 0; i < AT.rows; ++i) {
-            leftA[i][b] = ra[i];
-            leftB[i][b] = rb[i];
-        }
+        auto rr = em.apply(AT, col);
+        for (int i = 0; i < AT.rows; ++i) left[i][b] = rr[i];
     }
-    for (int half = 0; half < 2; ++half) {
-        auto& left = half ? leftB : leftA;
+    {
         std::vector<std::vector<std::string>> yv(AT.rows);
         for (int i = 0; i < AT.rows; ++i) yv[i] = em.apply(AT, left[i]);
-        os << "    " << (half ? "if (2 * kp + 1 < K) " : "")
-           << "sc2_store<MODE>(out, coop, live, wbuf, lane, soff, sy0, img, K, 2 * kp + " << half
-           << ", Ho, Wo, y0, x0";
-        for (int a = 0; a < m; ++a)
-            for (int b = 0; b < m; ++b) os << ", " << yv[a][b];
-        os << ");\n";
+        for (int half = 0; half < 2; ++half) {
+            os << "    " << (half ? "if (2 * kp + 1 < K) " : "")
+               << "sc2_store<MODE>(out, coop, live, wbuf, lane, soff, sy0, img, K, 2 * kp + " << half
+               << ", Ho, Wo, y0, x0";
+            for (int a = 0; a < m; ++a)
+                for (int b = 0; b < m; ++b) os << ", " << (half ? "k2_hi(" : "k2_lo(") << yv[a][b] << ")";
+            os << ");\n";
+        }
     }
     os << "    first = false;\n  }\n}\n";
     for (int C = 1; C <= 4; ++C)
@@ -1173,9 +1195,10 @@ static void emit_smallc2(std::ostringstream& os, int r, int m, const MatProg& AT
                 os << "extern \"C\" __global__ void __launch_bounds__(" << bn * KG << ", 1) wino_smallc2_c" << C
                    << (pw ? "p" : "l") << "_m" << mode
                    << "(\n    const float* __restrict__ U, const float* __restrict__ V, float* __restrict__ out, int K,\n"
-                      "    int Ho, int Wo, int th, int tw, long long T, long long Tp, long long Kp, long long Cp) {\n"
+                      "    int Ho, int Wo, int th, int tw, long long T, long long Tp, long long Kp, long long Cp,\n"
+                      "    unsigned long long nz2) {\n"
                    << "  sc2_body<" << C << ", " << pw << ", " << mode
-                   << ">(U, V, out, K, Ho, Wo, th, tw, T, Tp, Kp, Cp);\n}\n";
+                   << ">(U, V, out, K, Ho, Wo, th, tw, T, Tp, Kp, Cp, nz2);\n}\n";
     os << "\n";
 }
 

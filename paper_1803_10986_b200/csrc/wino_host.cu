@@ -1438,7 +1438,8 @@ int wino_contract_output_smallc(wino_plan* plan, const wino_layer_shape* s, cons
             CUresult cr = wino::driver().FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
             if (cr != CUDA_SUCCESS) return wino::fail(WINO_ECUDA, "contract_output_smallc: set smem: " + wino::cu_err(cr));
         }
-        void* args[] = {(void*)&U, (void*)&V, &out, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp, &Cp};
+        unsigned long long nz2 = 0x8000000080000000ull;  // (-0, -0): exact packed products (codegen.cpp k2_mul)
+        void* args[] = {(void*)&U, (void*)&V, &out, &K, &Ho, &Wo, &th, &tw, &T, &Tp, &Kp, &Cp, &nz2};
         return wino::launch(f, dim3((unsigned)nb), dim3((unsigned)(bn * smallc2_kg())), smem, stream, args,
                             "contract_output_smallc");
     }

@@ -69,15 +69,52 @@ FFMA2_LINE = re.compile(r"\bFFMA2\s+([^;]*);")
 
 def _fused_ops(sass: str) -> list:
     """Instructions that would fuse a multiply into a per-thread sum.  FFMA/DFMA
-    always do.  FFMA2 is allowed only with a uniform-register or constant-bank
-    addend: that is the packed exact product fma.rn.f32x2(a, b, -0) ==
-    fl(a*b) of contract_template.cuh (accumulators are per-thread registers,
-    never uniform)."""
+    always do.  FFMA2 is allowed only as the packed exact product
+    fma.rn.f32x2(a, b, -0) == fl(a*b) (contract_template.cuh, codegen.cpp k2_mul), whose
+    addend is the (-0, -0) kernel parameter: a uniform register or constant-bank operand,
+    or -- e.g. when another product in the kernel takes an immediate multiplier, which
+    leaves no slot for a second special operand -- a register pair that the function only
+    ever loads from the parameter bank (LDC.64 Rn, c[0x0][..]) and never writes otherwise.
+    Accumulators are per-thread registers written by arithmetic, so a fused sum fails
+    both tests."""
     bad = [m.group(0) for m in re.finditer(r"\b(FFMA|DFMA)\b(?!2)[^;]*;", sass)]
-    for m in FFMA2_LINE.finditer(sass):
-        ops = [o.strip() for o in m.group(1).split(",")]
-        if len(ops) != 4 or not re.match(r"^(UR\d+|c\[0x[0-9a-f]+\]\[0x[0-9a-f]+\])", ops[3]):
-            bad.append(m.group(0))
+    nodest = ("STG", "STS", "ST", "STL", "RED", "ATOMS", "BAR", "BRA", "EXIT", "ISETP", "FSETP")
+    for fn in re.split(r"\n\s*Function : ", sass):
+        # program-order list of (position, opcode, registers written); destination = first operand
+        writes, uses = [], []
+        for m in re.finditer(r"(?:@!?U?P\d+\s+)?\b([A-Z][A-Z0-9_]*(?:\.[A-Za-z0-9_]+)*)\s+([^;/]*);", fn):
+            op, body = m.group(1), m.group(2)
+            base = op.split(".")[0]
+            d = re.match(r"R(\d+)\b", body)
+            if d and base not in nodest:
+                r = int(d.group(1))
+                wide = 4 if ".128" in op else 2 if (".64" in op or ".WIDE" in op or base in
+                                                     ("FFMA2", "FADD2", "FMUL2", "DADD", "DMUL", "DFMA")) else 1
+                writes.append((m.start(), op, set(range(r, r + wide))))
+            if base == "FFMA2":
+                uses.append((m.start(), m.group(0), [o.strip() for o in body.split(",")]))
+        by_reg = {}
+        for pos, text, ops in uses:
+            if len(ops) == 4 and re.match(r"^(UR\d+|c\[0x[0-9a-f]+\]\[0x[0-9a-f]+\])", ops[3]):
+                continue
+            mr = re.match(r"^R(\d+)\b", ops[3]) if len(ops) == 4 else None
+            if not mr:
+                bad.append(text)
+                continue
+            by_reg.setdefault(int(mr.group(1)), []).append((pos, text))
+        for n, lst in by_reg.items():
+            pair = {n, n + 1}
+            first, last = lst[0][0], lst[-1][0]
+            before = [w for w in writes if w[0] < first and w[2] & pair]
+            # the definition reaching the first use must be a parameter load covering the pair (or one
+            # load per half), and nothing may write the pair while the products that use it run
+            reach = {}
+            for w in before:
+                for q in w[2] & pair:
+                    reach[q] = w[1]
+            inside = [w for w in writes if first <= w[0] <= last and w[2] & pair and not w[1].startswith("LDC")]
+            if set(reach) != pair or not all(o.startswith("LDC") for o in reach.values()) or inside:
+                bad.extend(t for _, t in lst)
     return bad
 
 
@@ -129,6 +166,12 @@ def test_sass_gate_rejects_fused_sums():
     assert _fused_ops("FFMA2 R16, R25.F32, R32.F32x2.HI_LO, R8.F32x2.HI_LO ;")
     assert _fused_ops("DFMA R2, R4, R6, R8 ;")
     assert not _fused_ops("FFMA2 R16, R25.F32, R32.F32x2.HI_LO, UR8.F32x2.HI_LO ;")
+    ldc = "        /*0100*/                   LDC.64 R2, c[0x0][0x390] ;\n"
+    imm = "        /*01d0*/                   FFMA2 R4, R4.F32x2.HI_LO, 0.5, R2.F32x2.HI_LO ;\n"
+    assert not _fused_ops(ldc + imm)                                   # immediate multiplier, -0 parameter addend
+    assert _fused_ops(imm)                                             # addend of unknown origin
+    assert _fused_ops(ldc + "        /*0110*/                   FADD2 R2, R6.F32x2.HI_LO, R8.F32x2.HI_LO ;\n" + imm)
+    assert _fused_ops(ldc + "        /*0110*/                   LDS.128 R0, [R9] ;\n" + imm)  # R2 rewritten by a wide load
     assert not _fused_ops("FMUL R1, R2, R3 ; FADD2 R4, R6.F32x2.HI_LO, R8.F32x2.HI_LO ; HFMA2 R5, -RZ, RZ, 0, 0 ;")
 
 
