@@ -61,7 +61,7 @@ class ConvStack:
         self.out_hw = (h, w)
         # small-C layers (VGG-16 layer 1, C = 3) run K3 + K4 + activation in one kernel (M -- 6 GB
         # at batch 256 -- never stored, wino_contract_output_smallc) where the fast variant applies
-        # (wino_smallc_supported == 2: 1.63 vs 2.73 ms at VGG layer 1)
+        # (wino_smallc_supported == 2: 1.43 vs 2.73 ms at VGG layer 1)
         self._fuse_on = False
         self.use_smallc(True, fast_only=True)
         ws = max(op.layout.workspace_bytes for op in self.ops)
