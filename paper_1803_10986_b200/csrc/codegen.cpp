@@ -517,8 +517,22 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
     // spill); tuning key k1rowwise = 2..6 selects another bound (0: row-wise off)
     const int rw_blocks = std::atoi(tuning("k1rowwise").c_str()) >= 2 ? std::atoi(tuning("k1rowwise").c_str()) : 3;
     const std::string lb = rowwise ? std::to_string(TB) + ", " + std::to_string(rw_blocks * 128 / TB) : std::to_string(TB);
+    // bulk-staged variants: tuning key "k1st_blocks" = minimum blocks per SM (register cap), default none
+    // minimum blocks per SM = register cap.  alpha = 8: 6 blocks (<= 85 registers, a few spilled values)
+    // beat the unconstrained 106 registers / 4 blocks on every VGG-16 layer -- bulk-staged K1 at 14 x 14
+    // 103.1 -> 98.8 us, 28 x 28 246 -> 231, 56 x 56 456 -> 420; global gather at 112 x 112 865 -> 832,
+    // 224 x 224 1665 -> 1626 (7 and 8 blocks spill too much: 56 x 56 547 / 759 us); alpha = 4 loses
+    // (cfg2 15.0 -> 16.8 us), so only P = 64 gets the bound (tools/sweeps/sweep_k1st_blocks.sh)
+    auto blocks_of = [&](const char* key) {
+        const std::string e = tuning(key);
+        return e.empty() ? (P == 64 ? 6 : 0) : std::atoi(e.c_str());
+    };
+    const int st_blocks = blocks_of("k1st_blocks"), pl_blocks = blocks_of("k1_blocks");
+    const std::string lb_plain = lb;
     for (int st = 0; st < 2; ++st) {
         const std::string sfx = st ? "_st" : "", tp = st ? "<true>" : "<false>";
+        const int nb = st ? st_blocks : pl_blocks;
+        const std::string lb = !rowwise && nb > 0 ? std::to_string(TB) + ", " + std::to_string(nb) : lb_plain;
         os << "extern \"C\" __global__ void __launch_bounds__(" << lb << ") wino_input_gather" << sfx << "(\n"
               "    const in_t* __restrict__ x, uv_t* __restrict__ V, int C, int H, int W, int pad, int th,\n"
               "    int tw, long long T, long long Tp, long long Cp, int Wl, float rtw, float rth) {\n"
@@ -555,7 +569,9 @@ static void emit_output_gather(std::ostringstream& os, int r, int m, const MatPr
     const bool rowwise = ty.compute_double && !ty.uv_double && std::string(mt) == "uv_t" && n >= 6 &&
                          tuning("k4rowwise") != "0";
     const int rw_blocks = std::atoi(tuning("k4rowwise").c_str()) >= 2 ? std::atoi(tuning("k4rowwise").c_str()) : 3;  // cfg3 mixed K4 65.8 -> 47.2 us at 2..4 blocks, 61.5 at 5 (spills)
-    os << "extern \"C\" __global__ void __launch_bounds__(" << TB << (rowwise ? ", " + std::to_string(rw_blocks) : std::string())
+    os << "extern \"C\" __global__ void __launch_bounds__(" << TB
+       << (rowwise ? ", " + std::to_string(rw_blocks)
+                   : std::atoi(tuning("k4_blocks").c_str()) > 0 ? ", " + tuning("k4_blocks") : std::string())
        << ") wino_output_gather(\n"
           "    const " << mt << "* __restrict__ Mm, y_t* __restrict__ y, int K, int Ho, int Wo, int th, int tw,\n"
           "    long long T, long long Tp, long long Kp, float rtw, float rth) {\n"
@@ -638,7 +654,9 @@ static void emit_output_gather_act(std::ostringstream& os, int r, int m, const M
                                    int TB, int& ctr) {
     const int n = r + m - 1;
     os << "static __device__ __forceinline__ float wino_relu(float v) { return v > 0.f ? v : 0.f; }\n"
-          "extern \"C\" __global__ void __launch_bounds__(" << TB << ") wino_output_gather_act(\n"
+          "extern \"C\" __global__ void __launch_bounds__(" << TB
+       << (std::atoi(tuning("k4_blocks").c_str()) > 0 ? ", " + tuning("k4_blocks") : std::string())
+       << ") wino_output_gather_act(\n"
           "    const uv_t* __restrict__ Mm, float* __restrict__ act, int K, int Ho, int Wo, int th, int tw,\n"
           "    long long T, long long Tp, long long Kp, float rtw, float rth, int pool) {\n"
        << "  const int t0 = blockIdx.x * " << TB << ";\n"

@@ -743,7 +743,7 @@ const char* wino_last_error(void) { return wino::g_last_error.c_str(); }
 
 int wino_tuning_set(const char* key, const char* value) {
     static const char* const keys[] = {"gemm", "dbuf", "k1", "k1order", "k4", "k1tc", "tile_interp",
-                                       "cpt", "kpt", "tcf_nk", "tcf_dbg", "tc_epi", "k1rowwise", "k4rowwise", "sc2_kg", "k4k1_ks"};
+                                       "cpt", "kpt", "tcf_nk", "tcf_dbg", "tc_epi", "k1rowwise", "k4rowwise", "sc2_kg", "k4k1_ks", "k1st_blocks", "k1_blocks", "k4_blocks"};
     if (!key) return wino::fail(WINO_EINVAL, "tuning_set: null key");
     bool known = false;
     for (const char* k : keys) known = known || std::strcmp(k, key) == 0;
