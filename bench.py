@@ -191,12 +191,24 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def contraction_note(mode):
+    """What a non-exact contraction mode means for parity (stated on every such line)."""
+    if mode == "exact":
+        return "reference arithmetic: one rounded product and one rounded sum per channel term, bit-identical"
+    if mode == "ffma":
+        return ("NOT reference arithmetic: fused multiply-add in the channel sum; against the exact output it differs "
+                "by 9-127 ulp-scaled units at p99 depending on the config (tests/test_gpu_ffma.py), above "
+                "north_star's 4-ulp example; error_vs_fp64 is this mode's own")
+    return ("NOT reference arithmetic: U and V rounded to 16 bits, tensor-core FP32 accumulation; error_vs_fp64 is "
+            "this mode's own (tc_bf16 at F(6,3): rel. L1 3.9e-2, not a usable Winograd result)")
+
+
 def config_dict(args, cfg, world=1):
     r, m, pts, N, C, K, H, pad, xd, wi, prec, order, cs = cfg
     return {"workload": args.config, "winograd": f"F({m}x{m},{r}x{r})", "points": pts, "N_per_gpu": N,
             "global_batch": N * world, "C": C, "K": K, "H": H, "W": H, "pad": pad, "precision": prec,
             "dot_order": order, "channel_sum": cs, "contraction": args.contraction,
-            "x_dist": xd, "w_init": wi, "l2": "flushed between timed steps: 256 MiB write, then 256 MiB read of a clean buffer "
+            "contraction_note": contraction_note(args.contraction), "x_dist": xd, "w_init": wi, "l2": "flushed between timed steps: 256 MiB write, then 256 MiB read of a clean buffer "
                   "(no step data and no dirty lines left in L2)",
             "parallelism": f"dp{world} (independent batches per GPU)"}
 
@@ -469,7 +481,8 @@ def vgg_config(args, n_per_gpu, world):
     return {"workload": "vgg16", "model": "VGG-16 conv stack (13 conv layers, ReLU, 4 max-pools; no FC head)",
             "winograd": "F(6x6,3x3)", "points": VGG_POINTS, "global_batch": args.vgg_batch,
             "batch_per_gpu": n_per_gpu, "image": [3, 224, 224], "precision": "fp32", "dot_order": "huffman",
-            "channel_sum": "pairwise", "contraction": args.contraction, "layers": 13, "pools_after": [2, 4, 7, 10],
+            "channel_sum": "pairwise", "contraction": args.contraction,
+            "contraction_note": contraction_note(args.contraction), "layers": 13, "pools_after": [2, 4, 7, 10],
             "l2": "no flush needed: inputs and activations >> 126 MB L2 (layer-1 x 154 MB, M 6 GB)",
             "parallelism": f"dp{world} (global batch sharded by images)"}
 

@@ -27,7 +27,7 @@ def jobs(which):
     from paper_1803_10986_b200.stack import VGG16
     out = []
     if "vgg16" in which:
-        for n in (256, 64, 2):
+        for n in (256, 192, 128, 64, 32, 2):  # batch, e2e chunks (32, 192, 32), per-rank shards, the CPU slice
             h = 224
             for C, K, pool in VGG16:
                 out.append((3, 6, bench.VGG_POINTS, "fp32", "huffman", "pairwise", "exact", n, C, h, K, 1, 3))
