@@ -87,3 +87,28 @@ def test_interpreted_tile_transforms_pass_the_tile_goldens():
                         "-x", "-k", "golden"], env=env, cwd=os.path.dirname(here), capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0, r.stdout[-3000:]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "mixed"])
+def test_bulk_staged_k1_equals_global_gather(prec):
+    """K1 from bulk-copied image planes in shared memory (the default where the planes of a block
+    fit) writes the V that the global-memory gather writes, bit for bit, padding included:
+    several planes per block, partial edge tiles, padded channels and tiles, alpha = 4 and 8."""
+    import torch
+    import paper_1803_10986_b200 as W
+    from paper_1803_10986_b200 import _native
+    from oracle import wino_oracle as O
+    try:
+        for m, pts in ((6, "0,-1,1,1/2,-1/2,2,-2,inf"), (2, "0,1,-1,inf")):
+            ts = W.build_transforms(3, m, W.parse_points(pts))
+            for (N, C, H, Wd, K) in [(5, 6, 14, 14, 8), (3, 70, 28, 28, 16), (2, 9, 20, 24, 8), (17, 3, 8, 8, 4)]:
+                op = W.layer_op(ts, W.ConvConfig(prec, "huffman", "pairwise"), N, C, H, Wd, K, 1)
+                x = torch.from_numpy(O.synthetic((N, C, H, Wd), 33, C)).cuda()
+                _native.set_tuning("k1", "gather")
+                want = op.input_transform(x)
+                _native.set_tuning("k1", None)
+                got = op.input_transform(x)
+                torch.cuda.synchronize()
+                assert torch.equal(got.view(torch.int32), want.view(torch.int32)), (prec, m, N, C, H, Wd)
+    finally:
+        _native.set_tuning("k1", None)
