@@ -159,6 +159,13 @@ int wino_input_transform(wino_plan* plan, const wino_layer_shape* s, const void*
 /* K1 + K2 in one launch (the filter transform's blocks ride along) */
 int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w,
                     void* U, void* V, void* stream);
+/* wino_transforms for a layer whose contraction is wino_contract_output_smallc (shapes with
+ * wino_smallc_supported() == 2): the same U and the same values in V's C real channel rows, but
+ * the rows that pad C up to the contraction's channel stage are left unwritten -- that kernel
+ * never reads them (VGG-16 layer 1: 5 of 8 rows, 473 MB per batch of 256).  V is NOT valid input
+ * for wino_contract. */
+int wino_transforms_smallc(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w,
+                           void* U, void* V, void* stream);
 /* K3: M_p = sum_c U_p[c] * V_p[c] for the alpha^2 points, channel order
  * linear or pairwise (halving tree) -- engine.py:415, 252-278, 336-338 */
 int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, const void* V,

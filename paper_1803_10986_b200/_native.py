@@ -60,6 +60,7 @@ SIGNATURES = [
     ("wino_contract", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_void_p]),
     ("wino_output_transform", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p]),
     ("wino_output_transform_act", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_int, c_void_p]),
+    ("wino_transforms_smallc", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("wino_output_input_supported", c_int, [c_void_p, POINTER(LayerShape), c_int, POINTER(LayerShape)]),
     ("wino_output_input_transform", c_int, [c_void_p, POINTER(LayerShape), c_void_p, c_int, POINTER(LayerShape),
                                             c_void_p, c_void_p]),

@@ -544,6 +544,7 @@ static void emit_input_gather(std::ostringstream& os, int r, int m, const MatPro
               "    int tw, long long T, long long Tp, long long Cp, int n_tb,\n"
               "    const in_t* __restrict__ w, uv_t* __restrict__ U, int K, long long Kp, int Wl, float rtw, float rth) {\n"
               "  if ((int)blockIdx.y < n_tb) {\n"
+           << "    if (Wl && (int)blockIdx.x * " << gather_cpt(P) << " >= C) return;  // consumer reads the C real rows only\n"
            << "    input_gather_body" << tp << "(x, V, C, H, W, pad, th, tw, T, Tp, Cp, rtw, rth, blockIdx.y * " << TB
            << ", blockIdx.x);\n"
            << "  } else {\n"

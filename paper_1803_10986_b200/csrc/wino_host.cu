@@ -994,8 +994,23 @@ int wino_filter_transform(wino_plan* plan, const wino_layer_shape* s, const void
     return wino::launch(f, dim3(cdiv(Kp, tb), (unsigned)Cp, 1), dim3(tb), 0, stream, args, "filter_transform");
 }
 
+static int transforms_impl(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w, void* U, void* V,
+                           void* stream, bool skip_pad);
+
 int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w, void* U, void* V,
                     void* stream) {
+    return transforms_impl(plan, s, x, w, U, V, stream, false);
+}
+
+int wino_transforms_smallc(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w, void* U, void* V,
+                           void* stream) {
+    if (wino_smallc_supported(plan, s) != 2)
+        return wino::fail(WINO_EUNSUPPORTED, "transforms_smallc: the fast small-C kernel does not apply to this shape");
+    return transforms_impl(plan, s, x, w, U, V, stream, true);
+}
+
+static int transforms_impl(wino_plan* plan, const wino_layer_shape* s, const void* x, const void* w, void* U, void* V,
+                           void* stream, bool skip_pad) {
     wino_layer_layout L;
     int rc = layout_of(plan, s, &L);
     if (rc) return rc;
@@ -1012,7 +1027,7 @@ int wino_transforms(wino_plan* plan, const wino_layer_shape* s, const void* x, c
     int n_tb = (int)cdiv(Tp, tb), n_kb = (int)cdiv(Kp, tb);
     const long long blocks = (long long)n_tb * (tc ? Cp / 8 : Cp) + (long long)n_kb * Cp;
     if (blocks >= (1LL << 31)) return wino::fail(WINO_EUNSUPPORTED, "transforms: grid too large");
-    int cfast = k1_cfast(), Wl = 0;
+    int cfast = k1_cfast(), Wl = skip_pad ? 1 : 0;  // gather kernels: 1 = leave V's padded channel rows unwritten
     if (tc && (k1_gather() || plan->fused()) && Cp / 8 <= 65535 && L.P <= 16 && !k1_no8()) {
         CUfunction fg;
         if ((rc = plan->layer_mod(plan->pick(s))->function("wino_transforms_tcg8", &fg))) return rc;

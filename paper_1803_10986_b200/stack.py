@@ -85,9 +85,10 @@ class ConvStack:
         """Route qualifying small-C layers through the fused K3 + K4 + activation kernel
         (fast_only: only where libwino reports the faster-than-unfused variant)."""
         lib = _native.lib()
-        self.smallc = [on and not op.tensor_core and self.fused_act and
-                       lib.wino_smallc_supported(op.plan.handle, ctypes.byref(op.shape)) >= (2 if fast_only else 1)
-                       for op in self.ops]
+        sup = [0 if op.tensor_core else lib.wino_smallc_supported(op.plan.handle, ctypes.byref(op.shape))
+               for op in self.ops]
+        self._smallc_fast = [v == 2 for v in sup]
+        self.smallc = [on and self.fused_act and v >= (2 if fast_only else 1) for v in sup]
         if hasattr(self, "fuse_next"):
             self.use_fuse_next(self._fuse_on)
         return self
@@ -174,8 +175,10 @@ class ConvStack:
             _native.check(lib.wino_filter_transform(op.plan.handle, sh, D.ptr(self.weights[i]), ctypes.c_void_p(U), s),
                           f"layer {i + 1} K2")
         else:
-            _native.check(lib.wino_transforms(op.plan.handle, sh, D.ptr(cur), D.ptr(self.weights[i]),
-                                              ctypes.c_void_p(U), ctypes.c_void_p(V), s), f"layer {i + 1} K1/K2")
+            # a layer that goes through the fast small-C kernel needs only the C real channel rows of V
+            k12 = lib.wino_transforms_smallc if self.smallc[i] and self._smallc_fast[i] else lib.wino_transforms
+            _native.check(k12(op.plan.handle, sh, D.ptr(cur), D.ptr(self.weights[i]),
+                              ctypes.c_void_p(U), ctypes.c_void_p(V), s), f"layer {i + 1} K1/K2")
         hook()
         if events is not None:
             events[1].record()

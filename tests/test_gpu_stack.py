@@ -207,3 +207,37 @@ def test_fused_output_input_transform_matches_k4_then_k1(cs):
                                                               pool, ctypes.byref(nxt.shape), _native.as_ptr(got), s))
                 torch.cuda.synchronize()
                 assert torch.equal(got.view(torch.int32), want.view(torch.int32)), (m, cs, N, C, K, H, Wd, pool)
+
+
+def test_transforms_smallc_leaves_padding_unwritten_and_unread():
+    """wino_transforms_smallc writes only the C real channel rows of V (the rest stays as it was)
+    and wino_contract_output_smallc never reads the others: poisoned padding, same bits."""
+    import ctypes
+    from paper_1803_10986_b200 import _native
+    lib = _native.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    ts = W.build_transforms(3, 6, W.parse_points(P8))
+    N, C, K, H, Wd = 3, 3, 24, 32, 40
+    op = W.layer_op(ts, W.ConvConfig("fp32", "huffman", "pairwise"), N, C, H, Wd, K, 1)
+    assert lib.wino_smallc_supported(op.plan.handle, ctypes.byref(op.shape)) == 2
+    op.prepare(_native.PREPARE_CONV | _native.PREPARE_ACT)
+    x = torch.from_numpy(O.synthetic((N, C, H, Wd), 5, 0)).cuda()
+    w = torch.from_numpy(O.synthetic((K, C, 3, 3), 5, 1)).cuda()
+    L = op.layout
+    U, V = op.filter_transform(w), op.input_transform(x)
+    want = torch.empty((N, K, L.Ho, L.Wo), device="cuda")
+    _native.check(lib.wino_output_transform_act(op.plan.handle, ctypes.byref(op.shape), _native.as_ptr(op.contract(U, V)),
+                                                _native.as_ptr(want), 0, s))
+    U2 = torch.full_like(U, float("nan"))
+    V2 = torch.full_like(V, float("nan"))
+    _native.check(lib.wino_transforms_smallc(op.plan.handle, ctypes.byref(op.shape), _native.as_ptr(x), _native.as_ptr(w),
+                                             _native.as_ptr(U2), _native.as_ptr(V2), s))
+    torch.cuda.synchronize()
+    Vv, V2v = V.view(L.P, -1, L.Cp, L.bn), V2.view(L.P, -1, L.Cp, L.bn)
+    assert torch.equal(V2v[:, :, :C].view(torch.int32), Vv[:, :, :C].view(torch.int32))   # real rows: same bits
+    assert torch.isnan(V2v[:, :, C:]).all()                                             # padding: untouched
+    got = torch.full_like(want, 7.0)
+    _native.check(lib.wino_contract_output_smallc(op.plan.handle, ctypes.byref(op.shape), _native.as_ptr(U2),
+                                                  _native.as_ptr(V2), _native.as_ptr(got), 1, s))
+    torch.cuda.synchronize()
+    assert torch.equal(got.view(torch.int32), want.view(torch.int32))
