@@ -634,7 +634,7 @@ def run_vgg(args):
     y_dev = st.act[-1].clone()
 
     # ---- per-layer stage times from an instrumented eager forward (events between stages)
-    per_layer, c_ms, c_flops, other_ms, fused_ms, n_contract = [], 0.0, 0, 0.0, 0.0, 0
+    per_layer, c_ms, c_flops, other_ms, fused_ms, n_contract, c_bytes = [], 0.0, 0, 0.0, 0.0, 0, 0
     mp_ = measured_peaks()
     hbm = mp_["hbm_gbs"]
     cur = x
@@ -648,8 +648,10 @@ def run_vgg(args):
             t_x, t_c, t_o = (ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]))
             P, T = L.P, L.T
             fused_prev, fused_next = i > 0 and st.fuse_next[i - 1], st.fuse_next[i]
-            # x read, V + U written (K2 only when the previous layer's K4 already wrote this layer's V)
-            b_x = (0 if fused_prev else 4 * n * C * h * w_ + 4 * P * C * T) + 4 * K * C * 9 + 4 * P * C * K
+            # x read, V + U written (K2 only when the previous layer's K4 already wrote this layer's V);
+            # the tensor-core modes store U and V as 16-bit operands
+            uvb = 2 if op_.tensor_core else 4
+            b_x = (0 if fused_prev else 4 * n * C * h * w_ + uvb * P * C * T) + 4 * K * C * 9 + uvb * P * C * K
             out_el = n * K * (L.Ho // 2) * (L.Wo // 2) if pool else n * K * L.Ho * L.Wo
             b_o = 4 * P * K * T + 4 * out_el                                             # M read, act written
             if fused_next:  # K4 + act + K1 of the next layer: M read, the next layer's V written
@@ -671,6 +673,10 @@ def run_vgg(args):
                               "contract_ms": t_c, "contract_tflops": op_.contraction_flops / (t_c * 1e-3) / 1e12,
                               "output_act_ms": t_o, "output_act_frac_hbm": b_o / (t_o * 1e-3) / 1e9 / hbm,
                               "v_written_by_previous_k4": bool(fused_prev), "k4_fused_with_next_k1": bool(fused_next)})
+            if op_.tensor_core:  # U16 + V16 read, fp32 M written: the HBM bytes that bound K3t at alpha = 8
+                b_c = 2 * P * L.Cp * (L.Tp + L.Kp) + 4 * P * L.Kp * L.Tp
+                per_layer[-1]["contract_frac_hbm"] = b_c / (t_c * 1e-3) / 1e9 / hbm
+                c_bytes += b_c
             c_ms += t_c
             other_ms += t_x + t_o
             c_flops += op_.contraction_flops
@@ -743,7 +749,8 @@ def run_vgg(args):
         if (rank == 0 and world == 1 and not args.no_cpu) else None
     st._conv_out = None
     if rank == 0:
-        roof = vgg_roof(args, ach, peak, c_ms / (c_ms + other_ms) if c_ms else None)
+        roof = vgg_roof(args, ach, peak, c_ms / (c_ms + other_ms) if c_ms else None,
+                        c_bytes / (c_ms * 1e-3) / 1e9 if (c_bytes and c_ms) else None)
         roof.update({"flops_per_forward": c_flops, "launches": n_contract,
                      "kernel": roof["kernel"].replace("13 layers", f"{n_contract} layers"),
                      "achieved_note": f"sum of the {n_contract} contraction launches' algorithmic flops (2 P T C K "
@@ -827,9 +834,19 @@ def vgg_traffic(kernel="wino_contract"):
         return None
 
 
-def vgg_roof(args, ach, peak, share):
+def vgg_roof(args, ach, peak, share, gbs=None):
     if args.contraction.startswith("tc_"):
         mp = measured_peaks()
+        if gbs is not None:
+            # 2 P T C K flops against 2 P Cp (Tp + Kp) + 4 P Kp Tp bytes: with K = 64..512 the unfused
+            # tensor-core contraction at alpha = 8 is bound by writing its fp32 M, not by the tensor pipe
+            return {"kernel": "tc_contract_kernel (13 layers)", "bound": "hbm", "achieved": gbs,
+                    "peak": mp["hbm_gbs"], "unit": "GB/s", "frac": gbs / mp["hbm_gbs"], "traffic": None,
+                    "peak_source": mp["source"] + " HBM copy bandwidth",
+                    "bound_note": "U16 + V16 read and the fp32 M written per launch (algorithmic bytes); "
+                                  "the same launches as a fraction of the dense bf16 tensor peak: "
+                                  f"{ach / mp['bf16_tflops']:.3f} ({ach:.1f} of {mp['bf16_tflops']:.0f} TFLOP/s)",
+                    "tensor_tflops": ach, "frac_of_tensor_peak": ach / mp["bf16_tflops"], "share_of_step": share}
         return {"kernel": "tc_contract_kernel (13 layers)", "bound": "tensor", "achieved": ach,
                 "peak": mp["bf16_tflops"], "unit": "TFLOP/s", "frac": ach / mp["bf16_tflops"], "traffic": None,
                 "peak_source": mp["source"] + " bf16 dense (burst)", "share_of_step": share}

@@ -652,20 +652,20 @@ static void emit_output_gather(std::ostringstream& os, int r, int m, const MatPr
 // expressions as wino_relu_pool (wino_static.cu): v = max(max(q00, q01),
 // max(q10, q11)); out = v > 0 ? v : 0.  fp32 y only.
 static void emit_output_gather_act(std::ostringstream& os, int r, int m, const MatProg& AT, const GenTypes& ty,
-                                   int TB, int& ctr) {
+                                   int TB, int& ctr, const char* mt = "uv_t") {
     const int n = r + m - 1;
     os << "static __device__ __forceinline__ float wino_relu(float v) { return v > 0.f ? v : 0.f; }\n"
           "extern \"C\" __global__ void __launch_bounds__(" << TB
        << (std::atoi(tuning("k4_blocks").c_str()) > 0 ? ", " + tuning("k4_blocks") : std::string())
        << ") wino_output_gather_act(\n"
-          "    const uv_t* __restrict__ Mm, float* __restrict__ act, int K, int Ho, int Wo, int th, int tw,\n"
+          "    const " << mt << "* __restrict__ Mm, float* __restrict__ act, int K, int Ho, int Wo, int th, int tw,\n"
           "    long long T, long long Tp, long long Kp, float rtw, float rth, int pool) {\n"
        << "  const int t0 = blockIdx.x * " << TB << ";\n"
           "  const int t = t0 + threadIdx.x;\n"
           "  if (t >= T) return;\n"
           "  const int k = blockIdx.y;\n"
           "  const long long plane = Kp * Tp;\n"
-          "  const uv_t* src = Mm + (long long)k * Tp + t;\n";
+          "  const " << mt << "* src = Mm + (long long)k * Tp + t;\n";
     std::vector<std::vector<std::string>> mm(n, std::vector<std::string>(n));
     for (int a = 0; a < n; ++a)
         for (int b = 0; b < n; ++b) {
@@ -2075,6 +2075,94 @@ std::string gen_layer_source_tc(int r, int m, const MatProg& G, const MatProg& B
             for (int j = 0; j < n; ++j) os << "  o[" << (i * n + j) << " * plane] = " << cv << v[i][j] << "));\n";
         os << "}\n\n";
     }
+    // 16 < P <= 96 (alpha = 5..9): thread = one tile x one channel with a WARP = 32 consecutive
+    // tiles of one channel, so the window loads coalesce like the fp32 gather kernel's (the
+    // 4-tiles x 8-channels map of input_tcg touches 8 image planes per load instruction).  The
+    // 16-bit results are parked in shared memory as [p][channel pair 0..3][tile 0..31][channel & 1]
+    // (a warp's store of one p: one 16-bit half per bank, conflict-free; the write-out reads whole
+    // 32-bit channel pairs, lanes on consecutive banks) and the block then writes every p's 32 rows
+    // of the canonical layout -- 16 bytes (8 channels) per row, 512 contiguous bytes per warp
+    // store.  Block = 256 threads = 32 tiles x 8 channels, P x 512 bytes of shared memory.
+    const bool staged_k1 = P > 16 && P <= 96 && tuning("k1tc_staged") != "0";
+    if (staged_k1) {
+        os << "static __device__ __forceinline__ void input_tcs(const in_t* __restrict__ x, unsigned short* __restrict__ V,\n"
+              "    int C, int H, int W, int pad, int th, int tw, long long T, long long Tp, long long Cp,\n"
+              "    float rtw, float rth, int t0, int c0) {\n"
+           << "  __shared__ __align__(16) unsigned short park[" << P << " * 256];\n"
+              "  const long long plane = tc_vstride(Cp, Tp);\n"
+              "  const int tl = threadIdx.x & 31, cl = threadIdx.x >> 5;\n"
+              "  const int t = t0 + tl, c = c0 + cl;\n"
+              "  unsigned short* pk = park + ((cl >> 1) * 32 + tl) * 2 + (cl & 1);\n"
+              "  if (c >= C || t >= T) {\n"
+              "#pragma unroll\n"
+           << "    for (int p = 0; p < " << P << "; ++p) pk[p * 256] = 0;\n"
+              "  } else {\n"
+              "  const int g0 = t0 / tw, off0 = t0 - g0 * tw;\n"
+              "  const int img0 = g0 / th, ti0 = g0 - img0 * th;\n"
+              "  const int off = off0 + tl;\n"
+              "  const int kk = idiv_small(off, tw, rtw), tj = off - kk * tw;\n"
+              "  const int di = idiv_small(ti0 + kk, th, rth);\n"
+              "  const int ti = ti0 + kk - di * th;\n"
+           << "  const int h0 = ti * " << m << " - pad, w0 = tj * " << m << " - pad;\n"
+           << "  const in_t* src = x + ((long long)(img0 + di) * C + c) * ((long long)H * W);\n";
+        std::vector<std::vector<std::string>> d(n, std::vector<std::string>(n));
+        for (int a = 0; a < n; ++a)
+            for (int b = 0; b < n; ++b) {
+                d[a][b] = "x" + std::to_string(a) + "_" + std::to_string(b);
+                os << "  ct_t " << d[a][b] << ";\n";
+            }
+        os << "  const bool interior = h0 >= 0 && w0 >= 0 && h0 + " << n << " <= H && w0 + " << n << " <= W;\n";
+        if (m % 2 == 0 && !ty.in_double) {
+            // even m: 8-byte row loads from the even column at or below w0 (as in input_gather_body)
+            for (int sh = 0; sh < 2; ++sh) {
+                const int nl = (n + sh + 1) / 2;
+                os << "  " << (sh == 0 ? "if" : "else if") << " (interior && (W & 1) == 0 && (pad & 1) == " << sh
+                   << " && (reinterpret_cast<size_t>(src) & 7) == 0) {\n"
+                   << "    const float2* rp = reinterpret_cast<const float2*>(src + h0 * W + w0 - " << sh << ");\n"
+                   << "    const int W2 = W >> 1;\n";
+                for (int a = 0; a < n; ++a) {
+                    for (int q = 0; q < nl; ++q)
+                        os << "    const float2 f" << a << "_" << q << " = __ldg(rp + " << a << " * W2 + " << q << ");\n";
+                    for (int b = 0; b < n; ++b) {
+                        const int e = b + sh;
+                        os << "    " << d[a][b] << " = (ct_t)f" << a << "_" << e / 2 << (e % 2 ? ".y" : ".x") << ";\n";
+                    }
+                }
+                os << "  }\n";
+            }
+            os << "  else if (interior) {\n";
+        } else {
+            os << "  if (interior) {\n";
+        }
+        os << "    const in_t* rp = src + h0 * W + w0;\n";
+        for (int a = 0; a < n; ++a)
+            for (int b = 0; b < n; ++b)
+                os << "    " << d[a][b] << " = (ct_t)__ldg(rp + " << a << " * W + " << b << ");\n";
+        os << "  } else {\n";
+        for (int a = 0; a < n; ++a)
+            os << "    const bool r" << a << " = (unsigned)(h0 + " << a << ") < (unsigned)H;\n";
+        for (int b = 0; b < n; ++b)
+            os << "    const bool c" << b << " = (unsigned)(w0 + " << b << ") < (unsigned)W;\n";
+        for (int a = 0; a < n; ++a)
+            for (int b = 0; b < n; ++b)
+                os << "    " << d[a][b] << " = (r" << a << " && c" << b << ") ? (ct_t)__ldg(src + (h0 + " << a
+                   << ") * W + (w0 + " << b << ")) : (ct_t)0;\n";
+        os << "  }\n";
+        Emitter em(os, ty.compute_double, ctr);
+        auto v = em.apply2d(BT, d);
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) os << "  pk[" << (i * n + j) << " * 256] = " << cv << v[i][j] << "));\n";
+        os << "  }\n"
+              "  __syncthreads();\n"
+              "  // write-out: item = (p, tile): 8 channels gathered from the park, one 16-byte row\n"
+              "  uint4* o = reinterpret_cast<uint4*>(V + tc_voff(t0 + tl, c0, Cp));\n"
+              "#pragma unroll 4\n"
+           << "  for (int p = cl; p < " << P << "; p += 8) {\n"
+              "    const unsigned* q = reinterpret_cast<const unsigned*>(park + p * 256) + tl;\n"
+              "    o[p * (plane >> 3)] = make_uint4(q[0], q[32], q[64], q[96]);\n"
+              "  }\n"
+              "}\n\n";
+    }
     // P <= 16: thread = one tile x 8 channels, the 8 transformed values of
     // each p packed in registers and written as one 16-byte row of the
     // canonical layout (a warp of 32 consecutive tiles stores 512 contiguous
@@ -2179,11 +2267,32 @@ std::string gen_layer_source_tc(int r, int m, const MatProg& G, const MatProg& B
           "  const int k = (int)blockIdx.x * 32 + ((threadIdx.x >> 5) << 2) + ((threadIdx.x >> 3) & 3);\n"
           "  if (k < Kp) filter_tcg(w, U, K, C, Kp, Cp, k, blockIdx.y * 8 + (threadIdx.x & 7));\n"
           "}\n\n";
+    // minimum blocks per SM of the staged K1 (register cap; tuning key k1tc_blocks)
+    const int tcs_blocks = std::atoi(tuning("k1tc_blocks").c_str()) > 0 ? std::atoi(tuning("k1tc_blocks").c_str()) : 3;
+    if (staged_k1)  // same grids and arguments as the *_tcg kernels; the host picks by image size
+        os << "extern \"C\" __global__ void __launch_bounds__(256, " << tcs_blocks << ") wino_input_tcs(\n"
+              "    const in_t* __restrict__ x, unsigned short* __restrict__ V, int C, int H, int W, int pad, int th,\n"
+              "    int tw, long long T, long long Tp, long long Cp, float rtw, float rth) {\n"
+              "  input_tcs(x, V, C, H, W, pad, th, tw, T, Tp, Cp, rtw, rth, blockIdx.x * 32, blockIdx.y * 8);\n"
+              "}\n\n"
+           << "extern \"C\" __global__ void __launch_bounds__(256, " << tcs_blocks << ") wino_transforms_tcs(\n"
+              "    const in_t* __restrict__ x, unsigned short* __restrict__ V, int C, int H, int W, int pad, int th,\n"
+              "    int tw, long long T, long long Tp, long long Cp, int n_tb,\n"
+              "    const in_t* __restrict__ w, unsigned short* __restrict__ U, int K, long long Kp, float rtw, float rth) {\n"
+              "  if ((int)blockIdx.x < n_tb) {\n"
+              "    input_tcs(x, V, C, H, W, pad, th, tw, T, Tp, Cp, rtw, rth, blockIdx.x * 32, blockIdx.y * 8);\n"
+              "  } else {\n"
+              "    const int k = ((int)blockIdx.x - n_tb) * 32 + ((threadIdx.x >> 5) << 2) + ((threadIdx.x >> 3) & 3);\n"
+              "    if (k < Kp) filter_tcg(w, U, K, C, Kp, Cp, k, blockIdx.y * 8 + (threadIdx.x & 7));\n"
+              "  }\n"
+              "}\n\n";
     int TB = 128;
     while (TB > 32 && (long long)P * TB * 4 > 64 * 1024) TB /= 2;
     emit_output_kernel(os, r, m, AT, ty, TB, ctr, "float", 4);
     emit_output_flat(os, r, m, AT, ty, TB, ctr, "float", 4);
     emit_output_gather(os, r, m, AT, ty, 128, ctr, "float");
+    // conv stacks in the tensor-core modes: K4 + ReLU (+ max-pool) in one kernel, as in the exact path
+    if (!ty.y_double) emit_output_gather_act(os, r, m, AT, ty, 128, ctr, "float");
     if (fused_nk) emit_tcf_kernel(os, r, m, AT, ty, fp16, fused_nk, ctr);
     return os.str();
 }

@@ -686,6 +686,17 @@ bool k4_gather() {
     return v;
 }
 
+// Tensor-core K1 at 16 < P <= 96: the warp-per-channel kernel that parks its 16-bit results in shared
+// memory (codegen.cpp input_tcs) for images of more than 32 x 32 pixels; smaller planes keep the
+// 4-tiles x 8-channels map, whose eight adjacent channel planes are one contiguous run of x
+// (VGG-16 batch 256, tc_bf16: 224^2 2.18 -> 1.62 ms, 112^2 1.17 -> 0.89, 56^2 0.68 -> 0.50, 28^2 equal,
+// 14^2 0.100 -> 0.137; tuning key k1tc_staged = 0: off, 2: every size)
+bool k1tc_staged(int P, const wino_layer_shape* s) {
+    const std::string e = wino::tuning("k1tc_staged");
+    if (P <= 16 || P > 96 || e == "0") return false;
+    return e == "2" || (long long)s->H * s->W > 32 * 32;
+}
+
 bool k1_no8() {  // WINO_K1TC=4x8: use the 4-tiles x 8-channels TC kernel also for P <= 16
     static const bool v = [] {
         const std::string es = wino::tuning("k1tc");
@@ -743,7 +754,7 @@ const char* wino_last_error(void) { return wino::g_last_error.c_str(); }
 
 int wino_tuning_set(const char* key, const char* value) {
     static const char* const keys[] = {"gemm", "dbuf", "k1", "k1order", "k4", "k1tc", "tile_interp",
-                                       "cpt", "kpt", "tcf_nk", "tcf_dbg", "tc_epi", "k1rowwise", "k4rowwise", "sc2_kg", "k4k1_ks", "k1st_blocks", "k1_blocks", "k4_blocks"};
+                                       "cpt", "kpt", "tcf_nk", "tcf_dbg", "tc_epi", "k1rowwise", "k4rowwise", "sc2_kg", "k4k1_ks", "k1st_blocks", "k1_blocks", "k4_blocks", "k1tc_staged", "k1tc_blocks"};
     if (!key) return wino::fail(WINO_EINVAL, "tuning_set: null key");
     bool known = false;
     for (const char* k : keys) known = known || std::strcmp(k, key) == 0;
@@ -1040,7 +1051,9 @@ static int transforms_impl(wino_plan* plan, const wino_layer_shape* s, const voi
     }
     if (tc && (k1_gather() || plan->fused()) && Cp / 8 <= 65535) {
         CUfunction fg;
-        if ((rc = plan->layer_mod(plan->pick(s))->function("wino_transforms_tcg", &fg))) return rc;
+        if ((rc = plan->layer_mod(plan->pick(s))->function(k1tc_staged(L.P, s) ? "wino_transforms_tcs" : "wino_transforms_tcg",
+                                                           &fg)))
+            return rc;
         float rtw = 1.0f / tw, rth = 1.0f / th;
         int nt32 = (int)cdiv(Tp, 32), nk32 = (int)cdiv(Kp, 32);
         void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &nt32, (void*)&w, &U, &K, &Kp,
@@ -1098,7 +1111,8 @@ int wino_input_transform(wino_plan* plan, const wino_layer_shape* s, const void*
                             "input_transform");
     }
     if (plan->mode >= WINO_CONTRACT_TC_BF16 && (k1_gather() || plan->fused()) && Cp / 8 <= 65535) {
-        if ((rc = plan->layer_mod(plan->pick(s))->function("wino_input_tcg", &f))) return rc;
+        if ((rc = plan->layer_mod(plan->pick(s))->function(k1tc_staged(L.P, s) ? "wino_input_tcs" : "wino_input_tcg", &f)))
+            return rc;
         float rtw = 1.0f / tw, rth = 1.0f / th;
         void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &rtw, &rth};
         return wino::launch(f, dim3((unsigned)cdiv(Tp, 32), (unsigned)(Cp / 8)), dim3(256), 0, stream, args,
@@ -1164,8 +1178,8 @@ int wino_output_transform_act(wino_plan* plan, const wino_layer_shape* s, const 
     wino_layer_layout L;
     int rc = layout_of(plan, s, &L);
     if (rc) return rc;
-    if (plan->mode >= WINO_CONTRACT_TC_BF16 || plan->ty.y_double)
-        return wino::fail(WINO_EUNSUPPORTED, "output_transform_act: fp32 plans with an FP32 contraction only");
+    if (plan->fused() || plan->ty.y_double)
+        return wino::fail(WINO_EUNSUPPORTED, "output_transform_act: plans with an fp32 M and an fp32 y only");
     if (pool != 0 && pool != 1) return wino::fail(WINO_EINVAL, "output_transform_act: pool must be 0 or 1");
     if (pool && (plan->m & 1)) return wino::fail(WINO_EUNSUPPORTED, "output_transform_act: pooling needs an even m");
     if (s->K > 65535) return wino::fail(WINO_EUNSUPPORTED, "output_transform_act: K > 65535");

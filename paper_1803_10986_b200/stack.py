@@ -139,7 +139,8 @@ class ConvStack:
     def fused_act(self) -> bool:
         """K4 writes the activation directly (ReLU / 2x2 max-pool fused, y not stored)."""
         pools = any(pool for _, _, pool in self.layers)
-        return not self.ops[0].tensor_core and (self.ts.n_o % 2 == 0 or not pools)
+        # tc_* modes keep an fp32 M, so the same fused K4 applies; tcf_* modes have no M at all
+        return not self.ops[0].contraction.startswith("tcf_") and (self.ts.n_o % 2 == 0 or not pools)
 
     @property
     def kernels_per_forward(self) -> int:

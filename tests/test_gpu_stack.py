@@ -71,6 +71,33 @@ def test_fused_activation_matches_relu_pool(m, pts):
             assert torch.equal(got.view(torch.int32), want.view(torch.int32)), (N, C, K, H, Wd, pool)
 
 
+@pytest.mark.parametrize("mode", ["tc_bf16", "tc_fp16"])
+def test_tensor_core_stack_fuses_activation(mode):
+    """tc_* modes keep an fp32 M, so a stack runs K4 + ReLU (+ pool) as one kernel there too:
+    same bits as the unfused forward (wino_conv2d then wino_relu_pool) of the same mode,
+    on edge tiles and pooled / un-pooled layers."""
+    from paper_1803_10986_b200.stack import ConvStack, he_normal_weights
+    ts = W.build_transforms(3, 6, W.parse_points(P8))
+    layers = [(3, 16, False), (16, 24, True), (24, 40, False), (40, 40, True)]
+    st = ConvStack(ts, W.ConvConfig("fp32", "huffman", "pairwise"), layers, 3, 36, 44, contraction=mode)
+    assert st.fused_act and st.kernels_per_forward == 3 * len(layers)
+    st.set_weights(he_normal_weights(layers, 3))
+    x = torch.from_numpy(O.synthetic((3, 3, 36, 44), 5, 0)).cuda()
+    fused = st.forward(x).clone()
+    acts = [a.clone() for a in st.act]
+    plain = st.forward(x, keep_conv_out=True)
+    torch.cuda.synchronize()
+    for i, a in enumerate(acts):
+        assert torch.equal(a.view(torch.int32), st.act[i].view(torch.int32)), i
+    assert torch.equal(fused.view(torch.int32), plain.view(torch.int32))
+    # and it is a convolution: final activation close to the exact path's
+    ex = ConvStack(ts, W.ConvConfig("fp32", "huffman", "pairwise"), layers, 3, 36, 44)
+    ex.set_weights(he_normal_weights(layers, 3))
+    ref = ex.forward(x)
+    rel = float((fused - ref).abs().sum() / ref.abs().sum())
+    assert rel < (0.2 if mode == "tc_bf16" else 0.03), rel
+
+
 def test_vgg16_geometry():
     from paper_1803_10986_b200.stack import VGG16, ConvStack
     ts = W.build_transforms(3, 6, W.parse_points(P8))
