@@ -96,7 +96,9 @@ typedef struct {
  * so one pipeline stage of a contraction tile is one contiguous block.
  * Cp/Kp/Tp are padded to the contraction kernel's tile sizes; padded channels
  * hold +0 (U) and -0 (V) so their products are -0 and leave every sum
- * bit-identical. */
+ * bit-identical.  M's padded rows (k >= K) and columns (t >= T) are scratch:
+ * the output transform never reads them and the tensor-core contraction
+ * leaves the padded rows unwritten. */
 typedef struct {
     int32_t P, th, tw, Ho, Wo;
     int32_t bm, bn; /* U / V block widths */

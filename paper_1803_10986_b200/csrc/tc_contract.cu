@@ -17,7 +17,7 @@
 //   warp 1      one elected thread issues tcgen05.mma (M=128, N=128, K=16) into
 //               one of two 128-column TMEM accumulators; tcgen05.commit frees
 //               the smem stage / publishes the finished accumulator
-//   warps 2-5   epilogue: tcgen05.ld TMEM -> registers -> M (fp32) while the
+//   warps 2..   epilogue (4 x EPW warps): tcgen05.ld TMEM -> registers -> M (fp32) while the
 //               next tile accumulates into the other TMEM buffer
 #include <mutex>
 #include <set>
@@ -117,13 +117,19 @@ constexpr int OSTAGES = 6;
 // wavefronts per warp instead of 32-way bank conflicts at a 128-byte pitch)
 constexpr int kStagePitch = 36;                                  // floats per staged row
 constexpr int kStageBytes = 32 * kStagePitch * 4;                // one 32x32 block
-constexpr int kEpiBytes = 4 * 2 * kStageBytes;                   // 4 warps x 2 buffers
+constexpr int kEpiBytes = 16 * kStageBytes;                      // 4 EPW warps x (EPW == 4 ? 1 : 2) buffers, at most
 constexpr int kEpiOffset = OSTAGES * 2 * kOpStage + 256;         // after operands + barriers
 
-__global__ void __launch_bounds__(192, 1) tc_contract_kernel(const unsigned short* __restrict__ U,
+// EPW epilogue warps per TMEM lane quarter (64 + 128 EPW threads): the kernel is bound by draining
+// the accumulators to M (C <= 512 is at most 16 stages of MMA work per 64 KB of output), and one warp
+// per quarter leaves its tcgen05.ld -> shared memory -> global store chain exposed; with EPW warps a
+// quarter's four 32-column chunks drain concurrently.
+template <int EPW>
+__global__ void __launch_bounds__(64 + 128 * EPW, 1) tc_contract_kernel(const unsigned short* __restrict__ U,
                                                              const unsigned short* __restrict__ V,
                                                              float* __restrict__ M, long long Kp, long long Tp,
-                                                             long long Cp, int n_tiles, int fp16, int tc_epi_mode) {
+                                                             long long Cp, int n_tiles, int fp16, int tc_epi_mode,
+                                                             int K) {
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned char* ops = smem;                                   // [OSTAGES][A | B]
     u64* bars = reinterpret_cast<u64*>(ops + OSTAGES * 2 * kOpStage);
@@ -144,7 +150,7 @@ __global__ void __launch_bounds__(192, 1) tc_contract_kernel(const unsigned shor
         }
         for (int s = 0; s < 2; ++s) {
             bar_init(&acc_full[s], 1);
-            bar_init(&acc_empty[s], 4);
+            bar_init(&acc_empty[s], 4 * EPW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -206,9 +212,11 @@ __global__ void __launch_bounds__(192, 1) tc_contract_kernel(const unsigned shor
             }
         }
     } else {
-        // ------------------------------------------------------------ epilogue warps 2..5
-        // TMEM lane quarter (warp % 4) = rows k of this warp
-        const int q4 = warp & 3;
+        // ------------------------------------------------------------ epilogue warps 2 .. 2 + 4 EPW
+        // TMEM lane quarter (warp % 4) = rows k of this warp; the EPW warps of a quarter take the
+        // 32-column chunks j = jh, jh + EPW, ...
+        const int q4 = warp & 3, ew = warp - 2, jh = ew >> 2;
+        constexpr int NB = EPW == 4 ? 1 : 2;  // staging buffers per warp
         int it = 0;
         unsigned eb = 0;  // staged blocks issued by this lane (buffer = eb & 1)
         const int epi = tc_epi_mode;
@@ -218,15 +226,25 @@ __global__ void __launch_bounds__(192, 1) tc_contract_kernel(const unsigned shor
             const int ab = it & 1;
             bar_wait(&acc_full[ab], (unsigned)((it >> 1) & 1));
             tc_fence_after();
+            // rows of this warp's quarter that are real filters: M's padded rows k >= K are never read
+            // (K4 walks k < K), so they are not written either -- at K = 64 (VGG-16 layers 1-2, 6 GB of
+            // M each at batch 256) that is half of the 128-row tile's store traffic
+            const int live = K - (kb * TBM + q4 * 32);
+            if (live <= 0) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) bar_arrive(&acc_empty[ab]);
+                continue;
+            }
             const long long krow = (long long)kb * TBM + q4 * 32 + lane;
             float* dst = M + (p * Kp + krow) * Tp + (long long)tb * TBN;
             // Each lane owns one row k: the 32 values of a tcgen05.ld go to its staged row
             // in smem, then one 128-byte cp.async.bulk per row writes a full line of M
             // (TMA engine) -- per-lane 16-byte global stores scattered over 32 rows
             // throttled the LSU (ncu: lg_throttle the top stall).
-            float* stage = reinterpret_cast<float*>(smem + kEpiOffset) + (size_t)q4 * 2 * 32 * kStagePitch;
+            float* stage = reinterpret_cast<float*>(smem + kEpiOffset) + (size_t)ew * NB * 32 * kStagePitch;
 #pragma unroll 1
-            for (int j = 0; j < TBN / 32; ++j) {
+            for (int j = jh; j < TBN / 32; j += EPW) {
                 uint32_t r[32];
                 const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * TBN + j * 32);
                 asm volatile(
@@ -241,24 +259,31 @@ __global__ void __launch_bounds__(192, 1) tc_contract_kernel(const unsigned shor
                     : "r"(taddr));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 if (epi == 0) {  // direct: lane-per-row 16-byte stores
+                    if (lane < live) {
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        *reinterpret_cast<uint4*>(dst + j * 32 + q * 4) =
-                            make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+                        for (int q = 0; q < 8; ++q)
+                            *reinterpret_cast<uint4*>(dst + j * 32 + q * 4) =
+                                make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+                    }
                 } else if (epi == 1) {  // staged row + one 128-byte bulk copy per lane
-                    float* row = stage + ((eb & 1) * 32 + lane) * kStagePitch;
-                    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    float* row = stage + ((eb & (NB - 1)) * 32 + lane) * kStagePitch;
+                    if (NB == 2)
+                        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    else
+                        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
                         *reinterpret_cast<uint4*>(row + q * 4) =
                             make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 128;" ::"l"(dst + j * 32),
-                                 "r"((uint32_t)__cvta_generic_to_shared(row))
-                                 : "memory");
+                    if (lane < live)
+                        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 128;" ::"l"(dst + j * 32),
+                                     "r"((uint32_t)__cvta_generic_to_shared(row))
+                                     : "memory");
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 } else {  // staged, read back 4 rows x 128 B per instruction: full-line stores
-                    float* blk = stage + (eb & 1) * 32 * kStagePitch;
+                    float* blk = stage + (eb & (NB - 1)) * 32 * kStagePitch;
+                    if (NB == 1) __syncwarp();  // the previous chunk's read-back is done
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
                         *reinterpret_cast<uint4*>(blk + lane * kStagePitch + q * 4) =
@@ -269,8 +294,9 @@ __global__ void __launch_bounds__(192, 1) tc_contract_kernel(const unsigned shor
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const int rr = i * 4 + rsub;
-                        *reinterpret_cast<uint4*>(gbase + (long long)rr * Tp) =
-                            *reinterpret_cast<const uint4*>(blk + rr * kStagePitch + c4);
+                        if (rr < live)
+                            *reinterpret_cast<uint4*>(gbase + (long long)rr * Tp) =
+                                *reinterpret_cast<const uint4*>(blk + rr * kStagePitch + c4);
                     }
                 }
                 ++eb;
@@ -295,6 +321,16 @@ namespace wino {
 
 // epilogue store form (tuning key "tc_epi"): 0 direct per-lane stores, 1 per-row bulk
 // copies, 2 (default) staged in smem and stored as full 128-byte lines
+// epilogue warps per lane quarter (tuning key "tc_epw": 1, 2 or 4)
+static int epi_warps() {
+    static const int v = [] {
+        const std::string e = tuning("tc_epw");
+        const int x = e.empty() ? 4 : std::atoi(e.c_str());
+        return (x == 1 || x == 2 || x == 4) ? x : 4;
+    }();
+    return v;
+}
+
 static int epi_mode() {
     static const int v = [] {
         const std::string e = tuning("tc_epi");
@@ -311,14 +347,18 @@ int tc_contract_prepare_device(int dev) {
     std::lock_guard<std::mutex> g(mu);
     if (done.count(dev)) return WINO_OK;
     const size_t smem = (size_t)kEpiOffset + kEpiBytes;
-    cudaError_t e = cudaFuncSetAttribute(tc_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(tc_contract_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(tc_contract_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(tc_contract_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(WINO_ECUDA, std::string("tc_contract: set smem: ") + cudaGetErrorString(e));
     done.insert(dev);
     return WINO_OK;
 }
 
 int tc_contract_launch(const void* U, const void* V, void* M, long long Kp, long long Tp, long long Cp, int P,
-                       int fp16, void* stream) {
+                       int fp16, int K, void* stream) {
     if (Kp % TBM || Tp % TBN || Cp % TBK) return fail(WINO_EINVAL, "tc_contract: layout not padded to 128/128/32");
     const long long tiles = (long long)P * (Kp / TBM) * (Tp / TBN);
     if (tiles > (1LL << 30)) return fail(WINO_EUNSUPPORTED, "tc_contract: too many tiles");
@@ -328,9 +368,10 @@ int tc_contract_launch(const void* U, const void* V, void* M, long long Kp, long
     if (int rc = tc_contract_prepare_device(dev)) return rc;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = (int)(tiles < sms ? tiles : sms);
-    tc_contract_kernel<<<grid, 192, smem, (cudaStream_t)stream>>>((const unsigned short*)U,
-                                                                 (const unsigned short*)V, (float*)M, Kp, Tp, Cp,
-                                                                 (int)tiles, fp16, epi_mode());
+    const int epw = epi_warps();
+    auto kern = epw == 1 ? tc_contract_kernel<1> : epw == 2 ? tc_contract_kernel<2> : tc_contract_kernel<4>;
+    kern<<<grid, 64 + 128 * epw, smem, (cudaStream_t)stream>>>((const unsigned short*)U, (const unsigned short*)V,
+                                                              (float*)M, Kp, Tp, Cp, (int)tiles, fp16, epi_mode(), K);
     return after_launch("tc_contract");
 }
 

@@ -754,7 +754,7 @@ const char* wino_last_error(void) { return wino::g_last_error.c_str(); }
 
 int wino_tuning_set(const char* key, const char* value) {
     static const char* const keys[] = {"gemm", "dbuf", "k1", "k1order", "k4", "k1tc", "tile_interp",
-                                       "cpt", "kpt", "tcf_nk", "tcf_dbg", "tc_epi", "k1rowwise", "k4rowwise", "sc2_kg", "k4k1_ks", "k1st_blocks", "k1_blocks", "k4_blocks", "k1tc_staged", "k1tc_blocks"};
+                                       "cpt", "kpt", "tcf_nk", "tcf_dbg", "tc_epi", "k1rowwise", "k4rowwise", "sc2_kg", "k4k1_ks", "k1st_blocks", "k1_blocks", "k4_blocks", "k1tc_staged", "k1tc_blocks", "tc_epw"};
     if (!key) return wino::fail(WINO_EINVAL, "tuning_set: null key");
     bool known = false;
     for (const char* k : keys) known = known || std::strcmp(k, key) == 0;
@@ -1140,7 +1140,7 @@ int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, con
         return wino::fail(WINO_EINVAL, "contract: fused tensor-core plan has no M; use wino_contract_output");
     if (plan->mode >= WINO_CONTRACT_TC_BF16)
         return wino::tc_contract_launch(U, V, M, L.Kp, L.Tp, L.Cp, L.P, plan->mode == WINO_CONTRACT_TC_FP16,
-                                        stream);
+                                        s->K, stream);
     const int ci = plan->pick(s);
     wino::Module* mod = plan->contract_module(L.Cp, ci);
     CUfunction f;

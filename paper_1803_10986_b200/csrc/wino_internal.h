@@ -15,7 +15,7 @@ int after_launch(const char* what);
 void count_launch();
 // K3t: tcgen05 tensor-core contraction (tc_contract.cu)
 int tc_contract_launch(const void* U, const void* V, void* M, long long Kp, long long Tp, long long Cp, int P,
-                       int fp16, void* stream);
+                       int fp16, int K, void* stream);
 // the tcgen05 contraction's dynamic smem opt-in, once per device
 int tc_contract_prepare_device(int dev);
 // device copies of a plan's row programs (postfix ops + row starts) for the

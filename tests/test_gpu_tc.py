@@ -24,7 +24,8 @@ def test_tc_contraction_matches_rounded_gemm(mode, dt):
     Uu = Ud.to(dt).double()
     Vu = Vd.to(dt).double()
     ref = torch.einsum("pck,pct->pkt", Uu, Vu)
-    err = (M.double() - ref).abs().max().item()
+    # M's padded filter rows (k >= K) are never read by K4 and are left unwritten
+    err = (M.double() - ref)[:, :150].abs().max().item()
     scale = torch.einsum("pck,pct->pkt", Uu.abs(), Vu.abs()).max().item()
     assert err <= 1e-5 * scale, (err, scale)
 
