@@ -482,7 +482,10 @@ def vgg_config(args, n_per_gpu, world):
             "winograd": "F(6x6,3x3)", "points": VGG_POINTS, "global_batch": args.vgg_batch,
             "batch_per_gpu": n_per_gpu, "image": [3, 224, 224], "precision": "fp32", "dot_order": "huffman",
             "channel_sum": "pairwise", "contraction": args.contraction,
-            "contraction_note": contraction_note(args.contraction), "layers": 13, "pools_after": [2, 4, 7, 10],
+            "contraction_note": contraction_note(args.contraction) + (
+                "; layer 1 (C = 3) runs the exact fp32 path (fused K3 + K4 + ReLU): a 3-channel contraction has "
+                "nothing for a tensor core" if args.contraction.startswith("tc_") else ""),
+            "layers": 13, "pools_after": [2, 4, 7, 10],
             "l2": "no flush needed: inputs and activations >> 126 MB L2 (layer-1 x 154 MB, M 6 GB)",
             "parallelism": f"dp{world} (global batch sharded by images)"}
 

@@ -49,8 +49,13 @@ class ConvStack:
         self.H, self.W = H, W
         self.ops, self.shapes = [], []
         h, w = H, W
+        self.contraction = contraction
         for C, K, pool in self.layers:
-            op = layer_op(ts, cfg, N, C, h, w, K, pad, contraction)
+            # tc_* stacks: a layer with C <= 4 (VGG-16 layer 1) has no contraction worth a tensor core --
+            # its 32-channel padded MMA only writes M -- so it runs the exact fp32 path (fused K3 + K4 +
+            # activation where supported); tcf_* plans keep one mode throughout (no M anywhere)
+            mode = "exact" if contraction.startswith("tc_") and C <= 4 else contraction
+            op = layer_op(ts, cfg, N, C, h, w, K, pad, mode)
             if not op.tensor_core:
                 op.prepare(_native.PREPARE_CONV | _native.PREPARE_ACT)
             self.ops.append(op)
@@ -140,7 +145,7 @@ class ConvStack:
         """K4 writes the activation directly (ReLU / 2x2 max-pool fused, y not stored)."""
         pools = any(pool for _, _, pool in self.layers)
         # tc_* modes keep an fp32 M, so the same fused K4 applies; tcf_* modes have no M at all
-        return not self.ops[0].contraction.startswith("tcf_") and (self.ts.n_o % 2 == 0 or not pools)
+        return not self.contraction.startswith("tcf_") and (self.ts.n_o % 2 == 0 or not pools)
 
     @property
     def kernels_per_forward(self) -> int:

@@ -80,7 +80,9 @@ def test_tensor_core_stack_fuses_activation(mode):
     ts = W.build_transforms(3, 6, W.parse_points(P8))
     layers = [(3, 16, False), (16, 24, True), (24, 40, False), (40, 40, True)]
     st = ConvStack(ts, W.ConvConfig("fp32", "huffman", "pairwise"), layers, 3, 36, 44, contraction=mode)
-    assert st.fused_act and st.kernels_per_forward == 3 * len(layers)
+    # the C = 3 layer has no contraction worth a tensor core: it runs the exact (fused small-C) path
+    assert st.fused_act and not st.ops[0].tensor_core and all(op.tensor_core for op in st.ops[1:])
+    assert st.kernels_per_forward in (2 + 3 * (len(layers) - 1), 3 * len(layers))
     st.set_weights(he_normal_weights(layers, 3))
     x = torch.from_numpy(O.synthetic((3, 3, 36, 44), 5, 0)).cuda()
     fused = st.forward(x).clone()
