@@ -175,8 +175,9 @@ int wino_contract(wino_plan* plan, const wino_layer_shape* s, const void* U, con
 /* K4: y = A^T M A per (k, tile), crop + NCHW write-back -- engine.py:418-423 */
 int wino_output_transform(wino_plan* plan, const wino_layer_shape* s, const void* M,
                           void* y, void* stream);
-/* K4 with the activation fused (conv stacks, BASELINE config 5; fp32 plans with
- * an FP32 contraction): act = relu(y) (pool = 0, act [N][K][Ho][Wo]) or the 2x2
+/* K4 with the activation fused (conv stacks, BASELINE config 5; plans with an fp32
+ * M and an fp32 y: fp32 precision with the exact, ffma, tc_bf16 or tc_fp16
+ * contraction): act = relu(y) (pool = 0, act [N][K][Ho][Wo]) or the 2x2
  * max-pool of relu(y) (pool = 1, even m only, act [N][K][Ho/2][Wo/2]); the same
  * values as wino_output_transform followed by wino_relu_pool, y never stored. */
 int wino_output_transform_act(wino_plan* plan, const wino_layer_shape* s, const void* M,
@@ -313,7 +314,8 @@ const char* wino_last_error(void);
  * (plans created afterwards), "dbuf", "tcf_nk" (same), "k1" = "tile" | "gather" (K1 from
  * global memory only) | "bulk<KB>" (shared-memory cap of the bulk-staged K1), "k1order" =
  * "t", "k4" = "staged", "k1tc" = "4x8", "tile_interp" = "0|1", "cpt" / "kpt" =
- * 1|2|4|8, "tcf_dbg", "tc_epi", "k1rowwise" / "k4rowwise", "sc2_kg" (filter-pair warp groups
+ * 1|2|4|8, "tcf_dbg", "tc_epi", "tc_epw" (epilogue warps per TMEM lane quarter: 1|2|4),
+ * "k1tc_staged" (0: off, 2: every image size) / "k1tc_blocks", "k1rowwise" / "k4rowwise", "sc2_kg" (filter-pair warp groups
  * of the small-C fused kernel), "k4k1_ks" (read once per process, before the first launch).
  * value NULL or "" clears the key.  Unknown keys -> WINO_EINVAL. */
 int wino_tuning_set(const char* key, const char* value);
