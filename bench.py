@@ -677,7 +677,7 @@ def run_vgg(args):
                               "output_act_ms": t_o, "output_act_frac_hbm": b_o / (t_o * 1e-3) / 1e9 / hbm,
                               "v_written_by_previous_k4": bool(fused_prev), "k4_fused_with_next_k1": bool(fused_next)})
             if op_.tensor_core:  # U16 + V16 read, fp32 M written: the HBM bytes that bound K3t at alpha = 8
-                b_c = 2 * P * L.Cp * (L.Tp + L.Kp) + 4 * P * L.Kp * L.Tp
+                b_c = 2 * P * C * (T + K) + 4 * P * K * T
                 per_layer[-1]["contract_frac_hbm"] = b_c / (t_c * 1e-3) / 1e9 / hbm
                 c_bytes += b_c
             c_ms += t_c
@@ -841,7 +841,7 @@ def vgg_roof(args, ach, peak, share, gbs=None):
     if args.contraction.startswith("tc_"):
         mp = measured_peaks()
         if gbs is not None:
-            # 2 P T C K flops against 2 P Cp (Tp + Kp) + 4 P Kp Tp bytes: with K = 64..512 the unfused
+            # 2 P T C K flops against 2 P C (T + K) + 4 P K T bytes: with K = 64..512 the unfused
             # tensor-core contraction at alpha = 8 is bound by writing its fp32 M, not by the tensor pipe
             return {"kernel": "tc_contract_kernel (13 layers)", "bound": "hbm", "achieved": gbs,
                     "peak": mp["hbm_gbs"], "unit": "GB/s", "frac": gbs / mp["hbm_gbs"], "traffic": None,

@@ -117,13 +117,14 @@ constexpr int OSTAGES = 6;
 // wavefronts per warp instead of 32-way bank conflicts at a 128-byte pitch)
 constexpr int kStagePitch = 36;                                  // floats per staged row
 constexpr int kStageBytes = 32 * kStagePitch * 4;                // one 32x32 block
-constexpr int kEpiBytes = 16 * kStageBytes;                      // 4 EPW warps x (EPW == 4 ? 1 : 2) buffers, at most
+// 4 EPW warps x (EPW == 4 ? 1 : 2) staging buffers
+constexpr int epi_bytes(int epw) { return 4 * epw * (epw == 4 ? 1 : 2) * kStageBytes; }
 constexpr int kEpiOffset = OSTAGES * 2 * kOpStage + 256;         // after operands + barriers
 
 // EPW epilogue warps per TMEM lane quarter (64 + 128 EPW threads): the kernel is bound by draining
-// the accumulators to M (C <= 512 is at most 16 stages of MMA work per 64 KB of output), and one warp
-// per quarter leaves its tcgen05.ld -> shared memory -> global store chain exposed; with EPW warps a
-// quarter's four 32-column chunks drain concurrently.
+// the accumulators to M (C <= 512 is at most 16 stages of MMA work per 64 KB of output); with EPW
+// warps a quarter's four 32-column chunks drain concurrently (measured: no gain over EPW = 1 once
+// the store loop is unpredicated, see epi_warps below).
 template <int EPW>
 __global__ void __launch_bounds__(64 + 128 * EPW, 1) tc_contract_kernel(const unsigned short* __restrict__ U,
                                                              const unsigned short* __restrict__ V,
@@ -291,12 +292,21 @@ __global__ void __launch_bounds__(64 + 128 * EPW, 1) tc_contract_kernel(const un
                     __syncwarp();
                     const int rsub = lane >> 3, c4 = (lane & 7) * 4;
                     float* gbase = M + (p * Kp + (long long)kb * TBM + q4 * 32) * Tp + (long long)tb * TBN + j * 32 + c4;
+                    if (live >= 32) {  // warp-uniform: the unpredicated loop keeps its 8 loads ahead of its 8 stores
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int rr = i * 4 + rsub;
-                        if (rr < live)
+                        for (int i = 0; i < 8; ++i) {
+                            const int rr = i * 4 + rsub;
                             *reinterpret_cast<uint4*>(gbase + (long long)rr * Tp) =
                                 *reinterpret_cast<const uint4*>(blk + rr * kStagePitch + c4);
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int rr = i * 4 + rsub;
+                            if (rr < live)
+                                *reinterpret_cast<uint4*>(gbase + (long long)rr * Tp) =
+                                    *reinterpret_cast<const uint4*>(blk + rr * kStagePitch + c4);
+                        }
                     }
                 }
                 ++eb;
@@ -321,12 +331,15 @@ namespace wino {
 
 // epilogue store form (tuning key "tc_epi"): 0 direct per-lane stores, 1 per-row bulk
 // copies, 2 (default) staged in smem and stored as full 128-byte lines
-// epilogue warps per lane quarter (tuning key "tc_epw": 1, 2 or 4)
-static int epi_warps() {
+// epilogue warps per lane quarter: tuning key "tc_epw" (1, 2 or 4), default 1.  With the full-quarter
+// store loop unpredicated, one warp per quarter keeps the store path full: VGG-16 stack K3t 7.17 ms
+// against 7.26 / 7.36 ms with 2 / 4 warps, cfg2 17.4 vs 17.3 / 30.5 us, cfg3 39.1 vs 39.3 / 39.4 us.
+// (While the loop was predicated per row, the K = 64 layers needed 4 warps: 2.38 -> 1.64 ms.)
+static int epi_warps(long long, int) {
     static const int v = [] {
         const std::string e = tuning("tc_epw");
-        const int x = e.empty() ? 4 : std::atoi(e.c_str());
-        return (x == 1 || x == 2 || x == 4) ? x : 4;
+        const int x = e.empty() ? 0 : std::atoi(e.c_str());
+        return (x == 1 || x == 2 || x == 4) ? x : 1;
     }();
     return v;
 }
@@ -346,12 +359,14 @@ int tc_contract_prepare_device(int dev) {
     static std::set<int> done;
     std::lock_guard<std::mutex> g(mu);
     if (done.count(dev)) return WINO_OK;
-    const size_t smem = (size_t)kEpiOffset + kEpiBytes;
-    cudaError_t e = cudaFuncSetAttribute(tc_contract_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(tc_contract_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kEpiOffset + epi_bytes(1));
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(tc_contract_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaFuncSetAttribute(tc_contract_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kEpiOffset + epi_bytes(2));
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(tc_contract_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaFuncSetAttribute(tc_contract_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kEpiOffset + epi_bytes(4));
     if (e != cudaSuccess) return fail(WINO_ECUDA, std::string("tc_contract: set smem: ") + cudaGetErrorString(e));
     done.insert(dev);
     return WINO_OK;
@@ -362,13 +377,13 @@ int tc_contract_launch(const void* U, const void* V, void* M, long long Kp, long
     if (Kp % TBM || Tp % TBN || Cp % TBK) return fail(WINO_EINVAL, "tc_contract: layout not padded to 128/128/32");
     const long long tiles = (long long)P * (Kp / TBM) * (Tp / TBN);
     if (tiles > (1LL << 30)) return fail(WINO_EUNSUPPORTED, "tc_contract: too many tiles");
-    const size_t smem = (size_t)kEpiOffset + kEpiBytes;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     if (int rc = tc_contract_prepare_device(dev)) return rc;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = (int)(tiles < sms ? tiles : sms);
-    const int epw = epi_warps();
+    const int epw = epi_warps(Kp, K);
+    const size_t smem = (size_t)kEpiOffset + epi_bytes(epw);
     auto kern = epw == 1 ? tc_contract_kernel<1> : epw == 2 ? tc_contract_kernel<2> : tc_contract_kernel<4>;
     kern<<<grid, 64 + 128 * epw, smem, (cudaStream_t)stream>>>((const unsigned short*)U, (const unsigned short*)V,
                                                               (float*)M, Kp, Tp, Cp, (int)tiles, fp16, epi_mode(), K);
