@@ -50,6 +50,44 @@ def test_tc_transforms_write_rounded_operands(mode):
 
 
 @pytest.mark.parametrize("mode", ["tc_bf16", "tc_fp16"])
+@pytest.mark.parametrize("m,pts,geom", [(6, "0,-1,1,1/2,-1/2,2,-2,inf", (3, 13, 37, 41, 9)),
+                                        (6, "0,-1,1,1/2,-1/2,2,-2,inf", (2, 20, 64, 34, 5)),
+                                        (4, "0,1,-1,1/2,-1/2,inf", (2, 9, 40, 40, 7)),
+                                        (6, "0,-1,1,1/2,-1/2,2,-2,inf", (5, 11, 14, 14, 9))],
+                         ids=["a8_37x41", "a8_64x34", "a6_40x40", "a8_14x14_old_map"])
+def test_tc_staged_input_transform_writes_rounded_operands(mode, m, pts, geom):
+    """K1 of the tc modes at 16 < alpha^2 <= 96: images above 32 x 32 take the warp-per-channel kernel that
+    parks its 16-bit results in shared memory (wino_input_tcs / wino_transforms_tcs), smaller ones the
+    4-tiles x 8-channels map; both store exactly round16(exact fp32 transform), through the standalone K1
+    and through the K1 + K2 launch, with zeros in the padded channels and tiles."""
+    import ctypes
+    from paper_1803_10986_b200 import _native
+    N, C, H, Wd, K = geom
+    ts = W.build_transforms(3, m, W.parse_points(pts))
+    x = torch.from_numpy(O.synthetic((N, C, H, Wd), 6, 0)).cuda()
+    w = torch.from_numpy(O.synthetic((K, C, 3, 3), 6, 1)).cuda()
+    ex = W.layer_op(ts, W.ConvConfig(), N, C, H, Wd, K, 1)
+    tc = W.layer_op(ts, W.ConvConfig(), N, C, H, Wd, K, 1, contraction=mode)
+    dt = torch.bfloat16 if mode == "tc_bf16" else torch.float16
+    Le, Lt = ex.layout, tc.layout
+    ve = ex.unblock_v(ex.input_transform(x))[:, :C, :Le.T].to(dt)
+    vt = tc.unblock_v(tc.input_transform(x))
+    assert torch.equal(vt[:, :C, :Lt.T], ve)
+    assert not vt[:, C:, :].any() and not vt[:, :, Lt.T:].any()
+    # the combined K1 + K2 launch
+    U = torch.full((Lt.P * Lt.Cp * Lt.Kp,), 0x7fff, dtype=torch.int16, device="cuda")
+    V = torch.full((Lt.P * Lt.Cp * Lt.Tp,), 0x7fff, dtype=torch.int16, device="cuda")
+    _native.check(_native.lib().wino_transforms(tc.plan.handle, ctypes.byref(tc.shape), _native.as_ptr(x),
+                                                _native.as_ptr(w), _native.as_ptr(U), _native.as_ptr(V),
+                                                torch.cuda.current_stream().cuda_stream), "transforms")
+    torch.cuda.synchronize()
+    v2 = tc.unblock_v(V.view(dt))
+    assert torch.equal(v2[:, :C, :Lt.T], ve) and not v2[:, C:, :].any() and not v2[:, :, Lt.T:].any()
+    ue = ex.unblock_u(ex.filter_transform(w))[:, :C, :K].to(dt)
+    assert torch.equal(tc.unblock_u(U.view(dt))[:, :C, :K], ue)
+
+
+@pytest.mark.parametrize("mode", ["tc_bf16", "tc_fp16"])
 def test_tc_layer_error_vs_fp64(mode):
     pts = "0,-1,1,1/2,-1/2,2,-2,inf"
     ts = W.build_transforms(3, 6, W.parse_points(pts))

@@ -31,7 +31,7 @@ ncu --set full --clock-control none --import-source on \
     -o gpurun_out/prof_bench python bench.py --ncu --steps 1 --warmup 3 > gpurun_out/ncu2.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"wino_smallc2" -s 3 -c 1 \
     -o gpurun_out/prof_smallc2 python bench.py --ncu --steps 1 --warmup 3 > gpurun_out/ncu3.log 2>&1
-# tensor-core mode: layer 2's three kernels (3 warm-up forwards x 39 kernels + layer 1's 3)
+# tensor-core mode: the three kernels of a 56 x 56 layer (layer 1 runs the exact path and is not matched: 36 matching kernels per forward)
 ncu --set full --clock-control none --import-source on \
     -k regex:"tc_contract_kernel|wino_transforms_tc|wino_output_gather_act" -s 120 -c 3 \
     -o gpurun_out/prof_tc python bench.py --ncu --contraction tc_bf16 --steps 1 --warmup 3 > gpurun_out/ncu4.log 2>&1
