@@ -30,6 +30,32 @@ def test_tc_contraction_matches_rounded_gemm(mode, dt):
     assert err <= 1e-5 * scale, (err, scale)
 
 
+@pytest.mark.parametrize("K", [64, 150, 7])
+def test_tc_contraction_leaves_padded_filter_rows_unwritten(K):
+    """K3t stores exactly the rows k < K of every point's [Kp][Tp] slab: poisoned padding rows stay
+    poisoned (K = 64 pads to 128: half of the tile's store traffic), every real row is written,
+    including the partially live lane quarter when K % 32 != 0."""
+    import ctypes
+    from paper_1803_10986_b200 import _native
+    ts = W.build_transforms(3, 4, W.parse_points("0,1,-1,1/2,-1/2,inf"))
+    op = W.layer_op(ts, W.ConvConfig(), 2, 40, 20, 20, K, 1, contraction="tc_fp16")
+    L = op.layout
+    Ud = torch.randn((L.P, L.Cp, L.Kp), device="cuda")
+    Vd = torch.randn((L.P, L.Cp, L.Tp), device="cuda")
+    U, V = op.block_u(Ud), op.block_v(Vd)
+    poison = torch.full((L.P, L.Kp, L.Tp), float("nan"), device="cuda")
+    M = poison.clone()
+    _native.check(_native.lib().wino_contract(op.plan.handle, ctypes.byref(op.shape), _native.as_ptr(U),
+                                              _native.as_ptr(V), _native.as_ptr(M),
+                                              torch.cuda.current_stream().cuda_stream), "contract")
+    torch.cuda.synchronize()
+    assert not torch.isnan(M[:, :K]).any()
+    assert torch.isnan(M[:, K:]).all() or L.Kp == K
+    ref = torch.einsum("pck,pct->pkt", Ud.half().double(), Vd.half().double())[:, :K]
+    scale = torch.einsum("pck,pct->pkt", Ud.half().double().abs(), Vd.half().double().abs()).max().item()
+    assert (M[:, :K].double() - ref).abs().max().item() <= 1e-5 * scale
+
+
 @pytest.mark.parametrize("mode", ["tc_bf16", "tc_fp16"])
 def test_tc_transforms_write_rounded_operands(mode):
     """The tc transforms store exactly round16(fp32 exact transform) in the UMMA layout."""
