@@ -22,6 +22,7 @@ layers = [int(v) for v in os.environ.get("PROBE_LAYERS", "2,4,6,9").split(",")]
 sizes = [int(v) for v in os.environ.get("PROBE_CHUNKS", "256,16,8,4,2,1").split(",")]
 ts = W.build_transforms(3, 6, W.parse_points("0,-1,1,1/2,-1/2,2,-2,inf"))
 cfg = W.ConvConfig("fp32", "huffman", "pairwise")
+MODE = os.environ.get("PROBE_MODE", "exact")  # tc_bf16 / tc_fp16: the HBM-bound tensor-core contraction
 lib = _native.lib()
 s = torch.cuda.current_stream().cuda_stream
 
@@ -37,8 +38,9 @@ for layer in layers:
     for n in sizes:
         if n > N:
             continue
-        op = W.layer_op(ts, cfg, n, C, H, H, K, 1)
-        op.prepare(_native.PREPARE_CONV | _native.PREPARE_ACT | _native.PREPARE_STAGES)
+        op = W.layer_op(ts, cfg, n, C, H, H, K, 1, MODE)
+        if not op.tensor_core:
+            op.prepare(_native.PREPARE_CONV | _native.PREPARE_ACT | _native.PREPARE_STAGES)
         L = op.layout
         U = op.filter_transform(w)
         V = torch.empty(L.v_bytes, dtype=torch.uint8, device="cuda")
