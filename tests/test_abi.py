@@ -175,6 +175,31 @@ def test_sass_gate_rejects_fused_sums():
     assert not _fused_ops("FMUL R1, R2, R3 ; FADD2 R4, R6.F32x2.HI_LO, R8.F32x2.HI_LO ; HFMA2 R5, -RZ, RZ, 0, 0 ;")
 
 
+def test_tensor_core_layer_module_has_the_stack_kernels(built):
+    """The tc_* layer module (NVRTC, CPU-only compile) carries the fused K4 + ReLU / max-pool kernel and,
+    at 16 < alpha^2 <= 96, the warp-per-channel K1 with its shared-memory park: separately rounded
+    transform arithmetic (no FMA), 16-bit park stores, 16-byte global row stores, three 256-thread blocks
+    per SM without spills; alpha^2 <= 16 keeps the register-packed 8-channel kernel instead."""
+    plan = _plan(3, 6, "0,-1,1,1/2,-1/2,2,-2,inf", "fp32", "pairwise", contraction="tc_bf16")
+    cub = plan.cubin(0, 0)
+    sass = _sass(cub)
+    fns = dict((f.split()[0], f) for f in re.split(r"\n\s*Function : ", sass)[1:])
+    for k in ("wino_transforms_tcs", "wino_input_tcs", "wino_transforms_tcg", "wino_output_gather_act"):
+        assert k in fns, sorted(fns)
+    tcs = fns["wino_input_tcs"]
+    assert not FMA.search(tcs)
+    assert re.search(r"\bSTS\.U16\b", tcs) and re.search(r"\bSTG\.E\.128\b", tcs) and "BAR.SYNC" in tcs
+    assert "STL" not in tcs and "LDL" not in tcs
+    with tempfile.NamedTemporaryFile(suffix=".cubin") as f:
+        f.write(cub)
+        f.flush()
+        res = subprocess.run(["cuobjdump", "-res-usage", f.name], capture_output=True, text=True, check=True).stdout
+    m = re.search(r"Function wino_input_tcs:\s*\n\s*REG:(\d+) .*?SHARED:(\d+)", res)
+    assert m and int(m.group(1)) <= 85 and int(m.group(2)) >= 64 * 512, res[:400]
+    small = _plan(3, 2, "0,1,-1,inf", "fp32", "linear", contraction="tc_bf16")
+    assert "wino_input_tcs" not in _sass(small.cubin(0, 0))
+
+
 def test_ffma_mode_uses_fma(built):
     plan = _plan(3, 2, "0,1,-1,inf", "fp32", "linear", contraction="ffma")
     assert FMA.search(_sass(plan.cubin(2, 128)))
