@@ -7,6 +7,7 @@ python bench.py --steps 20 --warmup 5 > gpurun_out/bench_vgg16.log 2>&1; echo be
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_vgg16_reference.log 2>&1; echo reference rc=$?
 python bench.py --steps 5 --warmup 3 --contraction tc_bf16 --no-cpu > gpurun_out/bench_vgg16_tc_bf16.log 2>&1
 python bench.py --steps 5 --warmup 3 --contraction tc_fp16 --no-cpu > gpurun_out/bench_vgg16_tc_fp16.log 2>&1
+python bench.py --steps 5 --warmup 3 --contraction ffma --no-cpu > gpurun_out/bench_vgg16_ffma.log 2>&1
 # single-layer configs (extra lines)
 for c in cfg1 cfg2 cfg3_m6 cfg3_m6_mixed_pw cfg4_m4; do
   python bench.py --config $c --steps 20 --warmup 5 --soak 0.5 > gpurun_out/bench_$c.log 2>&1
