@@ -130,6 +130,30 @@ def test_tc_layer_error_vs_fp64(mode):
 
 
 @pytest.mark.parametrize("mode,dt", [("tcf_bf16", torch.bfloat16), ("tcf_fp16", torch.float16)])
+def test_tcf_alpha5_with_the_staged_input_transform(mode, dt):
+    """alpha = 5 (P = 25) on an image above 32 x 32: the fused tensor-core plan's K1 is the staged
+    warp-per-channel kernel writing the fused operand layout ([t/128][c/16][p]...): V == round16(exact V),
+    and the fused layer agrees with the unfused tc mode (same operands) to accumulation accuracy."""
+    ts = W.build_transforms(3, 3, W.parse_points("0,1,-1,2,inf"))
+    N, C, H, Wd, K = 2, 19, 41, 50, 24
+    x = torch.from_numpy(O.synthetic((N, C, H, Wd), 8, 0)).cuda()
+    w = torch.from_numpy(O.synthetic((K, C, 3, 3), 8, 1)).cuda()
+    ex = W.layer_op(ts, W.ConvConfig(), N, C, H, Wd, K, 1)
+    op = W.layer_op(ts, W.ConvConfig(), N, C, H, Wd, K, 1, contraction=mode)
+    assert op.layout.P == 25
+    ve = ex.unblock_v(ex.input_transform(x))[:, :C, :ex.layout.T].to(dt)
+    vt = op.unblock_v(op.input_transform(x))
+    assert torch.equal(vt[:, :C, :op.layout.T], ve)
+    assert not vt[:, C:, :].any() and not vt[:, :, op.layout.T:].any()
+    y = W.conv2d_layer(ts, x, w, W.ConvConfig(), pad=1, contraction=mode)
+    y3 = W.conv2d_layer(ts, x, w, W.ConvConfig(), pad=1, contraction=mode.replace("tcf", "tc"))
+    yx = W.conv2d_layer(ts, x, w, W.ConvConfig(), pad=1)
+    scale = yx.abs().max().item()
+    assert (y.double() - y3.double()).abs().max().item() <= 1e-4 * scale
+    assert (y.double() - yx.double()).abs().max().item() <= (0.1 if "bf16" in mode else 0.02) * scale
+
+
+@pytest.mark.parametrize("mode,dt", [("tcf_bf16", torch.bfloat16), ("tcf_fp16", torch.float16)])
 @pytest.mark.parametrize("geom", [(3, 70, 20, 20, 150, 1), (2, 16, 9, 11, 16, 0), (1, 33, 28, 28, 40, 1)],
                          ids=lambda g: "N{}C{}H{}W{}K{}".format(*g[:5]))
 def test_tcf_fused_matches_rounded_gemm_then_output(mode, dt, geom):
