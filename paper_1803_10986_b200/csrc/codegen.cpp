@@ -2268,7 +2268,9 @@ std::string gen_layer_source_tc(int r, int m, const MatProg& G, const MatProg& B
           "  if (k < Kp) filter_tcg(w, U, K, C, Kp, Cp, k, blockIdx.y * 8 + (threadIdx.x & 7));\n"
           "}\n\n";
     // minimum blocks per SM of the staged K1 (register cap; tuning key k1tc_blocks)
-    const int tcs_blocks = std::atoi(tuning("k1tc_blocks").c_str()) > 0 ? std::atoi(tuning("k1tc_blocks").c_str()) : 3;
+    // (f64 transforms -- mixed precision -- hold the window in twice the registers: no cap there)
+    const int tcs_blocks = std::atoi(tuning("k1tc_blocks").c_str()) > 0 ? std::atoi(tuning("k1tc_blocks").c_str())
+                           : ty.compute_double ? 1 : 3;
     if (staged_k1)  // same grids and arguments as the *_tcg kernels; the host picks by image size
         os << "extern \"C\" __global__ void __launch_bounds__(256, " << tcs_blocks << ") wino_input_tcs(\n"
               "    const in_t* __restrict__ x, unsigned short* __restrict__ V, int C, int H, int W, int pad, int th,\n"
