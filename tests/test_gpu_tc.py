@@ -76,12 +76,12 @@ def test_tc_transforms_write_rounded_operands(mode):
 
 
 @pytest.mark.parametrize("mode", ["tc_bf16", "tc_fp16"])
-@pytest.mark.parametrize("m,pts,geom", [(6, "0,-1,1,1/2,-1/2,2,-2,inf", (3, 13, 37, 41, 9)),
-                                        (6, "0,-1,1,1/2,-1/2,2,-2,inf", (2, 20, 64, 34, 5)),
-                                        (4, "0,1,-1,1/2,-1/2,inf", (2, 9, 40, 40, 7)),
-                                        (6, "0,-1,1,1/2,-1/2,2,-2,inf", (5, 11, 14, 14, 9))],
-                         ids=["a8_37x41", "a8_64x34", "a6_40x40", "a8_14x14_old_map"])
-@pytest.mark.parametrize("prec", ["fp32", "mixed"])
+@pytest.mark.parametrize("m,pts,geom,prec", [(6, "0,-1,1,1/2,-1/2,2,-2,inf", (3, 13, 37, 41, 9), "fp32"),
+                                             (6, "0,-1,1,1/2,-1/2,2,-2,inf", (3, 13, 37, 41, 9), "mixed"),
+                                             (6, "0,-1,1,1/2,-1/2,2,-2,inf", (2, 20, 64, 34, 5), "fp32"),
+                                             (4, "0,1,-1,1/2,-1/2,inf", (2, 9, 40, 40, 7), "fp32"),
+                                             (6, "0,-1,1,1/2,-1/2,2,-2,inf", (5, 11, 14, 14, 9), "fp32")],
+                         ids=["a8_37x41", "a8_37x41_mixed", "a8_64x34", "a6_40x40", "a8_14x14_old_map"])
 def test_tc_staged_input_transform_writes_rounded_operands(mode, m, pts, geom, prec):
     """K1 of the tc modes at 16 < alpha^2 <= 96: images above 32 x 32 take the warp-per-channel kernel that
     parks its 16-bit results in shared memory (wino_input_tcs / wino_transforms_tcs), smaller ones the
@@ -93,8 +93,6 @@ def test_tc_staged_input_transform_writes_rounded_operands(mode, m, pts, geom, p
     ts = W.build_transforms(3, m, W.parse_points(pts))
     x = torch.from_numpy(O.synthetic((N, C, H, Wd), 6, 0)).cuda()
     w = torch.from_numpy(O.synthetic((K, C, 3, 3), 6, 1)).cuda()
-    if prec == "mixed" and geom[2] != 37:
-        pytest.skip("one mixed-precision geometry is enough")
     ex = W.layer_op(ts, W.ConvConfig(prec), N, C, H, Wd, K, 1)
     tc = W.layer_op(ts, W.ConvConfig(prec), N, C, H, Wd, K, 1, contraction=mode)
     dt = torch.bfloat16 if mode == "tc_bf16" else torch.float16
