@@ -400,10 +400,18 @@ def run_gpu(args, cfg):
                 "peak_source": mp["source"] + " hbm copy bandwidth", "bytes_per_launch": fb,
                 "tensor_tflops": ach, "tensor_frac": ach / mp["bf16_tflops"]}
     elif args.contraction.startswith("tc_"):
+        # 2 P T C K flop against 2 P C (T + K) + 4 P K T bytes (16-bit operands read, fp32 M written):
+        # <= 256 flop per byte at C = 512, so the unfused tensor-core contraction is bound by moving M
+        # (through L2 / HBM), not by the tensor pipe; the tensor-peak fraction is reported beside it
         pk = mp["bf16_tflops"]
-        roof = {"kernel": "tc_contract_kernel (tcgen05.mma kind::f16)", "bound": "tensor", "achieved": ach,
-                "peak": pk, "unit": "TFLOP/s", "frac": ach / pk, "traffic": None,
-                "peak_source": mp["source"] + " bf16 dense (burst)"}
+        cb = 2 * L.P * C * (L.T + K) + 4 * L.P * K * L.T
+        gbs = cb / (ms_stage[2] * 1e-3) / 1e9
+        roof = {"kernel": "tc_contract_kernel (tcgen05.mma kind::f16)", "bound": "hbm", "achieved": gbs,
+                "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "traffic": None, "bytes_per_launch": cb,
+                "peak_source": mp["source"] + " hbm copy bandwidth",
+                "bound_note": "algorithmic bytes (U16 + V16 read, fp32 M written); a single small layer's M "
+                              "partly stays in the 126 MB L2",
+                "tensor_tflops": ach, "frac_of_tensor_peak": ach / pk}
     else:
         pk = max(peak["ffma_tflops"], peak.get("ffma2_tflops", 0.0))  # FP32 pipe peak (scalar or packed FFMA)
         # exact modes: every MAC is a separately rounded multiply and add (scalar
@@ -419,10 +427,11 @@ def run_gpu(args, cfg):
                 "frac_of_exact_ceiling_reg": ach / peak["fmul_fadd_reg_tflops"] if exact else None}
     roof.update({"flops_per_launch": flops_c, "share_of_step": float(ms_stage[2] / ms_stage.sum())})
     eb = L.elem_bytes_uv
+    mb = 4 if args.contraction.startswith("tc_") else eb  # tensor-core modes: 16-bit U / V (eb = 2), fp32 M
     stage_bytes = [4 * K * C * r * r + eb * L.P * C * K + 4 * N * C * H * H + eb * L.P * L.T * C,
                    None,
                    None,
-                   eb * L.P * L.T * K + (4 if prec == "fp32" else 8) * N * K * L.Ho * L.Wo]
+                   mb * L.P * L.T * K + (4 if prec == "fp32" else 8) * N * K * L.Ho * L.Wo]
     stages = {}
     if fused:
         stage_bytes[2] = roof["bytes_per_launch"]
