@@ -1361,6 +1361,51 @@ std::string gen_layer_source(int r, int m, const MatProg& G, const MatProg& BT, 
         os << "}\n\n";
     }
 
+    // ---------------- K2, cooperative loads (large filters, r >= 5) ----------------
+    // filter_body's r^2 loads each touch 32 different lines (consecutive threads are consecutive k, and
+    // filters are C r^2 floats apart): at r = 5 the kernel is bound by L1 line requests, not bytes
+    // (cfg4: 35 of the 55.6 us of K1 + K2).  Here the block first copies its 128 filters' r^2 weights to
+    // shared memory with consecutive lanes on consecutive floats of a filter (about four lines per load
+    // instruction), then every thread transforms its own filter from there (row stride r^2 | 1: no bank
+    // conflicts).  Same arithmetic, same stores.  Grid (ceil(Kp / 128), Cp).
+    if (128 * ((r * r) | 1) * (ty.in_double ? 8 : 4) <= 48 * 1024) {  // static shared memory (host: k2_coop())
+        const int RR = r * r, RS = RR | 1;
+        os << "extern \"C\" __global__ void __launch_bounds__(128) wino_filter_coop(\n"
+              "    const in_t* __restrict__ w, uv_t* __restrict__ U, int K, int C, long long Kp, long long Cp) {\n"
+           << "  __shared__ in_t fw[128 * " << RS << "];\n"
+              "  const int k0 = blockIdx.x * 128, c = blockIdx.y, tid = threadIdx.x;\n"
+              "  if (c < C) {\n"
+              "#pragma unroll\n"
+           << "    for (int q = 0; q < " << RR << "; ++q) {\n"
+           << "      const int e = q * 128 + tid, ch = e / " << RR << ", off = e - ch * " << RR << ";\n"
+           << "      fw[ch * " << RS << " + off] = k0 + ch < K ? __ldg(w + ((long long)(k0 + ch) * C + c) * " << RR
+           << " + off) : (in_t)0;\n"
+              "    }\n"
+              "  }\n"
+              "  __syncthreads();\n"
+              "  const int k = k0 + tid;\n"
+              "  if (k >= Kp) return;\n"
+              "  const long long plane = Cp * Kp;\n"
+           << "  uv_t* o = U + ((long long)(k / " << bm << ") * Cp + c) * " << bm << " + (k % " << bm << ");\n"
+              "  if (k >= K || c >= C) {\n"
+              "#pragma unroll 1\n"
+           << "    for (int p = 0; p < " << P << "; ++p) o[p * plane] = (uv_t)0;\n"
+              "    return;\n  }\n";
+        std::vector<std::vector<std::string>> h(r, std::vector<std::string>(r));
+        for (int a = 0; a < r; ++a)
+            for (int b = 0; b < r; ++b) {
+                h[a][b] = "g" + std::to_string(a) + "_" + std::to_string(b);
+                os << "  const ct_t " << h[a][b] << " = (ct_t)fw[tid * " << RS << " + " << a * r + b << "];\n";
+            }
+        Emitter em(os, ty.compute_double, ctr);
+        auto u = em.apply2d(G, h);
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j)
+                os << "  o[" << (i * n + j) << " * plane] = " << store_cvt(ty.compute_double, ty.uv_double, u[i][j])
+                   << ";\n";
+        os << "}\n\n";
+    }
+
     // ---------------- K1 body: V[p][t/bn][c][t%bn] = (B^T d B)[p] ------------
     // Each thread transforms one (tile, channel) window gathered from x (zero
     // padding fused; interior windows take an unpredicated fast path), parks its

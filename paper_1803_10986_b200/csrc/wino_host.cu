@@ -697,6 +697,14 @@ bool k1tc_staged(int P, const wino_layer_shape* s) {
     return e == "2" || (long long)s->H * s->W > 32 * 32;
 }
 
+// K2 with cooperative weight loads (codegen.cpp wino_filter_coop): filters of 5 x 5 and larger, where the
+// per-thread loads are bound by L1 line requests (cfg4 K1 + K2 55.6 -> 46.0 us); its staging buffer is
+// static shared memory, so it exists only while 128 (r^2 | 1) input elements fit 48 KB
+bool k2_coop(const wino_plan* p) {
+    return p->r >= 5 && wino::tuning("k2coop") != "0" &&
+           128 * ((p->r * p->r) | 1) * (p->ty.in_double ? 8 : 4) <= 48 * 1024;
+}
+
 bool k1_no8() {  // WINO_K1TC=4x8: use the 4-tiles x 8-channels TC kernel also for P <= 16
     static const bool v = [] {
         const std::string es = wino::tuning("k1tc");
@@ -754,7 +762,7 @@ const char* wino_last_error(void) { return wino::g_last_error.c_str(); }
 
 int wino_tuning_set(const char* key, const char* value) {
     static const char* const keys[] = {"gemm", "dbuf", "k1", "k1order", "k4", "k1tc", "tile_interp",
-                                       "cpt", "kpt", "tcf_nk", "tcf_dbg", "tc_epi", "k1rowwise", "k4rowwise", "sc2_kg", "k4k1_ks", "k1st_blocks", "k1_blocks", "k4_blocks", "k1tc_staged", "k1tc_blocks", "tc_epw"};
+                                       "cpt", "kpt", "tcf_nk", "tcf_dbg", "tc_epi", "k1rowwise", "k4rowwise", "sc2_kg", "k4k1_ks", "k1st_blocks", "k1_blocks", "k4_blocks", "k1tc_staged", "k1tc_blocks", "tc_epw", "k2coop"};
     if (!key) return wino::fail(WINO_EINVAL, "tuning_set: null key");
     bool known = false;
     for (const char* k : keys) known = known || std::strcmp(k, key) == 0;
@@ -998,6 +1006,13 @@ int wino_filter_transform(wino_plan* plan, const wino_layer_shape* s, const void
                             "filter_transform");
     }
     if (plan->fused()) return wino::fail(WINO_EUNSUPPORTED, "filter_transform: grid too large for the fused layout");
+    if (plan->mode < WINO_CONTRACT_TC_BF16 && k2_coop(plan) && Cp <= 65535) {
+        // large filters: cooperative weight loads through shared memory (codegen.cpp wino_filter_coop)
+        if ((rc = plan->layer_mod(plan->pick(s))->function("wino_filter_coop", &f))) return rc;
+        void* args[] = {(void*)&w, &U, &K, &C, &Kp, &Cp};
+        return wino::launch(f, dim3((unsigned)cdiv(Kp, 128), (unsigned)Cp, 1), dim3(128), 0, stream, args,
+                            "filter_transform");
+    }
     if ((rc = plan->layer_mod(plan->pick(s))->function("wino_filter_xform", &f))) return rc;
     int smem = 0;
     const int tb = plan->mode >= WINO_CONTRACT_TC_BF16 ? 64 : xform_block(plan, &smem);
@@ -1065,10 +1080,25 @@ static int transforms_impl(wino_plan* plan, const wino_layer_shape* s, const voi
         CUfunction fg;
         unsigned st_smem = 0;
         const bool st = k1_staged(plan, s, L, x, tb, &st_smem);
+        float rtw = 1.0f / tw, rth = 1.0f / th;
+        if (k2_coop(plan) && Cp <= 65535) {
+            // large filters: K2 as its own kernel with cooperative weight loads (codegen.cpp wino_filter_coop:
+            // cfg4 K2 35 -> see profiles/r2_experiments.md), then K1 alone
+            CUfunction fk;
+            if ((rc = plan->layer_mod(plan->pick(s))->function("wino_filter_coop", &fk))) return rc;
+            void* kargs[] = {(void*)&w, &U, &K, &C, &Kp, &Cp};
+            if ((rc = wino::launch(fk, dim3((unsigned)cdiv(Kp, 128), (unsigned)Cp), dim3(128), 0, stream, kargs,
+                                   "filter_transform")))
+                return rc;
+            if ((rc = plan->layer_mod(plan->pick(s))->function(st ? "wino_input_gather_st" : "wino_input_gather", &fg)))
+                return rc;
+            void* iargs[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &Wl, &rtw, &rth};
+            return wino::launch(fg, dim3((unsigned)(Cp / wino::gather_cpt(L.P)), (unsigned)n_tb), dim3(tb),
+                                st ? st_smem : 0, stream, iargs, "input_transform");
+        }
         if ((rc = plan->layer_mod(plan->pick(s))->function(st ? "wino_transforms_gather_st" : "wino_transforms_gather",
                                                            &fg)))
             return rc;
-        float rtw = 1.0f / tw, rth = 1.0f / th;
         void* args[] = {(void*)&x, &V, &C, &H, &W, &pad, &th, &tw, &T, &Tp, &Cp, &n_tb, (void*)&w, &U, &K, &Kp,
                         &Wl, &rtw, &rth};
         return wino::launch(fg, dim3((unsigned)(Cp / wino::gather_cpt(L.P)), (unsigned)(n_tb + n_kb)), dim3(tb),
