@@ -956,6 +956,10 @@ int wino_plan_prepare(wino_plan* plan, const wino_layer_shape* s, int flags) {
     if (flags & WINO_PREPARE_CONV) {
         work.push_back({lm, k1_gather() && n_tb + n_kb <= 65535 && L.Cp <= 65535 ? "wino_transforms_gather"
                                                                                   : "wino_transforms"});
+        if (k2_coop(plan) && k1_gather() && L.Cp <= 65535) {  // r >= 5: K2 and K1 are two launches
+            work.push_back({lm, "wino_filter_coop"});
+            work.push_back({lm, "wino_input_gather"});
+        }
         work.push_back({plan->contract_module(L.Cp, ci), "wino_contract"});
         work.push_back({lm, k4_gather() && s->K <= 65535 ? "wino_output_gather"
                             : plan->m <= 2               ? "wino_output_flat"
